@@ -1,0 +1,132 @@
+/*
+ * prrp_b200.h — C ABI of the B200 (sm_100a) LU_PRRP / CALU_PRRP library.
+ *
+ * Drop-in boundary for the reference package `prrp` (arXiv 1208.2451
+ * reference, /root/reference/pkg/src/prrp).  The reference is pure Python, so
+ * its "FFI" is its public Python API; each entry point below replaces the
+ * numpy work behind one of those functions (file:line cited per function).
+ * The Python mirror package `paper_1208_2451_b200` binds these with ctypes
+ * (INTEGRATION.md shows the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *  - All matrix pointers are DEVICE pointers to float64.  The factorization
+ *    matrix is ROW-MAJOR, element (i, j) at A[i*lda + j], lda >= n, lda even
+ *    (16-byte row pitch for the TMA descriptors).  The result is stored in
+ *    place as the packed L\U of the reference's BlockLUFactors: unit lower L
+ *    strictly below the diagonal, U on and above it (luprrp.py:81-87 keeps
+ *    them as separate arrays; the Python shim splits them).
+ *  - perm is a DEVICE int64 array of length m: row i of the factored matrix
+ *    is row perm[i] of the input (matcore.apply_row_perm, matcore.py:152-159).
+ *  - Small outputs (stats, error record, swap counts) are HOST pointers;
+ *    the call synchronizes the stream before returning them.
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy
+ *    default stream.  Calls are stream-ordered and keep no global mutable
+ *    state besides a per-process cache of kernel attributes.
+ *  - Return value: PRRP_OK or one of the status codes below; the error
+ *    record carries the payload the reference attaches to its exceptions.
+ */
+#ifndef PRRP_B200_H
+#define PRRP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; each maps onto the reference's exception contract
+ * (errors.py:4-54, luprrp.py:143-150). */
+enum prrp_status {
+  PRRP_OK = 0,
+  PRRP_ERR_DIM = 1,              /* DimensionMismatch (errors.py:4-5)              */
+  PRRP_ERR_ARG = 2,              /* ValueError: b out of range, tau <= 1, ...       */
+  PRRP_ERR_RANK_DEFICIENT = 3,   /* RankDeficient(index)   (errors.py:30-38)        */
+  PRRP_ERR_NONCONVERGENCE = 4,   /* NonConvergence(worst)  (errors.py:41-50)        */
+  PRRP_ERR_SINGULAR_MATRIX = 5,  /* SingularMatrix(column) (errors.py:19-27)        */
+  PRRP_ERR_SINGULAR_FACTOR = 6,  /* SingularFactor(index)  (errors.py:8-16)         */
+  PRRP_ERR_CUDA = 7,             /* CUDA runtime failure (message in err->msg)      */
+  PRRP_ERR_UNSUPPORTED = 8,      /* shape outside the device path (e.g. b > 128)    */
+  PRRP_ERR_NCCL = 9
+};
+
+/* Error payload: the attributes the reference sets on its exceptions
+ * (exc.index / exc.column / exc.worst, exc.panel at luprrp.py:172-174,192-194,
+ * exc.tree_node at tournament.py:182-184). */
+typedef struct prrp_err {
+  int32_t code;        /* prrp_status                                       */
+  int32_t panel;       /* panel index, -1 if not attached                   */
+  int32_t index;       /* RankDeficient / SingularFactor index, else -1     */
+  int32_t column;      /* SingularMatrix column, else -1                    */
+  int32_t tree_level;  /* CALU tournament node, -1 if none                  */
+  int32_t tree_index;
+  double worst;        /* NonConvergence: largest multiplier still > tau    */
+  char msg[160];
+} prrp_err;
+
+/* ElimStats scalars (luprrp.py:33-78).  Flop counters are exact rationals in
+ * the reference; the shim rebuilds them on the host from swap_counts. */
+typedef struct prrp_stats {
+  double original_max;
+  double intermediate_max;
+  double finish_max;
+  double panel_multiplier_max;
+  int64_t total_swaps;
+} prrp_stats;
+
+/* Library identification: returns the ABI version (major*100 + minor). */
+int prrp_b200_abi_version(void);
+
+/* Probe the device: writes SM count and whether 16-CTA clusters are
+ * available; returns PRRP_OK or PRRP_ERR_CUDA. */
+int prrp_b200_device_probe(int32_t* sm_count, int32_t* max_cluster, prrp_err* err);
+
+/* LU_PRRP factorization, Algorithm 1 — replaces prrp.luprrp_factor
+ * (luprrp.py:153-201).  A: m x n row-major device matrix (m >= n), factored
+ * in place into packed L\U.  perm: device int64[m].  swap_counts: host
+ * int32[ceil(n/b)] (ElimStats.swap_counts).  Requires 1 <= b <= min(n,128)
+ * for the device panel engine (b > 128 returns PRRP_ERR_UNSUPPORTED). */
+int prrp_luprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
+                int64_t* perm, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
+                void* stream);
+
+/* CALU_PRRP factorization with a binary tournament tree of `leaf_count`
+ * leaves — replaces prrp.caluprrp_factor(a, b, tau, binary_tree(P))
+ * (tournament.py:237-296).  Arguments as prrp_luprrp. */
+int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
+                  int32_t leaf_count, int64_t* perm, int32_t* swap_counts,
+                  prrp_stats* stats, prrp_err* err, void* stream);
+
+/* Strong RRQR of an h x p matrix `a` (column-major, lda >= h) with leading
+ * block size bsel <= h and threshold tau — replaces prrp.strong_rrqr
+ * (pivoted_qr.py:113-147).  Outputs (device, column-major): R h x p (ldr=h),
+ * Q h x h, perm int64[p], Lblk (p-bsel) x bsel.  swap_count: host int32.
+ * Requires h <= 128, p >= bsel+1, h >= bsel. */
+int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t bsel,
+                     double tau, double* R, double* Q, int64_t* perm, double* Lblk,
+                     int32_t* swap_count, prrp_err* err, void* stream);
+
+/* Unpivoted Householder QR of an h x p column-major matrix — replaces
+ * prrp.householder_qr (pivoted_qr.py:64-71).  R h x p, Q h x h (device). */
+int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p,
+                        double* R, double* Q, prrp_err* err, void* stream);
+
+/* Rank-K Schur update C <- C - L*B with the reference's rounding recipe
+ * (matcore.rank_update, matcore.py:54-61: product accumulated in increasing
+ * k from zero, then one subtraction).  C: M x N row-major (ldc), L: M x K
+ * column-major (ldl), B: K x N row-major (ldb).  absmax (host, may be NULL)
+ * receives max|C_new|.  K must be a multiple of 4, <= 128. */
+int prrp_schur_update(double* C, int64_t ldc, const double* L, int64_t ldl,
+                      const double* B, int64_t ldb, int64_t M, int64_t N, int32_t K,
+                      double* absmax, prrp_err* err, void* stream);
+
+/* Partial-pivoting LU of an m x n row-major device matrix in place —
+ * replaces prrp.gepp_factor (gepp.py:39-65) for the b x w block-row shapes
+ * the factorizations use (m <= 128).  perm: device int64[m];
+ * intermediate_max: host double. */
+int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* perm,
+                       double* intermediate_max, prrp_err* err, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRRP_B200_H */

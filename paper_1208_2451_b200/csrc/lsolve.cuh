@@ -1,0 +1,349 @@
+// Multiplier block L21 = (R11^-1 R12)^T, the strong-RRQR tau test and swap
+// loop, and the partial-pivoting finish of the b x b diagonal block.
+//
+// Reference semantics:
+//   matcore.trsm_upper      matcore.py:78-94   axpy back substitution from the
+//                           last row, TRUE division x_i /= u_ii, then
+//                           x_l -= u_li * x_i (product, then subtraction);
+//                           exact-zero diagonal -> SingularFactor(index)
+//   pivoted_qr._check_rank  pivoted_qr.py:101-105  |R[k,k]| < 2^-52 ||A||_F
+//   pivoted_qr.strong_rrqr  pivoted_qr.py:113-147  while max|lt| > tau: swap
+//                           the row-major first argmax (i, j) -> perm[i] <->
+//                           perm[b+j], QR from scratch, re-check; cap
+//                           ceil(2 b log p / log tau) + 10 (swap_cap :108-110)
+//   gepp.gepp_factor        gepp.py:39-65   first-max pivot in column k,
+//                           SingularMatrix(column) on an exact zero, true
+//                           division, product-then-subtract rank-1 update,
+//                           running max of the trailing block after each step
+// Every operation above is reproduced element for element, so given the same
+// R (resp. the same block) the outputs are bit-identical to the reference.
+#pragma once
+#include "panel.cuh"
+
+#define TRSM_TW 128   // columns (threads) per trsm block
+
+// packed upper triangle of R11, column q holds rows 0..q
+__device__ __forceinline__ int upk(int i, int q) { return q * (q + 1) / 2 + i; }
+
+__device__ void load_r11(const double* Rbuf, int64_t p, int bsel, double* r11) {
+  for (int idx = threadIdx.x; idx < bsel * bsel; idx += blockDim.x) {
+    const int i = idx / bsel, q = idx % bsel;
+    if (i <= q) r11[upk(i, q)] = Rbuf[(int64_t)i * p + q];
+  }
+}
+
+// Rank check then singular-diagonal check (in the reference's order).
+// Returns 0 when the block is usable.
+__device__ int r11_checks(const double* r11, int bsel, double fro, DevState* st, int panel, bool report) {
+  for (int k = 0; k < bsel; ++k) {
+    if (fabs(r11[upk(k, k)]) < PRRP_EPS * fro) {
+      if (report) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, k, -1, 0.0);
+      return 1;
+    }
+  }
+  for (int i = bsel - 1; i >= 0; --i) {
+    if (r11[upk(i, i)] == 0.0) {
+      if (report) prrp_set_error(st, PRRP_ERR_SINGULAR_FACTOR, panel, i, -1, 0.0);
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// Solve R11 x = R12[:, pos] for the positions [q0, q0 + blockDim.x) and write
+// L21 (column-major, row pos - bsel).  Tracks the worst |x| with its
+// row-major flat index in lt = R11^-1 R12 (bsel x (p - bsel)).
+__device__ void trsm_tile(const double* Rbuf, int64_t p, int bsel, const double* r11, double* xs, int TW,
+                          int64_t q0, double* L21, int64_t ldl, double& worst, long long& wflat) {
+  const int t = threadIdx.x;
+  const int64_t pos = q0 + t;
+  const bool on = t < TW && pos < p;
+  if (on)
+    for (int i = 0; i < bsel; ++i) xs[i * TW + t] = Rbuf[(int64_t)i * p + pos];
+  if (!on) return;
+  for (int i = bsel - 1; i >= 0; --i) {
+    const double xi = div_rn(xs[i * TW + t], r11[upk(i, i)]);
+    xs[i * TW + t] = xi;
+    const double* rc = r11 + upk(0, i);
+    for (int l = 0; l < i; ++l) xs[l * TW + t] = sub_rn(xs[l * TW + t], mul_rn(rc[l], xi));
+  }
+  const int64_t jj = pos - bsel;
+  const int64_t ncol = p - bsel;
+  for (int i = 0; i < bsel; ++i) {
+    const double x = xs[i * TW + t];
+    L21[(int64_t)i * ldl + jj] = x;
+    const double ax = fabs(x);
+    const long long fl = (long long)i * ncol + jj;
+    if (ax > worst || (ax == worst && fl < wflat)) { worst = ax; wflat = fl; }
+  }
+}
+
+__device__ void reduce_worst(double& worst, long long& wflat, double* red_d, long long* red_l) {
+  for (int o = 16; o; o >>= 1) {
+    const double ow = __shfl_xor_sync(0xffffffffu, worst, o);
+    const long long of = __shfl_xor_sync(0xffffffffu, wflat, o);
+    if (ow > worst || (ow == worst && of < wflat)) { worst = ow; wflat = of; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) { red_d[w] = worst; red_l[w] = wflat; }
+  __syncthreads();
+  if (w == 0) {
+    worst = l < nw ? red_d[l] : -1.0;
+    wflat = l < nw ? red_l[l] : LLONG_MAX;
+    for (int o = 16; o; o >>= 1) {
+      const double ow = __shfl_xor_sync(0xffffffffu, worst, o);
+      const long long of = __shfl_xor_sync(0xffffffffu, wflat, o);
+      if (ow > worst || (ow == worst && of < wflat)) { worst = ow; wflat = of; }
+    }
+    if (l == 0) { red_d[32] = worst; red_l[32] = wflat; }
+  }
+  __syncthreads();
+  worst = red_d[32];
+  wflat = red_l[32];
+}
+
+// All-SM multiplier kernel (fast path): block b solves positions
+// [bsel + b*TW, ...).  Block 0 performs the rank / singular checks.
+__global__ void __launch_bounds__(TRSM_TW) trsm_kernel(const double* Rbuf, int64_t p, int bsel, double* L21,
+                                                      int64_t ldl, double* cand, long long* cand_flat,
+                                                      DevState* st, int panel) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red_d[33];
+  __shared__ long long red_l[33];
+  if (prrp_failed(st)) return;
+  double* r11 = sm;
+  double* xs = sm + bsel * (bsel + 1) / 2;
+  load_r11(Rbuf, p, bsel, r11);
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, st->fro, st, panel, true);
+  double worst = -1.0;
+  long long wflat = LLONG_MAX;
+  trsm_tile(Rbuf, p, bsel, r11, xs, blockDim.x, bsel + (int64_t)blockIdx.x * blockDim.x, L21, ldl, worst, wflat);
+  reduce_worst(worst, wflat, red_d, red_l);
+  if (threadIdx.x == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
+}
+
+// ---------------------------------------------------------------------------
+// GEPP of the b x b diagonal block (gepp.py:39-65 restricted to the block's
+// columns; the trailing columns of the block row are finished per column by
+// blockrow_kernel with the same multipliers and pivots).
+// src row q of the block: src + (rowmap ? rowmap[q] : q) * ld, b entries.
+// Output: D (b x b row-major packed L\U), piv[k] (row exchanged at step k),
+// gperm (final order of the block rows).  Single CTA.
+// ---------------------------------------------------------------------------
+__device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, int b, double* c /* smem b*b */,
+                          double* D, int32_t* piv, int32_t* gperm, DevState* st, int panel, double* red) {
+  const int t = threadIdx.x, T = blockDim.x;
+  __shared__ int s_piv;
+  __shared__ double s_colmax;
+  __shared__ int s_gp[PRRP_MAXH];
+  double mx = 0.0;
+  for (int idx = t; idx < b * b; idx += T) {
+    const int i = idx / b, j = idx % b;
+    const int64_t row = rowmap ? rowmap[i] : i;
+    const double v = src[row * ld + j];
+    c[idx] = v;
+    mx = fmax(mx, fabs(v));
+  }
+  if (t < b) s_gp[t] = t;
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    if (t < 32) {
+      double best = -1.0;
+      int bi = INT_MAX;
+      for (int i = k + t; i < b; i += 32) {
+        const double v = fabs(c[i * b + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (t == 0) { s_piv = bi; s_colmax = best; }
+    }
+    __syncthreads();
+    const int pv = s_piv;
+    if (s_colmax == 0.0) {
+      if (t == 0) prrp_set_error(st, PRRP_ERR_SINGULAR_MATRIX, panel, -1, k, 0.0);
+      return;
+    }
+    if (pv != k) {
+      for (int j = t; j < b; j += T) {
+        const double x = c[k * b + j];
+        c[k * b + j] = c[pv * b + j];
+        c[pv * b + j] = x;
+      }
+      if (t == 0) { const int g = s_gp[k]; s_gp[k] = s_gp[pv]; s_gp[pv] = g; }
+    }
+    if (t == 0) piv[k] = pv;
+    __syncthreads();
+    if (k + 1 < b) {
+      const double ckk = c[k * b + k];
+      for (int i = k + 1 + t; i < b; i += T) c[i * b + k] = div_rn(c[i * b + k], ckk);
+      __syncthreads();
+      const int w = b - k - 1;
+      for (int idx = t; idx < w * w; idx += T) {
+        const int i = k + 1 + idx / w, j = k + 1 + idx % w;
+        const double v = sub_rn(c[i * b + j], mul_rn(c[i * b + k], c[k * b + j]));
+        c[i * b + j] = v;
+        mx = fmax(mx, fabs(v));
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = t; idx < b * b; idx += T) D[idx] = c[idx];
+  if (t < b) gperm[t] = s_gp[t];
+  const double m = block_max(mx, red);
+  if (t == 0) atomic_max_abs(&st->finish_max, m);
+}
+
+__global__ void __launch_bounds__(1024) gepp_diag_kernel(const double* src, int64_t ld, int b, double* D,
+                                                          int32_t* piv, int32_t* gperm, DevState* st, int panel) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  gepp_diag(src, ld, nullptr, b, sm, D, piv, gperm, st, panel, red);
+}
+
+// ---------------------------------------------------------------------------
+// Finalize a panel after the fast multiplier kernel: reduce the candidates,
+// run the strong-RRQR swap loop if the tau bound is violated (rare; QR from
+// scratch + multipliers inside the cluster), record the swap count and the
+// multiplier max, compact the moved-row list and factor the diagonal block.
+// ---------------------------------------------------------------------------
+struct FinalizeArgs {
+  PanelArgs pa;
+  int swap_cap;
+  double* D;
+  int32_t* piv;
+  int32_t* gperm;
+  int32_t* swaps_dev;     // per-panel swap counts (device)
+  int do_gepp;
+};
+
+__global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f) {
+  extern __shared__ __align__(16) double dyn_smem[];
+  __shared__ PanelShared S;
+  __shared__ double red_d[33];
+  __shared__ long long red_l[33];
+  __shared__ double s_worst;
+  __shared__ long long s_flat;
+  __shared__ int s_cnt[33];
+  cg::cluster_group cl = cg::this_cluster();
+  const PanelArgs& a = f.pa;
+  if (prrp_failed(a.st)) return;
+  const int c = (int)cl.block_rank(), C = (int)cl.num_blocks();
+  const int t = threadIdx.x;
+
+  // reduce the fast-path candidates
+  double worst = -1.0;
+  long long wflat = LLONG_MAX;
+  for (int i = t; i < a.ncand; i += blockDim.x) {
+    const double w = a.cand[i];
+    const long long fl = a.cand_flat[i];
+    if (w > worst || (w == worst && fl < wflat)) { worst = w; wflat = fl; }
+  }
+  reduce_worst(worst, wflat, red_d, red_l);
+
+  int swaps = 0;
+  const int64_t ncol = a.p - a.bsel;
+  while (ncol > 0 && worst > a.tau) {
+    if (swaps >= f.swap_cap) {
+      if (c == 0 && t == 0) prrp_set_error(a.st, PRRP_ERR_NONCONVERGENCE, a.panel_id, -1, -1, worst);
+      return;
+    }
+    const int i = (int)(wflat / ncol);
+    const int64_t jj = wflat % ncol;
+    cl.sync();
+    if (c == 0 && t == 0) {
+      const int32_t x = a.perm[i];
+      a.perm[i] = a.perm[a.bsel + jj];
+      a.perm[a.bsel + jj] = x;
+    }
+    cl.sync();
+    engine_run(a, 1, a.perm, dyn_smem, S);
+    cl.sync();
+    // rank check + multipliers over this cluster
+    double* r11 = dyn_smem;
+    double* xs = dyn_smem + a.bsel * (a.bsel + 1) / 2;
+    load_r11(a.Rbuf, a.p, a.bsel, r11);
+    __syncthreads();
+    if (r11_checks(r11, a.bsel, a.st->fro, a.st, a.panel_id, c == 0 && t == 0)) return;
+    worst = -1.0;
+    wflat = LLONG_MAX;
+    const int TW = a.bsel > 64 ? 64 : 128;
+    const int64_t ntile = (ncol + TW - 1) / TW;
+    for (int64_t tile = c; tile < ntile; tile += C) {
+      trsm_tile(a.Rbuf, a.p, a.bsel, r11, xs, TW, a.bsel + tile * TW, a.L21, a.ldl, worst, wflat);
+      __syncthreads();
+    }
+    reduce_worst(worst, wflat, red_d, red_l);
+    if (t == 0) { S.red[0] = worst; S.rec[0].pos = wflat; }
+    cl.sync();
+    if (t < 32) {
+      double w = -1.0;
+      long long fl = LLONG_MAX;
+      if (t < C) {
+        w = *cl.map_shared_rank(&S.red[0], t);
+        fl = cl.map_shared_rank(&S.rec[0], t)->pos;
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ow = __shfl_xor_sync(0xffffffffu, w, o);
+        const long long of = __shfl_xor_sync(0xffffffffu, fl, o);
+        if (ow > w || (ow == w && of < fl)) { w = ow; fl = of; }
+      }
+      if (t == 0) { s_worst = w; s_flat = fl; }
+    }
+    __syncthreads();
+    worst = s_worst;
+    wflat = s_flat;
+    ++swaps;
+  }
+  cl.sync();
+  if (c != 0) return;
+
+  if (t == 0) {
+    f.swaps_dev[a.panel_id] = swaps;
+    a.st->swaps = swaps;
+    if (ncol > 0) atomic_max_abs(&a.st->pmm, worst);
+  }
+  // compact the moved positions (pos -> src j with j != pos), deterministic order
+  {
+    const int T = blockDim.x;
+    const int64_t per_t = (a.p + T - 1) / T;
+    const int64_t lo = t * per_t, hi = min(a.p, lo + per_t);
+    int cnt = 0;
+    for (int64_t q = lo; q < hi; ++q) cnt += a.perm[q] != q;
+    // block exclusive scan of cnt
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((t & 31) >= o) incl += y;
+    }
+    if ((t & 31) == 31) s_cnt[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+      const int nw = (T + 31) >> 5;
+      int v = t < nw ? s_cnt[t] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (t >= o) v += y;
+      }
+      s_cnt[t] = v;   // inclusive per-warp totals
+    }
+    __syncthreads();
+    int off = incl - cnt + ((t >> 5) ? s_cnt[(t >> 5) - 1] : 0);
+    for (int64_t q = lo; q < hi; ++q) {
+      const int32_t j = a.perm[q];
+      if (j != q) { a.moved[2 * off] = (int32_t)q; a.moved[2 * off + 1] = j; ++off; }
+    }
+    if (t == blockDim.x - 1) a.st->moved = off;
+  }
+  __syncthreads();
+  if (f.do_gepp) {
+    __shared__ double red[40];
+    gepp_diag(a.src, a.ld, a.perm, a.h, dyn_smem, f.D, f.piv, f.gperm, a.st, a.panel_id, red);
+  }
+}

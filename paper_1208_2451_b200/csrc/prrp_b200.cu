@@ -1,0 +1,621 @@
+// C-ABI entry points and the stream-ordered host driver of the B200 LU_PRRP /
+// CALU_PRRP library (see include/prrp_b200.h for the contract).
+//
+// Per panel (luprrp.py:164-199) the driver launches:
+//   panel_qrcp_kernel      cluster: QRCP of the transposed panel (strong RRQR step 1)
+//   trsm_kernel            all SMs: L21 = (R11^-1 R12)^T, rank check, tau candidates
+//   panel_finalize_kernel  cluster: swap loop if needed, moved rows, GEPP of A11
+//   permute_kernel         all SMs: move the <= 2b permuted rows
+//   schur_dmma_kernel      all SMs: A22 -= L21 A12 (TMA + DMMA), growth max
+//   compose_kernel         all SMs: L21 <- L21[:, perm] L11 into the L part
+//   blockrow_kernel        all SMs: GEPP finish of the block row, finish max
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <vector>
+#include <algorithm>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "panel.cuh"
+#include "lsolve.cuh"
+#include "rowops.cuh"
+#include "schur.cuh"
+
+namespace {
+
+constexpr int kAbiVersion = 100;
+constexpr size_t kSmemOptin = 227 * 1024;
+
+struct Fail {
+  int code;
+  char msg[160];
+};
+
+#define CU_TRY(expr)                                                             \
+  do {                                                                           \
+    cudaError_t e__ = (expr);                                                    \
+    if (e__ != cudaSuccess) {                                                    \
+      Fail f__{PRRP_ERR_CUDA, {0}};                                              \
+      snprintf(f__.msg, sizeof(f__.msg), "%s: %s (%s:%d)", #expr,                \
+               cudaGetErrorString(e__), __FILE__, __LINE__);                     \
+      throw f__;                                                                 \
+    }                                                                            \
+  } while (0)
+
+void fail(int code, const char* msg) {
+  Fail f{code, {0}};
+  snprintf(f.msg, sizeof(f.msg), "%s", msg);
+  throw f;
+}
+
+void clear_err(prrp_err* err) {
+  if (!err) return;
+  memset(err, 0, sizeof(*err));
+  err->panel = err->index = err->column = err->tree_level = err->tree_index = -1;
+}
+
+int report(prrp_err* err, const Fail& f) {
+  if (err) {
+    err->code = f.code;
+    snprintf(err->msg, sizeof(err->msg), "%s", f.msg);
+  }
+  return f.code;
+}
+
+// ---------------------------------------------------------------- device probe
+struct DeviceCaps {
+  bool init = false;
+  int sms = 0;
+  int max_cluster = 8;
+};
+
+DeviceCaps& caps() {
+  static DeviceCaps c;
+  if (!c.init) {
+    int dev = 0;
+    CU_TRY(cudaGetDevice(&dev));
+    CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+    for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel}) {
+      CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
+    }
+    CU_TRY(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptin));
+    CU_TRY(cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 16 * 1024)));
+    CU_TRY(cudaFuncSetAttribute(blockrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
+    CU_TRY(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
+    CU_TRY(cudaFuncSetAttribute(gepp_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
+    CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
+    // largest cluster the panel engine can get with a full shared-memory CTA per SM
+    for (int cs : {16, 8}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = kSmemOptin - 16 * 1024;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, (void*)panel_qrcp_kernel, &cfg) == cudaSuccess && ncl > 0) {
+        c.max_cluster = cs;
+        break;
+      }
+      cudaGetLastError();
+    }
+    c.init = true;
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) fail(PRRP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2-D FP64 map: `inner` contiguous elements, `outer` lines `pitch` elements apart; box {8, KC}
+CUtensorMap make_map(const double* base, uint64_t inner, uint64_t outer, uint64_t pitch) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch * 8};
+  cuuint32_t box[2] = {8, SCH_KC};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(PRRP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+// ---------------------------------------------------------------- workspace
+struct Arena {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t st) : s(st) {}
+  template <typename T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    CU_TRY(cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), s));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+// ---------------------------------------------------------------- launches
+struct PanelCfg {
+  int C, T;
+  int64_t per;
+  int cap, cap_pad;
+  int64_t ovpad;
+  size_t dyn_engine, dyn_final;
+};
+
+PanelCfg panel_config(int h, int64_t p, int bsel) {
+  PanelCfg g{};
+  const int maxc = caps().max_cluster;
+  g.C = (int)std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 127) / 128));
+  g.per = (p + g.C - 1) / g.C;
+  if (g.per > (int64_t)PRRP_MAXCPT * 1024) fail(PRRP_ERR_UNSUPPORTED, "panel too tall for the cluster engine");
+  g.T = (int)std::min<int64_t>(1024, std::max<int64_t>(32, ((std::min<int64_t>(g.per, 1024) + 31) / 32) * 32));
+  while ((int64_t)g.T * PRRP_MAXCPT < g.per) g.T += 32;
+  const size_t budget = kSmemOptin - 16 * 1024 - sizeof(PanelShared);
+  int64_t maxcols = (int64_t)(budget / ((size_t)h * 8));
+  if (maxcols % 2 == 0) --maxcols;
+  g.cap = (int)std::min<int64_t>(g.per, maxcols);
+  g.cap_pad = g.cap | 1;
+  g.ovpad = std::max<int64_t>(0, g.per - g.cap);
+  g.dyn_engine = (size_t)g.cap_pad * h * 8;
+  const int tw = bsel > 64 ? 64 : 128;
+  const size_t trsm_need = ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8;
+  const size_t gepp_need = (size_t)h * h * 8;
+  g.dyn_final = std::max({g.dyn_engine, trsm_need, gepp_need});
+  return g;
+}
+
+template <typename K, typename... Args>
+void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.C);
+  cfg.blockDim = dim3(g.T);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
+int swap_cap(int b, int64_t p, double tau) {   // pivoted_qr.py:108-110
+  return (int)std::ceil(2.0 * b * std::log((double)std::max<int64_t>(p, 2)) / std::log(tau)) + 10;
+}
+
+struct PanelBuffers {
+  double* Rbuf;
+  int32_t* perm;
+  double* ovf;
+  double* cand;
+  long long* cand_flat;
+  int32_t* moved;
+  double* refl;
+};
+
+// One strong RRQR of the h x p transposed panel: QRCP (cluster), multipliers
+// (all SMs), swap loop + moved rows (+ optional GEPP of the pivot block).
+void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel, double tau, int panel,
+                       double* L21, int64_t ldl, const PanelBuffers& B, DevState* st, int32_t* swaps_dev,
+                       double* D, int32_t* piv, int32_t* gperm, bool do_gepp, cudaStream_t s) {
+  const PanelCfg g = panel_config(h, p, bsel);
+  PanelArgs a{};
+  a.src = src;
+  a.ld = ld;
+  a.rowidx = nullptr;
+  a.h = h;
+  a.p = p;
+  a.bsel = bsel;
+  a.steps = (int)std::min<int64_t>(h, p);
+  a.mode = 0;
+  a.perm = B.perm;
+  a.Rbuf = B.Rbuf;
+  a.refl = B.refl;
+  a.ovf = B.ovf;
+  a.per = g.per;
+  a.cap = g.cap;
+  a.cap_pad = g.cap_pad;
+  a.ovpad = g.ovpad;
+  a.st = st;
+  a.panel_id = panel;
+  a.tau = tau;
+  a.L21 = L21;
+  a.ldl = ldl;
+  a.moved = B.moved;
+  launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
+  CU_TRY(cudaGetLastError());
+
+  const int64_t ncol = p - bsel;
+  const int tw = 128;
+  const int nblk = ncol > 0 ? (int)((ncol + tw - 1) / tw) : 0;
+  if (nblk > 0) {
+    const size_t dyn = ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8;
+    trsm_kernel<<<nblk, tw, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+    CU_TRY(cudaGetLastError());
+  }
+  FinalizeArgs f{};
+  f.pa = a;
+  f.pa.cand = B.cand;
+  f.pa.cand_flat = B.cand_flat;
+  f.pa.ncand = nblk;
+  f.swap_cap = swap_cap(bsel, p, tau);
+  f.D = D;
+  f.piv = piv;
+  f.gperm = gperm;
+  f.swaps_dev = swaps_dev;
+  f.do_gepp = do_gepp ? 1 : 0;
+  launch_cluster(panel_finalize_kernel, g, g.dyn_final, s, f);
+  CU_TRY(cudaGetLastError());
+}
+
+void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* Bm, int64_t ldb, int64_t M,
+                  int64_t N, int K, DevState* st, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  const bool tma_ok = ((uintptr_t)L % 16 == 0) && ((uintptr_t)Bm % 16 == 0) && (ldl % 2 == 0) && (ldb % 2 == 0) &&
+                      K <= 4 * SCH_KC && M < (1ll << 31) && N < (1ll << 31);
+  if (tma_ok) {
+    const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl);
+    const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb);
+    const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
+    dim3 grid((unsigned)((N + SCH_BN - 1) / SCH_BN), (unsigned)((M + SCH_BM - 1) / SCH_BM));
+    schur_dmma_kernel<<<grid, SCH_THREADS, sizeof(SchurSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st);
+  } else {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 7) / 8));
+    schur_simt_kernel<<<grid, 256, 0, s>>>(L, ldl, Bm, ldb, C, ldc, (int)M, (int)N, K, st);
+  }
+  CU_TRY(cudaGetLastError());
+}
+
+void read_state(DevState* st_dev, DevState& hs, cudaStream_t s) {
+  CU_TRY(cudaMemcpyAsync(&hs, st_dev, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CU_TRY(cudaStreamSynchronize(s));
+}
+
+int state_to_err(const DevState& hs, prrp_err* err) {
+  if (hs.code == 0) return PRRP_OK;
+  if (err) {
+    err->code = hs.code;
+    err->panel = hs.panel;
+    err->index = hs.index;
+    err->column = hs.column;
+    err->tree_level = hs.tree_level;
+    err->tree_index = hs.tree_index;
+    err->worst = hs.worst;
+    snprintf(err->msg, sizeof(err->msg), "device error %d", hs.code);
+  }
+  return hs.code;
+}
+
+double bits_to_double(unsigned long long b) {
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+
+void fill_stats(const DevState& hs, prrp_stats* stats) {
+  if (!stats) return;
+  stats->original_max = bits_to_double(hs.orig_max);
+  stats->intermediate_max = bits_to_double(hs.inter_max);
+  stats->finish_max = bits_to_double(hs.finish_max);
+  stats->panel_multiplier_max = bits_to_double(hs.pmm);
+}
+
+// Q = H_0 H_1 ... assembled like pivoted_qr._reflect (q[:, k:] -= outer(beta*qv, v)).
+__global__ void form_q_kernel(const double* refl, int h, int steps, double* Q /* col-major h x h */) {
+  extern __shared__ __align__(16) double q[];   // row-major h x h
+  __shared__ double qv[PRRP_MAXH];
+  const int t = threadIdx.x;
+  for (int e = t; e < h * h; e += blockDim.x) q[e] = (e / h == e % h) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int k = 0; k < steps; ++k) {
+    const double* v = refl + (int64_t)k * (h + 1);
+    const double beta = v[h];
+    if (beta == 0.0) continue;
+    for (int i = t; i < h; i += blockDim.x) {
+      double acc = 0.0;
+      for (int l = k; l < h; ++l) acc = fma(q[i * h + l], v[l], acc);
+      qv[i] = mul_rn(beta, acc);
+    }
+    __syncthreads();
+    for (int e = t; e < h * (h - k); e += blockDim.x) {
+      const int i = e / (h - k), l = k + e % (h - k);
+      q[i * h + l] = sub_rn(q[i * h + l], mul_rn(qv[i], v[l]));
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < h * h; e += blockDim.x) {
+    const int i = e / h, j = e % h;
+    Q[i + (int64_t)j * h] = q[e];
+  }
+}
+
+__global__ void r_out_kernel(const double* Rbuf, int h, int64_t p, const int32_t* perm, double* R, int64_t* perm_out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)h * p; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = e / h;
+    const int i = (int)(e % h);
+    R[e] = Rbuf[(int64_t)i * p + pos];
+    if (i == 0) perm_out[pos] = perm[pos];
+  }
+}
+
+__global__ void iota32_kernel(int32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
+}
+
+DevState* new_state(Arena& ar, cudaStream_t s) {
+  DevState* st = ar.get<DevState>(1);
+  CU_TRY(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  return st;
+}
+
+// ---------------------------------------------------------------- LU_PRRP driver
+int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm,
+                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  caps();
+  const int npanels = (int)((n + b - 1) / b);
+  Arena ar(s);
+  DevState* st = new_state(ar, s);
+  const int64_t ldl = ((m + 7) / 8) * 8;
+  double* L21 = ar.get<double>((size_t)b * ldl);
+  const PanelCfg g0 = panel_config(b, m, b);
+  PanelBuffers B{};
+  B.Rbuf = ar.get<double>((size_t)b * m);
+  B.perm = ar.get<int32_t>(m);
+  B.ovf = ar.get<double>((size_t)g0.C * b * std::max<int64_t>(1, g0.ovpad));
+  B.cand = ar.get<double>((m + 127) / 128 + 1);
+  B.cand_flat = ar.get<long long>((m + 127) / 128 + 1);
+  B.moved = ar.get<int32_t>(2 * m);
+  B.refl = nullptr;
+  double* D = ar.get<double>((size_t)b * b);
+  int32_t* piv = ar.get<int32_t>(b);
+  int32_t* gperm = ar.get<int32_t>(b);
+  int32_t* swaps_dev = ar.get<int32_t>(npanels);
+  CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
+
+  const int sms = caps().sms;
+  iota_kernel<<<sms, 256, 0, s>>>(perm, m);
+  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  CU_TRY(cudaGetLastError());
+
+  int panel = 0;
+  for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
+    const int bj = (int)std::min<int64_t>(b, n - col0);
+    const int64_t rows = m - col0;
+    const int64_t width = n - col0 - bj;
+    double* blk = A + col0 * lda + col0;
+    if (rows > bj) {
+      strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L21, ldl, B, st, swaps_dev, D, piv, gperm, true, s);
+      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
+          A, lda, col0, n, B.moved, perm, st, panel);
+      CU_TRY(cudaGetLastError());
+      if (width > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L21, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
+                     width, bj, st, s);
+      const int ctw = bj > 64 ? 64 : 128;
+      compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, s>>>(
+          L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
+      CU_TRY(cudaGetLastError());
+    } else {
+      gepp_diag_kernel<<<1, 1024, (size_t)bj * bj * 8, s>>>(blk, lda, bj, D, piv, gperm, st, panel);
+      CU_TRY(cudaGetLastError());
+    }
+    blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, s>>>(
+        A, lda, col0, bj, n, D, piv, gperm, perm, st);
+    CU_TRY(cudaGetLastError());
+  }
+  DevState hs;
+  read_state(st, hs, s);
+  std::vector<int32_t> sw(npanels);
+  CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
+  if (swap_counts) memcpy(swap_counts, sw.data(), sizeof(int32_t) * npanels);
+  fill_stats(hs, stats);
+  if (stats) {
+    stats->total_swaps = 0;
+    for (int v : sw) stats->total_swaps += v;
+  }
+  return state_to_err(hs, err);
+}
+
+}  // namespace
+
+// ======================================================================== ABI
+extern "C" {
+
+int prrp_b200_abi_version(void) { return kAbiVersion; }
+
+int prrp_b200_device_probe(int32_t* sm_count, int32_t* max_cluster, prrp_err* err) {
+  clear_err(err);
+  try {
+    DeviceCaps& c = caps();
+    if (sm_count) *sm_count = c.sms;
+    if (max_cluster) *max_cluster = c.max_cluster;
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_luprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau, int64_t* perm,
+                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    return luprrp_impl(A, lda, m, n, b, tau, perm, swap_counts, stats, err, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_caluprrp(double*, int64_t, int64_t, int64_t, int32_t, double, int32_t, int64_t*, int32_t*, prrp_stats*,
+                  prrp_err* err, void*) {
+  clear_err(err);
+  return report(err, Fail{PRRP_ERR_UNSUPPORTED, "caluprrp device path not built yet"});
+}
+
+int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t bsel, double tau, double* R,
+                     double* Q, int64_t* perm, double* Lblk, int32_t* swap_count, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+    if (h < bsel || p < bsel + 1 || bsel < 1) fail(PRRP_ERR_ARG, "strong_rrqr needs >= b rows and >= b+1 columns");
+    if (h > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "h > 128 is outside the device panel engine");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    const PanelCfg g = panel_config(h, p, bsel);
+    PanelBuffers B{};
+    B.Rbuf = ar.get<double>((size_t)h * p);
+    B.perm = ar.get<int32_t>(p);
+    B.ovf = ar.get<double>((size_t)g.C * h * std::max<int64_t>(1, g.ovpad));
+    B.cand = ar.get<double>((p + 127) / 128 + 1);
+    B.cand_flat = ar.get<long long>((p + 127) / 128 + 1);
+    B.moved = ar.get<int32_t>(2 * p);
+    const int steps = (int)std::min<int64_t>(h, p);
+    B.refl = ar.get<double>((size_t)steps * (h + 1));
+    const int64_t ldl = std::max<int64_t>(1, p - bsel);
+    double* L = ar.get<double>((size_t)bsel * ldl);
+    int32_t* swaps_dev = ar.get<int32_t>(1);
+    CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t), s));
+    strong_rrqr_panel(a, lda, h, p, bsel, tau, 0, L, ldl, B, st, swaps_dev, nullptr, nullptr, nullptr, false, s);
+    r_out_kernel<<<caps().sms, 256, 0, s>>>(B.Rbuf, h, p, B.perm, R, perm);
+    form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(B.refl, h, steps, Q);
+    CU_TRY(cudaGetLastError());
+    if (p > bsel) CU_TRY(cudaMemcpyAsync(Lblk, L, sizeof(double) * (size_t)bsel * (p - bsel), cudaMemcpyDeviceToDevice, s));
+    DevState hs;
+    read_state(st, hs, s);
+    int32_t sw = 0;
+    CU_TRY(cudaMemcpy(&sw, swaps_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (swap_count) *swap_count = sw;
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p, double* R, double* Q, prrp_err* err,
+                        void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "h > 128 is outside the device panel engine");
+    if (h < 1 || p < 1) fail(PRRP_ERR_ARG, "empty matrix");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    const PanelCfg g = panel_config(h, p, 1);
+    double* Rbuf = ar.get<double>((size_t)h * p);
+    int32_t* permb = ar.get<int32_t>(p);
+    const int steps = (int)std::min<int64_t>(h, p);
+    double* refl = ar.get<double>((size_t)steps * (h + 1));
+    double* ovf = ar.get<double>((size_t)g.C * h * std::max<int64_t>(1, g.ovpad));
+    iota32_kernel<<<caps().sms, 256, 0, s>>>(permb, p);
+    PanelArgs pa{};
+    pa.src = a;
+    pa.ld = lda;
+    pa.h = h;
+    pa.p = p;
+    pa.bsel = 1;
+    pa.steps = steps;
+    pa.mode = 1;
+    pa.perm = permb;
+    pa.Rbuf = Rbuf;
+    pa.refl = refl;
+    pa.ovf = ovf;
+    pa.per = g.per;
+    pa.cap = g.cap;
+    pa.cap_pad = g.cap_pad;
+    pa.ovpad = g.ovpad;
+    pa.st = st;
+    launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
+    int64_t* dummy_perm = ar.get<int64_t>(p);
+    r_out_kernel<<<caps().sms, 256, 0, s>>>(Rbuf, h, p, permb, R, dummy_perm);
+    form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(refl, h, steps, Q);
+    CU_TRY(cudaGetLastError());
+    DevState hs;
+    read_state(st, hs, s);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* B, int64_t ldb, int64_t M,
+                      int64_t N, int32_t K, double* absmax, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    schur_update(C, ldc, L, ldl, B, ldb, M, N, K, st, s);
+    DevState hs;
+    read_state(st, hs, s);
+    if (absmax) *absmax = bits_to_double(hs.inter_max);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* perm, double* intermediate_max,
+                       prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (m < 1 || m > PRRP_MAXH || n < m) fail(PRRP_ERR_UNSUPPORTED, "gepp_blockrow needs 1 <= m <= 128, n >= m");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    double* D = ar.get<double>((size_t)m * m);
+    int32_t* piv = ar.get<int32_t>(m);
+    int32_t* gperm = ar.get<int32_t>(m);
+    iota_kernel<<<1, 128, 0, s>>>(perm, m);
+    maxabs_kernel<<<caps().sms, 256, 0, s>>>(A, lda, m, n, st);
+    gepp_diag_kernel<<<1, 1024, (size_t)m * m * 8, s>>>(A, lda, m, D, piv, gperm, st, 0);
+    blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)m * m + (size_t)m * BR_TW) * 8, s>>>(
+        A, lda, 0, m, n, D, piv, gperm, perm, st);
+    CU_TRY(cudaGetLastError());
+    DevState hs;
+    read_state(st, hs, s);
+    if (intermediate_max) *intermediate_max = bits_to_double(hs.finish_max);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// FP64 Schur update C <- C - L21 * A12 on the FP64 tensor pipe (DMMA).
+//
+// Reference: matcore.rank_update (matcore.py:54-61) = c - matmul(a, b),
+// matmul (matcore.py:41-51) accumulating rank-1 dger terms in increasing k
+// from a zero matrix.  On FMA hosts dger performs acc = fma(a_ik, b_kj, acc)
+// per k, and sm_100 DMMA.8x8x4 performs exactly that chain over its 4 k's
+// (verified on the B200: tools/probes/probe_fp64.cu), so chaining the k-steps
+// in increasing order from a zero accumulator and subtracting once in the
+// epilogue reproduces the reference's rank_update bit for bit.
+//
+// sm_100a has no tcgen05 FP64 kind, so the tensor path is warp-level
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operands are staged by TMA
+// (cp.async.bulk.tensor.2d) into shared memory in a [8-row group][k][8]
+// layout: every m8n8k4 fragment is then one contiguous 256-byte read (no bank
+// conflicts).  An mbarrier ring pipelines the K chunks; the epilogue reads C,
+// subtracts, writes C and folds max|C| into the growth statistic.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+#define SCH_BM 128
+#define SCH_BN 64
+#define SCH_KC 32
+#define SCH_STAGES 2
+#define SCH_THREADS 256
+
+struct SchurSmem {
+  double a[SCH_STAGES][SCH_BM * SCH_KC];
+  double b[SCH_STAGES][SCH_BN * SCH_KC];
+  unsigned long long full[SCH_STAGES];
+  unsigned long long empty[SCH_STAGES];
+  double red[40];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// mapL: L21 column-major (dims {M, K}, box {8, KC}); mapB: A12 row-major (dims {N, K}, box {8, KC})
+__global__ void __launch_bounds__(SCH_THREADS, 2)
+schur_dmma_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
+                  double* C, int64_t ldc, int M, int N, int K, int vec_ok, DevState* st) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  SchurSmem& S = *reinterpret_cast<SchurSmem*>(sbuf);
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int m0 = blockIdx.y * SCH_BM, n0 = blockIdx.x * SCH_BN;
+  const int nk = (K + SCH_KC - 1) / SCH_KC;   // K tail is zero-filled by TMA (exact: fma(0,0,acc) = acc)
+  constexpr uint32_t kStageBytes = (SCH_BM + SCH_BN) * SCH_KC * 8;
+
+  if (t == 0) {
+    for (int s = 0; s < SCH_STAGES; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], SCH_THREADS / 32); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapL) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapB) : "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kc) {
+    const int s = kc % SCH_STAGES;
+    mbar_expect_tx(&S.full[s], kStageBytes);
+    for (int g = 0; g < SCH_BM / 8; ++g) tma_load_2d(&S.a[s][g * SCH_KC * 8], &mapL, &S.full[s], m0 + 8 * g, kc * SCH_KC);
+    for (int g = 0; g < SCH_BN / 8; ++g) tma_load_2d(&S.b[s][g * SCH_KC * 8], &mapB, &S.full[s], n0 + 8 * g, kc * SCH_KC);
+  };
+  if (t == 0)
+    for (int kc = 0; kc < nk && kc < SCH_STAGES; ++kc) issue(kc);
+
+  // warp tile 32 x 32: warps 4 (M) x 2 (N)
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int fr = lane & 3, fc = lane >> 2;   // fragment k index, row/col index
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc % SCH_STAGES;
+    mbar_wait(&S.full[s], (kc / SCH_STAGES) & 1);
+    const double* sa = S.a[s];
+    const double* sb = S.b[s];
+#pragma unroll
+    for (int k4 = 0; k4 < SCH_KC; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SCH_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SCH_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (t == 0 && kc + SCH_STAGES < nk) {
+      mbar_wait(&S.empty[s], (kc / SCH_STAGES) & 1);
+      issue(kc + SCH_STAGES);
+    }
+    __syncwarp();
+  }
+
+  // epilogue: C -= acc, max|C|
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + fc;
+    if (r >= M) continue;
+    double* crow = C + (int64_t)r * ldc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cidx = n0 + wn + j * 8 + 2 * fr;
+      if (vec_ok && cidx + 1 < N) {
+        double2 cv = *reinterpret_cast<const double2*>(crow + cidx);
+        cv.x = sub_rn(cv.x, acc[i][j][0]);
+        cv.y = sub_rn(cv.y, acc[i][j][1]);
+        *reinterpret_cast<double2*>(crow + cidx) = cv;
+        mx = fmax(mx, fmax(fabs(cv.x), fabs(cv.y)));
+      } else {
+        if (cidx < N) {
+          const double v = sub_rn(crow[cidx], acc[i][j][0]);
+          crow[cidx] = v;
+          mx = fmax(mx, fabs(v));
+        }
+        if (cidx + 1 < N) {
+          const double v = sub_rn(crow[cidx + 1], acc[i][j][1]);
+          crow[cidx + 1] = v;
+          mx = fmax(mx, fabs(v));
+        }
+      }
+    }
+  }
+  mx = block_max(mx, S.red);
+  if (t == 0) atomic_max_abs(&st->inter_max, mx);
+}
+
+// Generic-shape fallback with the identical rounding recipe (odd K or
+// unaligned operands): one thread per C element, fma chain from zero.
+__global__ void __launch_bounds__(256) schur_simt_kernel(const double* L, int64_t ldl, const double* B, int64_t ldb,
+                                                        double* C, int64_t ldc, int M, int N, int K, DevState* st) {
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
+  double mx = 0.0;
+  if (r < M && c < N) {
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) acc = fma(L[(int64_t)k * ldl + r], B[(int64_t)k * ldb + c], acc);
+    const double v = sub_rn(C[(int64_t)r * ldc + c], acc);
+    C[(int64_t)r * ldc + c] = v;
+    mx = fabs(v);
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) atomic_max_abs(&st->inter_max, mx);
+}

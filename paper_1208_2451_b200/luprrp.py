@@ -1,0 +1,208 @@
+"""LU_PRRP (Algorithm 1) behind the reference's entry point.
+
+``luprrp_factor(a, b, tau)`` keeps the signature, validation, exceptions and
+return type of the reference (luprrp.py:153-201); the factorization itself
+runs on the B200 through ``prrp_luprrp`` in libprrp_b200.so.  The growth
+statistics (luprrp.py:33-78) come back from the device; the exact rational
+flop counters are rebuilt on the host from the per-panel swap counts with
+the reference's charging rules (luprrp.py:135-140, 168-197).
+"""
+import ctypes
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatch
+
+
+@dataclass
+class ElimStats:
+    """Element-growth bookkeeping (reference luprrp.py:33-78)."""
+
+    original_max: float
+    intermediate_max: float
+    finish_max: float = 0.0
+    swap_counts: list = field(default_factory=list)
+    flops_charged: Fraction = Fraction(0)
+    flops_executed: Fraction = Fraction(0)
+    panel_multiplier_max: float = 0.0
+
+    @property
+    def growth_factor(self):
+        if self.original_max == 0.0:
+            raise ZeroDivisionError("growth factor of an all-zero matrix")
+        return self.intermediate_max / self.original_max
+
+    @property
+    def full_growth_factor(self):
+        if self.original_max == 0.0:
+            raise ZeroDivisionError("growth factor of an all-zero matrix")
+        return max(self.intermediate_max, self.finish_max) / self.original_max
+
+
+@dataclass
+class BlockLUFactors:
+    perm: np.ndarray       # apply_row_perm(perm, a) == l @ u
+    l: np.ndarray          # m x n unit lower trapezoidal
+    u: np.ndarray          # n x n upper triangular
+    panel_width: int
+    stats: ElimStats
+
+
+@dataclass
+class DeviceLU:
+    """Device-resident result: packed L\\U (row-major m x n view of the
+    working buffer), global row order and statistics."""
+    perm: object           # torch int64 [m] on the device
+    lu: object             # torch float64 [m, n] view, packed L\\U in place
+    panel_width: int
+    stats: ElimStats
+
+
+def _qr_charge(rows, cols):
+    return Fraction(2 * rows * cols * cols) - Fraction(2, 3) * cols ** 3
+
+
+def _finish_charge(bj, width):
+    return Fraction(2, 3) * bj ** 3 + Fraction((width - bj) * bj * bj)
+
+
+def flop_counters(m, n, b, swap_counts, compose=True, tournament_extra=None):
+    """(charged, executed) exactly as luprrp_factor accumulates them."""
+    charged = Fraction(0)
+    executed = Fraction(0)
+    col0 = 0
+    panel = 0
+    while col0 < n:
+        bj = min(b, n - col0)
+        rows = m - col0
+        width = n - col0 - bj
+        charged += _qr_charge(rows, bj)
+        if rows > bj:
+            if tournament_extra is not None and tournament_extra[panel] is not None:
+                extra = tournament_extra[panel]
+                charged += extra
+                executed += extra + _qr_charge(rows, bj)
+            else:
+                executed += (1 + swap_counts[panel]) * _qr_charge(rows, bj)
+        upd = Fraction(2 * bj * (rows - bj) * width)
+        charged += upd
+        executed += upd
+        if compose and col0 + bj < m:
+            executed += Fraction(2 * (m - col0 - bj) * bj * bj)
+        fin = _finish_charge(bj, n - col0)
+        charged += fin
+        executed += fin
+        col0 += bj
+        panel += 1
+    return charged, executed
+
+
+def _validate(a, b, tau):
+    m, n = a.shape
+    if m < n:
+        raise DimensionMismatch("need at least as many rows as columns")
+    if not 1 <= b <= n:
+        raise ValueError(f"panel width {b} out of range [1, {n}]")
+    if tau <= 1.0:
+        raise ValueError("tau must exceed 1")
+
+
+def as_matrix(a):
+    m = np.asarray(a, dtype=np.float64)
+    if m.ndim != 2:
+        raise DimensionMismatch(f"expected a 2-D array, got ndim={m.ndim}")
+    return m
+
+
+def upload(a):
+    """Host matrix -> device working buffer (row-major, even pitch)."""
+    import torch
+    m, n = a.shape
+    lda = n + (n & 1)
+    buf = torch.empty((m, lda), dtype=torch.float64, device="cuda")
+    buf[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(a)), non_blocking=False)
+    return buf, lda
+
+
+def run_device(fn_name, buf, lda, m, n, b, tau, extra=(), stream=None):
+    """Call prrp_luprrp / prrp_caluprrp on a device buffer; returns (perm, stats, swaps)."""
+    import torch
+    lib = _lib.device_lib()
+    perm = torch.empty(m, dtype=torch.int64, device=buf.device)
+    npan = (n + b - 1) // b
+    swaps = (ctypes.c_int32 * npan)()
+    st = _lib.PrrpStats()
+    err = _lib.PrrpErr()
+    fn = getattr(lib, fn_name)
+    rc = fn(ctypes.c_void_p(buf.data_ptr()), lda, m, n, b, float(tau), *extra,
+            ctypes.c_void_p(perm.data_ptr()), swaps, ctypes.byref(st), ctypes.byref(err),
+            _lib.stream_handle(stream))
+    _lib.raise_for(rc, err, fn_name)
+    return perm, st, list(swaps)
+
+
+def split_packed(packed, m, n):
+    """Packed L\\U (m x n) -> (l m x n unit lower trapezoidal, u n x n upper), F-order."""
+    l = np.tril(packed, -1)
+    idx = np.arange(n)
+    l[idx, idx] = 1.0
+    u = np.triu(packed[:n, :])
+    return np.asfortranarray(l), np.asfortranarray(u)
+
+
+def _stats(st, swaps, m, n, b):
+    charged, executed = flop_counters(m, n, b, swaps)
+    return ElimStats(original_max=st.original_max, intermediate_max=st.intermediate_max,
+                     finish_max=st.finish_max, swap_counts=list(map(int, swaps)),
+                     flops_charged=charged, flops_executed=executed,
+                     panel_multiplier_max=st.panel_multiplier_max)
+
+
+def luprrp_factor(a, b, tau=2.0):
+    """Factor an m x n (m >= n) matrix; panel width b, multiplier bound tau.
+
+    Drop-in for prrp.luprrp_factor (reference luprrp.py:153).  The input is
+    copied to the device; the caller's array is never modified."""
+    a = as_matrix(a)
+    _validate(a, b, tau)
+    m, n = a.shape
+    _lib.device_lib()
+    buf, lda = upload(a)
+    perm, st, swaps = run_device("prrp_luprrp", buf, lda, m, n, b, tau)
+    packed = buf[:, :n].cpu().numpy()
+    l, u = split_packed(packed, m, n)
+    return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b,
+                          stats=_stats(st, swaps, m, n, b))
+
+
+def luprrp_factor_device(buf, b, tau=2.0, n=None, stream=None):
+    """In-place LU_PRRP of a device-resident row-major float64 tensor
+    ``buf`` (m x lda, lda even, the first n columns are the matrix).
+    Returns DeviceLU with the packed L\\U view; nothing leaves the device
+    except the small statistics record."""
+    m, lda = buf.shape
+    n = lda if n is None else n
+    if m < n:
+        raise DimensionMismatch("need at least as many rows as columns")
+    if not 1 <= b <= n:
+        raise ValueError(f"panel width {b} out of range [1, {n}]")
+    if tau <= 1.0:
+        raise ValueError("tau must exceed 1")
+    perm, st, swaps = run_device("prrp_luprrp", buf, lda, m, n, b, tau, stream=stream)
+    return DeviceLU(perm=perm, lu=buf[:, :n], panel_width=b, stats=_stats(st, swaps, m, n, b))
+
+
+def growth_bound_luprrp_log2(n, b, tau):
+    """log2 of the growth envelope (1 + tau b)^ceil(n/b) (luprrp.py:217-221)."""
+    if not (n >= b >= 1) or tau <= 0:
+        raise ValueError("need n >= b >= 1 and tau > 0")
+    return math.ceil(n / b) * math.log2(1.0 + tau * b)
+
+
+def growth_bound_luprrp(n, b, tau):
+    lg = growth_bound_luprrp_log2(n, b, tau)
+    return math.inf if lg > 1023.0 else 2.0 ** lg
