@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
     if (r11_checks(r11, a.bsel, a.st->fro, a.st, a.panel_id, c == 0 && t == 0)) return;
     worst = -1.0;
     wflat = LLONG_MAX;
-    const int TW = a.bsel > 64 ? 64 : 128;
+    const int TW = min((int)blockDim.x, a.bsel > 64 ? 64 : 128);
     const int64_t ntile = (ncol + TW - 1) / TW;
     for (int64_t tile = c; tile < ntile; tile += C) {
       trsm_tile(a.Rbuf, a.p, a.bsel, r11, xs, TW, a.bsel + tile * TW, a.L21, a.ldl, worst, wflat);

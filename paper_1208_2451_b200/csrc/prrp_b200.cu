@@ -80,7 +80,7 @@ DeviceCaps& caps() {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
     }
-    CU_TRY(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptin));
+    CU_TRY(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
     CU_TRY(cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 16 * 1024)));
     CU_TRY(cudaFuncSetAttribute(blockrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
     CU_TRY(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));

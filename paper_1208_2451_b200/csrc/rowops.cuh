@@ -108,18 +108,16 @@ __global__ void __launch_bounds__(BR_TW) blockrow_kernel(double* A, int64_t lda,
     const int jc = (int)(j - col0);
     for (int i = 0; i < b; ++i) A[(col0 + i) * lda + j] = D[i * b + jc];
   } else if (trailing) {
+    // Rows carry their multipliers through later interchanges, so replaying
+    // the reference's step-by-step elimination equals: gather the rows in
+    // their final order, then eliminate with the final L11 column by column
+    // (same multiplier, same pivot value, same update order per element).
     for (int i = 0; i < b; ++i) {
-      const double v = A[(col0 + i) * lda + j];
+      const double v = A[(col0 + s_gp[i]) * lda + j];
       xs[i * BR_TW + t] = v;
       mx = fmax(mx, fabs(v));
     }
     for (int k = 0; k < b; ++k) {
-      const int pv = s_piv[k];
-      if (pv != k) {
-        const double x = xs[k * BR_TW + t];
-        xs[k * BR_TW + t] = xs[pv * BR_TW + t];
-        xs[pv * BR_TW + t] = x;
-      }
       if (k + 1 < b) {
         const double xk = xs[k * BR_TW + t];
         for (int i = k + 1; i < b; ++i) {
