@@ -73,6 +73,27 @@ typedef struct prrp_stats {
   int64_t total_swaps;
 } prrp_stats;
 
+/* Optional device-time breakdown of a factorization (CUDA events around
+ * every launch, summed per kernel class).  Classes: */
+enum prrp_kclass {
+  PRRP_K_PANEL = 0,      /* panel_qrcp_kernel    (cluster QRCP)            */
+  PRRP_K_TRSM = 1,       /* trsm_kernel          (L21, tau candidates)     */
+  PRRP_K_FINALIZE = 2,   /* panel_finalize_kernel (swap loop, GEPP A11)    */
+  PRRP_K_PERMUTE = 3,    /* permute_kernel                                 */
+  PRRP_K_SCHUR = 4,      /* schur_dmma_kernel / schur_simt_kernel          */
+  PRRP_K_COMPOSE = 5,    /* compose_kernel                                 */
+  PRRP_K_BLOCKROW = 6,   /* blockrow_kernel / gepp_diag_kernel             */
+  PRRP_K_OTHER = 7,      /* init kernels                                   */
+  PRRP_K_COUNT = 8
+};
+
+typedef struct prrp_timing {
+  double ms[PRRP_K_COUNT];       /* summed event time per class             */
+  int32_t launches[PRRP_K_COUNT];
+  double schur_flops;            /* algorithmic 2*M*N*K summed over updates */
+  double total_ms;               /* first to last event of the call         */
+} prrp_timing;
+
 /* Library identification: returns the ABI version (major*100 + minor). */
 int prrp_b200_abi_version(void);
 
@@ -88,6 +109,17 @@ int prrp_b200_device_probe(int32_t* sm_count, int32_t* max_cluster, prrp_err* er
 int prrp_luprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
                 int64_t* perm, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
                 void* stream);
+
+/* prrp_luprrp with an optional per-kernel-class device-time breakdown
+ * (timing may be NULL; then identical to prrp_luprrp). */
+int prrp_luprrp_timed(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
+                      int64_t* perm, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
+                      prrp_timing* timing, void* stream);
+
+/* Sustained FP64 tensor-pipe (DMMA.8x8x4) throughput of this device in
+ * TFLOP/s: register-resident mma.sync.m8n8k4.f64 loop on every SM for about
+ * `ms` milliseconds.  The roofline denominator of the Schur update. */
+int prrp_b200_dmma_peak(double ms, double* tflops, prrp_err* err);
 
 /* CALU_PRRP factorization with a binary tournament tree of `leaf_count`
  * leaves — replaces prrp.caluprrp_factor(a, b, tau, binary_tree(P))

@@ -34,6 +34,14 @@ class PrrpStats(ctypes.Structure):
                 ("total_swaps", ctypes.c_int64)]
 
 
+KCLASSES = ("panel", "trsm", "finalize", "permute", "schur", "compose", "blockrow", "other")
+
+
+class PrrpTiming(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 8), ("launches", ctypes.c_int32 * 8),
+                ("schur_flops", ctypes.c_double), ("total_ms", ctypes.c_double)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
@@ -43,6 +51,8 @@ SIGNATURES = {
     "prrp_b200_abi_version": ([], ctypes.c_int),
     "prrp_b200_device_probe": ([_P, _P, _P], ctypes.c_int),
     "prrp_luprrp": ([_P, _I64, _I64, _I64, _I32, _D, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_luprrp_timed": ([_P, _I64, _I64, _I64, _I32, _D, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_b200_dmma_peak": ([_D, _P, _P], ctypes.c_int),
     "prrp_caluprrp": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_strong_rrqr": ([_P, _I64, _I32, _I64, _I32, _D, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_householder_qr": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),

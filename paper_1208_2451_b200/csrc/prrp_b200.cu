@@ -159,6 +159,55 @@ struct Arena {
   }
 };
 
+// ---------------------------------------------------------------- timing
+// Optional per-kernel-class device timing: CUDA events recorded around every
+// launch on the launching stream, summed after the final synchronisation.
+struct Timer {
+  struct Span { int cls; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      CU_TRY(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void begin(int cls, cudaStream_t s) {
+    Span sp{cls, ev(), nullptr};
+    CU_TRY(cudaEventRecord(sp.a, s));
+    spans.push_back(sp);
+  }
+  void end(cudaStream_t s) {
+    spans.back().b = ev();
+    CU_TRY(cudaEventRecord(spans.back().b, s));
+  }
+  void collect(prrp_timing* t) {
+    memset(t->ms, 0, sizeof(t->ms));
+    memset(t->launches, 0, sizeof(t->launches));
+    for (const Span& sp : spans) {
+      float ms = 0.f;
+      CU_TRY(cudaEventElapsedTime(&ms, sp.a, sp.b));
+      t->ms[sp.cls] += ms;
+      t->launches[sp.cls] += 1;
+    }
+    if (!spans.empty()) {
+      float ms = 0.f;
+      CU_TRY(cudaEventElapsedTime(&ms, spans.front().a, spans.back().b));
+      t->total_ms = ms;
+    }
+  }
+  ~Timer() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+thread_local Timer* tl_timer = nullptr;
+thread_local double tl_schur_flops = 0.0;
+inline void tbegin(int cls, cudaStream_t s) { if (tl_timer) tl_timer->begin(cls, s); }
+inline void tend(cudaStream_t s) { if (tl_timer) tl_timer->end(s); }
+
 // ---------------------------------------------------------------- launches
 struct PanelCfg {
   int C, T;
@@ -250,7 +299,9 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.L21 = L21;
   a.ldl = ldl;
   a.moved = B.moved;
+  tbegin(PRRP_K_PANEL, s);
   launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
+  tend(s);
   CU_TRY(cudaGetLastError());
 
   const int64_t ncol = p - bsel;
@@ -258,7 +309,9 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   const int nblk = ncol > 0 ? (int)((ncol + tw - 1) / tw) : 0;
   if (nblk > 0) {
     const size_t dyn = ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8;
+    tbegin(PRRP_K_TRSM, s);
     trsm_kernel<<<nblk, tw, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+    tend(s);
     CU_TRY(cudaGetLastError());
   }
   FinalizeArgs f{};
@@ -272,13 +325,17 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   f.gperm = gperm;
   f.swaps_dev = swaps_dev;
   f.do_gepp = do_gepp ? 1 : 0;
+  tbegin(PRRP_K_FINALIZE, s);
   launch_cluster(panel_finalize_kernel, g, g.dyn_final, s, f);
+  tend(s);
   CU_TRY(cudaGetLastError());
 }
 
 void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* Bm, int64_t ldb, int64_t M,
                   int64_t N, int K, DevState* st, cudaStream_t s) {
   if (M <= 0 || N <= 0) return;
+  tl_schur_flops += 2.0 * (double)M * (double)N * (double)K;
+  tbegin(PRRP_K_SCHUR, s);
   const bool tma_ok = ((uintptr_t)L % 16 == 0) && ((uintptr_t)Bm % 16 == 0) && (ldl % 2 == 0) && (ldb % 2 == 0) &&
                       K <= 4 * SCH_KC && M < (1ll << 31) && N < (1ll << 31);
   if (tma_ok) {
@@ -291,6 +348,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 7) / 8));
     schur_simt_kernel<<<grid, 256, 0, s>>>(L, ldl, Bm, ldb, C, ldc, (int)M, (int)N, K, st);
   }
+  tend(s);
   CU_TRY(cudaGetLastError());
 }
 
@@ -366,6 +424,22 @@ __global__ void r_out_kernel(const double* Rbuf, int h, int64_t p, const int32_t
   }
 }
 
+// register-resident DMMA loop: 8 independent m8n8k4 chains per warp
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* sink, long iters) {
+  double acc[8][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) { acc[c][0] = threadIdx.x * 1e-3; acc[c][1] = c; }
+  const double av = 1.0000001 + threadIdx.x * 1e-9, bv = 0.9999999 - threadIdx.x * 1e-9;
+  for (long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dmma884(acc[c][0], acc[c][1], av, bv);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 1234.5) sink[0] = s;
+}
+
 __global__ void iota32_kernel(int32_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = (int32_t)i;
@@ -379,7 +453,11 @@ DevState* new_state(Arena& ar, cudaStream_t s) {
 
 // ---------------------------------------------------------------- LU_PRRP driver
 int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm,
-                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, prrp_timing* timing, cudaStream_t s) {
+  Timer timer;
+  tl_timer = timing ? &timer : nullptr;
+  tl_schur_flops = 0.0;
+  struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
   if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
   if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
   if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
@@ -407,8 +485,10 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
 
   const int sms = caps().sms;
+  tbegin(PRRP_K_OTHER, s);
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
   maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  tend(s);
   CU_TRY(cudaGetLastError());
 
   int panel = 0;
@@ -419,22 +499,30 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     double* blk = A + col0 * lda + col0;
     if (rows > bj) {
       strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L21, ldl, B, st, swaps_dev, D, piv, gperm, true, s);
+      tbegin(PRRP_K_PERMUTE, s);
       permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
           A, lda, col0, n, B.moved, perm, st, panel);
+      tend(s);
       CU_TRY(cudaGetLastError());
       if (width > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L21, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
                      width, bj, st, s);
       const int ctw = bj > 64 ? 64 : 128;
+      tbegin(PRRP_K_COMPOSE, s);
       compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, s>>>(
           L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
+      tend(s);
       CU_TRY(cudaGetLastError());
     } else {
+      tbegin(PRRP_K_BLOCKROW, s);
       gepp_diag_kernel<<<1, 1024, (size_t)bj * bj * 8, s>>>(blk, lda, bj, D, piv, gperm, st, panel);
+      tend(s);
       CU_TRY(cudaGetLastError());
     }
+    tbegin(PRRP_K_BLOCKROW, s);
     blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, s>>>(
         A, lda, col0, bj, n, D, piv, gperm, perm, st);
+    tend(s);
     CU_TRY(cudaGetLastError());
   }
   DevState hs;
@@ -446,6 +534,10 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   if (stats) {
     stats->total_swaps = 0;
     for (int v : sw) stats->total_swaps += v;
+  }
+  if (timing) {
+    timer.collect(timing);
+    timing->schur_flops = tl_schur_flops;
   }
   return state_to_err(hs, err);
 }
@@ -473,7 +565,51 @@ int prrp_luprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double 
                 int32_t* swap_counts, prrp_stats* stats, prrp_err* err, void* stream) {
   clear_err(err);
   try {
-    return luprrp_impl(A, lda, m, n, b, tau, perm, swap_counts, stats, err, (cudaStream_t)stream);
+    return luprrp_impl(A, lda, m, n, b, tau, perm, swap_counts, stats, err, nullptr, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_luprrp_timed(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau, int64_t* perm,
+                      int32_t* swap_counts, prrp_stats* stats, prrp_err* err, prrp_timing* timing, void* stream) {
+  clear_err(err);
+  if (timing) memset(timing, 0, sizeof(*timing));
+  try {
+    return luprrp_impl(A, lda, m, n, b, tau, perm, swap_counts, stats, err, timing, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_b200_dmma_peak(double ms, double* tflops, prrp_err* err) {
+  clear_err(err);
+  try {
+    caps();
+    double* sink = nullptr;
+    CU_TRY(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    CU_TRY(cudaEventCreate(&e0));
+    CU_TRY(cudaEventCreate(&e1));
+    const long iters = 4000;
+    const dim3 grid(caps().sms * 2), block(256);
+    dmma_peak_kernel<<<grid, block>>>(sink, 100);
+    CU_TRY(cudaDeviceSynchronize());
+    CU_TRY(cudaEventRecord(e0));
+    int reps = 0;
+    float el = 0.f;
+    while (el < ms) {
+      for (int r = 0; r < 10; ++r, ++reps) dmma_peak_kernel<<<grid, block>>>(sink, iters);
+      CU_TRY(cudaEventRecord(e1));
+      CU_TRY(cudaEventSynchronize(e1));
+      CU_TRY(cudaEventElapsedTime(&el, e0, e1));
+    }
+    const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * grid.x * (block.x / 32) * reps;
+    if (tflops) *tflops = flops / (el * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    return PRRP_OK;
   } catch (const Fail& f) {
     return report(err, f);
   }

@@ -154,6 +154,19 @@ def split_packed(packed, m, n):
     return np.asfortranarray(l), np.asfortranarray(u)
 
 
+def split_packed_device(packed, m, n):
+    """split_packed on the device: unit-lower L and upper U built with torch
+    and transposed there, so the host receives Fortran-ordered arrays (the
+    reference's layout, luprrp.py:130-132) without a host-side copy."""
+    import torch
+    lt = torch.tril(packed, -1)
+    lt.diagonal().fill_(1.0)
+    l = lt.t().contiguous().cpu().numpy().T
+    del lt
+    u = torch.triu(packed[:n, :]).t().contiguous().cpu().numpy().T
+    return l, u
+
+
 def _stats(st, swaps, m, n, b):
     charged, executed = flop_counters(m, n, b, swaps)
     return ElimStats(original_max=st.original_max, intermediate_max=st.intermediate_max,
@@ -173,8 +186,7 @@ def luprrp_factor(a, b, tau=2.0):
     _lib.device_lib()
     buf, lda = upload(a)
     perm, st, swaps = run_device("prrp_luprrp", buf, lda, m, n, b, tau)
-    packed = buf[:, :n].cpu().numpy()
-    l, u = split_packed(packed, m, n)
+    l, u = split_packed_device(buf[:, :n], m, n)
     return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b,
                           stats=_stats(st, swaps, m, n, b))
 
