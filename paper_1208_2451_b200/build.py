@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIBNAME = "libprrp_b200.so"
 SOURCES = ["prrp_b200.cu"]
-HEADERS = ["common.cuh", "panel.cuh", "lsolve.cuh", "rowops.cuh", "schur.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
     "-Xptxas", "-v",
     "-I" + os.path.join(ROOT, "include"),
-]
+] + (["-DPRRP_P64_PROF"] if os.environ.get("PRRP_P64_PROF") else [])
 
 
 def nvcc():

@@ -199,12 +199,13 @@ __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, 
   if (t == 0) atomic_max_abs(&st->finish_max, m);
 }
 
-__global__ void __launch_bounds__(1024) gepp_diag_kernel(const double* src, int64_t ld, int b, double* D,
-                                                          int32_t* piv, int32_t* gperm, DevState* st, int panel) {
+__global__ void __launch_bounds__(1024) gepp_diag_kernel(const double* src, int64_t ld, const int32_t* rowmap, int b,
+                                                          double* D, int32_t* piv, int32_t* gperm, DevState* st,
+                                                          int panel) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[40];
   if (prrp_failed(st)) return;
-  gepp_diag(src, ld, nullptr, b, sm, D, piv, gperm, st, panel, red);
+  gepp_diag(src, ld, rowmap, b, sm, D, piv, gperm, st, panel, red);
 }
 
 // ---------------------------------------------------------------------------

@@ -59,6 +59,7 @@ struct PanelArgs {
   int64_t ldl;
   int32_t* swaps_out;       // host-visible per-panel swap count (device pointer)
   int32_t* moved;           // out: compact list of moved positions (dst pos, src j) pairs
+  long long* prof;          // optional: per-phase clock64 totals of CTA 0 (diagnostics)
 };
 
 struct Rec {

@@ -19,6 +19,8 @@
 
 #include "panel.cuh"
 #include "lsolve.cuh"
+#include "panel64.cuh"
+#include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
 
@@ -76,7 +78,8 @@ DeviceCaps& caps() {
     int dev = 0;
     CU_TRY(cudaGetDevice(&dev));
     CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-    for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel}) {
+    for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
+                           (const void*)panel_qrcp64_kernel}) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
     }
@@ -85,6 +88,12 @@ DeviceCaps& caps() {
     CU_TRY(cudaFuncSetAttribute(blockrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
     CU_TRY(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
     CU_TRY(cudaFuncSetAttribute(gepp_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
+    for (const void* fn : {(const void*)trsm_w_kernel<1>, (const void*)trsm_w_kernel<2>, (const void*)trsm_w_kernel<3>,
+                           (const void*)trsm_w_kernel<4>, (const void*)compose_w_kernel<1>, (const void*)compose_w_kernel<2>,
+                           (const void*)compose_w_kernel<3>, (const void*)compose_w_kernel<4>,
+                           (const void*)blockrow_w_kernel<1>, (const void*)blockrow_w_kernel<2>,
+                           (const void*)blockrow_w_kernel<3>, (const void*)blockrow_w_kernel<4>})
+      CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
@@ -217,10 +226,13 @@ struct PanelCfg {
   size_t dyn_engine, dyn_final;
 };
 
-PanelCfg panel_config(int h, int64_t p, int bsel) {
+// generic-engine configuration; few_ctas: the smallest cluster that fits
+// (used by the finalize / swap-loop kernel, which is rarely busy)
+PanelCfg panel_config(int h, int64_t p, int bsel, bool few_ctas = false) {
   PanelCfg g{};
   const int maxc = caps().max_cluster;
   g.C = (int)std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 127) / 128));
+  if (few_ctas) g.C = (int)std::min<int64_t>(maxc, std::max<int64_t>(1, (p + PRRP_MAXCPT * 1024 - 1) / (PRRP_MAXCPT * 1024)));
   g.per = (p + g.C - 1) / g.C;
   if (g.per > (int64_t)PRRP_MAXCPT * 1024) fail(PRRP_ERR_UNSUPPORTED, "panel too tall for the cluster engine");
   g.T = (int)std::min<int64_t>(1024, std::max<int64_t>(32, ((std::min<int64_t>(g.per, 1024) + 31) / 32) * 32));
@@ -237,6 +249,12 @@ PanelCfg panel_config(int h, int64_t p, int bsel) {
   const size_t gepp_need = (size_t)h * h * 8;
   g.dyn_final = std::max({g.dyn_engine, trsm_need, gepp_need});
   return g;
+}
+
+// overflow scratch large enough for both the panel engine and the finalize config
+size_t ovf_elems(int h, int64_t p, int bsel) {
+  const PanelCfg a = panel_config(h, p, bsel), b = panel_config(h, p, bsel, true);
+  return std::max((size_t)a.C * h * std::max<int64_t>(1, a.ovpad), (size_t)b.C * h * std::max<int64_t>(1, b.ovpad));
 }
 
 template <typename K, typename... Args>
@@ -256,6 +274,24 @@ void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Arg
   CU_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
+// PRRP_GENERIC_PANEL=1 forces the generic shared-memory engine (A/B testing)
+bool force_generic_panel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PRRP_GENERIC_PANEL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// PRRP_PANEL_PROF=1: CTA 0 of the fast panel engine accumulates per-phase
+// clock64 totals; printed to stderr at the end of prrp_luprrp.
+thread_local long long* tl_prof = nullptr;
+bool panel_prof_enabled() {
+  const char* e = getenv("PRRP_PANEL_PROF");
+  return e && e[0] == '1';
+}
+
 int swap_cap(int b, int64_t p, double tau) {   // pivoted_qr.py:108-110
   return (int)std::ceil(2.0 * b * std::log((double)std::max<int64_t>(p, 2)) / std::log(tau)) + 10;
 }
@@ -269,6 +305,12 @@ struct PanelBuffers {
   int32_t* moved;
   double* refl;
 };
+
+constexpr int kMaxCand = 1024;   // trsm blocks per panel (candidate slots)
+
+void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_t p, int h, double tau, int ncand,
+                     double* D, int32_t* piv, int32_t* gperm, int32_t* swaps_dev, bool do_gepp, DevState* st,
+                     int panel, cudaStream_t s);
 
 // One strong RRQR of the h x p transposed panel: QRCP (cluster), multipliers
 // (all SMs), swap loop + moved rows (+ optional GEPP of the pivot block).
@@ -299,36 +341,83 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.L21 = L21;
   a.ldl = ldl;
   a.moved = B.moved;
+  a.prof = tl_prof;
   tbegin(PRRP_K_PANEL, s);
-  launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
+  const int maxc = caps().max_cluster;
+  const int64_t c64 = std::max<int64_t>((p + P64_MAXCOLS - 1) / P64_MAXCOLS,
+                                        std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 127) / 128)));
+  if (h == P64_H && c64 <= maxc && !force_generic_panel()) {
+    // register-resident fast engine (h = 64)
+    PanelCfg g64 = g;
+    g64.C = (int)c64;
+    g64.T = P64_T;
+    PanelArgs a64 = a;
+    a64.per = (p + c64 - 1) / c64;
+    const size_t dyn = a64.per > P64_GROUPS ? (size_t)P64_E * P64_T * 8 : 0;
+    launch_cluster(panel_qrcp64_kernel, g64, dyn, s, a64);
+  } else {
+    launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
+  }
   tend(s);
   CU_TRY(cudaGetLastError());
 
   const int64_t ncol = p - bsel;
-  const int tw = 128;
-  const int nblk = ncol > 0 ? (int)((ncol + tw - 1) / tw) : 0;
+  const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TW_WARPS - 1) / TW_WARPS) : 0;
   if (nblk > 0) {
-    const size_t dyn = ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8;
     tbegin(PRRP_K_TRSM, s);
-    trsm_kernel<<<nblk, tw, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+    const size_t dyn = (size_t)bsel * (bsel + 1) / 2 * 8;
+    if (force_generic_panel()) {
+      const int tw = 128;
+      const int nb = (int)((ncol + tw - 1) / tw);
+      // generic path keeps one candidate per 128 positions: at most kMaxCand blocks
+      if (nb > kMaxCand) fail(PRRP_ERR_UNSUPPORTED, "generic trsm path limited to 131072 rows");
+      trsm_kernel<<<nb, tw, dyn + (size_t)bsel * tw * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+      tend(s);
+      CU_TRY(cudaGetLastError());
+      launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
+      return;
+    }
+    switch ((bsel + 31) / 32) {
+      case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
+      case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
+      case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
+      default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
+    }
     tend(s);
     CU_TRY(cudaGetLastError());
   }
+  launch_finalize(a, B, bsel, p, h, tau, nblk, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
+}
+
+void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_t p, int h, double tau, int ncand,
+                     double* D, int32_t* piv, int32_t* gperm, int32_t* swaps_dev, bool do_gepp, DevState* st,
+                     int panel, cudaStream_t s) {
   FinalizeArgs f{};
   f.pa = a;
   f.pa.cand = B.cand;
   f.pa.cand_flat = B.cand_flat;
-  f.pa.ncand = nblk;
+  f.pa.ncand = ncand;
   f.swap_cap = swap_cap(bsel, p, tau);
   f.D = D;
   f.piv = piv;
   f.gperm = gperm;
   f.swaps_dev = swaps_dev;
-  f.do_gepp = do_gepp ? 1 : 0;
+  f.do_gepp = 0;   // the diagonal-block GEPP runs as its own small kernel below
   tbegin(PRRP_K_FINALIZE, s);
-  launch_cluster(panel_finalize_kernel, g, g.dyn_final, s, f);
+  const PanelCfg gf = panel_config(h, p, bsel, true);
+  f.pa.per = gf.per;
+  f.pa.cap = gf.cap;
+  f.pa.cap_pad = gf.cap_pad;
+  f.pa.ovpad = gf.ovpad;
+  launch_cluster(panel_finalize_kernel, gf, gf.dyn_final, s, f);
   tend(s);
   CU_TRY(cudaGetLastError());
+  if (do_gepp) {
+    tbegin(PRRP_K_BLOCKROW, s);
+    gepp_diag_kernel<<<1, 256, (size_t)h * h * 8, s>>>(a.src, a.ld, B.perm, h, D, piv, gperm, st, panel);
+    tend(s);
+    CU_TRY(cudaGetLastError());
+  }
 }
 
 void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* Bm, int64_t ldb, int64_t M,
@@ -451,6 +540,31 @@ DevState* new_state(Arena& ar, cudaStream_t s) {
   return st;
 }
 
+void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const double* D, const int32_t* gperm,
+                      double* out, int64_t ldo, DevState* st, cudaStream_t s) {
+  if (M <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 8, (M + TW_WARPS - 1) / TW_WARPS);
+  const size_t dyn = (size_t)b * b * 8;
+  switch ((b + 31) / 32) {
+    case 1: compose_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
+    case 2: compose_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
+    case 3: compose_w_kernel<3><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
+    default: compose_w_kernel<4><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
+  }
+}
+
+void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, const double* D, const int32_t* gperm,
+                       int64_t* perm, DevState* st, cudaStream_t s) {
+  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 8, (n + TW_WARPS - 1) / TW_WARPS);
+  const size_t dyn = (size_t)b * b * 8;
+  switch ((b + 31) / 32) {
+    case 1: blockrow_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
+    case 2: blockrow_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
+    case 3: blockrow_w_kernel<3><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
+    default: blockrow_w_kernel<4><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
+  }
+}
+
 // ---------------------------------------------------------------- LU_PRRP driver
 int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm,
                 int32_t* swap_counts, prrp_stats* stats, prrp_err* err, prrp_timing* timing, cudaStream_t s) {
@@ -473,9 +587,9 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   PanelBuffers B{};
   B.Rbuf = ar.get<double>((size_t)b * m);
   B.perm = ar.get<int32_t>(m);
-  B.ovf = ar.get<double>((size_t)g0.C * b * std::max<int64_t>(1, g0.ovpad));
-  B.cand = ar.get<double>((m + 127) / 128 + 1);
-  B.cand_flat = ar.get<long long>((m + 127) / 128 + 1);
+  B.ovf = ar.get<double>(ovf_elems(b, m, b));
+  B.cand = ar.get<double>(kMaxCand);
+  B.cand_flat = ar.get<long long>(kMaxCand);
   B.moved = ar.get<int32_t>(2 * m);
   B.refl = nullptr;
   double* D = ar.get<double>((size_t)b * b);
@@ -485,6 +599,11 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
 
   const int sms = caps().sms;
+  tl_prof = nullptr;
+  if (panel_prof_enabled()) {
+    tl_prof = ar.get<long long>(8);
+    CU_TRY(cudaMemsetAsync(tl_prof, 0, 8 * sizeof(long long), s));
+  }
   tbegin(PRRP_K_OTHER, s);
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
   maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
@@ -509,24 +628,37 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
                      width, bj, st, s);
       const int ctw = bj > 64 ? 64 : 128;
       tbegin(PRRP_K_COMPOSE, s);
-      compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, s>>>(
-          L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
+      if (!force_generic_panel())
+        launch_compose_w(L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
+      else
+        compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, s>>>(
+            L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
       tend(s);
       CU_TRY(cudaGetLastError());
     } else {
       tbegin(PRRP_K_BLOCKROW, s);
-      gepp_diag_kernel<<<1, 1024, (size_t)bj * bj * 8, s>>>(blk, lda, bj, D, piv, gperm, st, panel);
+      gepp_diag_kernel<<<1, 256, (size_t)bj * bj * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
       tend(s);
       CU_TRY(cudaGetLastError());
     }
     tbegin(PRRP_K_BLOCKROW, s);
-    blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, s>>>(
-        A, lda, col0, bj, n, D, piv, gperm, perm, st);
+    if (!force_generic_panel())
+      launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+    else
+      blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, s>>>(
+          A, lda, col0, bj, n, D, piv, gperm, perm, st);
     tend(s);
     CU_TRY(cudaGetLastError());
   }
   DevState hs;
   read_state(st, hs, s);
+  if (tl_prof) {
+    long long pr[8];
+    CU_TRY(cudaMemcpy(pr, tl_prof, sizeof(pr), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[prrp panel prof] launches=%lld cycles: reduce=%lld publish+cluster_sync=%lld "
+            "winner+reflector=%lld apply=%lld total=%lld\n", pr[5], pr[0], pr[1], pr[2], pr[3], pr[4]);
+    tl_prof = nullptr;
+  }
   std::vector<int32_t> sw(npanels);
   CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
   if (swap_counts) memcpy(swap_counts, sw.data(), sizeof(int32_t) * npanels);
@@ -636,9 +768,9 @@ int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t
     PanelBuffers B{};
     B.Rbuf = ar.get<double>((size_t)h * p);
     B.perm = ar.get<int32_t>(p);
-    B.ovf = ar.get<double>((size_t)g.C * h * std::max<int64_t>(1, g.ovpad));
-    B.cand = ar.get<double>((p + 127) / 128 + 1);
-    B.cand_flat = ar.get<long long>((p + 127) / 128 + 1);
+    B.ovf = ar.get<double>(ovf_elems(h, p, bsel));
+    B.cand = ar.get<double>(kMaxCand);
+    B.cand_flat = ar.get<long long>(kMaxCand);
     B.moved = ar.get<int32_t>(2 * p);
     const int steps = (int)std::min<int64_t>(h, p);
     B.refl = ar.get<double>((size_t)steps * (h + 1));
@@ -741,7 +873,7 @@ int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* pe
     int32_t* gperm = ar.get<int32_t>(m);
     iota_kernel<<<1, 128, 0, s>>>(perm, m);
     maxabs_kernel<<<caps().sms, 256, 0, s>>>(A, lda, m, n, st);
-    gepp_diag_kernel<<<1, 1024, (size_t)m * m * 8, s>>>(A, lda, m, D, piv, gperm, st, 0);
+    gepp_diag_kernel<<<1, 256, (size_t)m * m * 8, s>>>(A, lda, nullptr, m, D, piv, gperm, st, 0);
     blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)m * m + (size_t)m * BR_TW) * 8, s>>>(
         A, lda, 0, m, n, D, piv, gperm, perm, st);
     CU_TRY(cudaGetLastError());

@@ -134,13 +134,19 @@ int main() {
     printf("grid P=%3d: fence+atomic %.3f us/step | red.release %.3f us/step | flags %.3f us/step\n", P,
            ms[0] * 1e3 / steps, ms[1] * 1e3 / steps, ms[2] * 1e3 / steps);
   }
-  {
+  for (int cs : {2, 4, 8}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs); cfg.blockDim = dim3(256); cfg.stream = 0;
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
     float ms;
     CK(cudaEventRecord(e0));
-    exch_cluster<8><<<dim3(8), 256>>>(steps, b, sink);
+    if (cs == 2) CK(cudaLaunchKernelEx(&cfg, exch_cluster<2>, steps, b, sink));
+    if (cs == 4) CK(cudaLaunchKernelEx(&cfg, exch_cluster<4>, steps, b, sink));
+    if (cs == 8) CK(cudaLaunchKernelEx(&cfg, exch_cluster<8>, steps, b, sink));
     CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); CK(cudaGetLastError());
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    printf("cluster 8: %.3f us/step\n", ms * 1e3 / steps);
+    printf("cluster %d: %.3f us/step\n", cs, ms * 1e3 / steps);
   }
   {
     auto fn = exch_cluster<16>;
