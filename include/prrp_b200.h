@@ -82,9 +82,10 @@ enum prrp_kclass {
   PRRP_K_PERMUTE = 3,    /* permute_kernel                                 */
   PRRP_K_SCHUR = 4,      /* schur_dmma_kernel / schur_simt_kernel          */
   PRRP_K_COMPOSE = 5,    /* compose_kernel                                 */
-  PRRP_K_BLOCKROW = 6,   /* blockrow_kernel / gepp_diag_kernel             */
-  PRRP_K_OTHER = 7,      /* init kernels                                   */
-  PRRP_K_COUNT = 8
+  PRRP_K_BLOCKROW = 6,   /* blockrow kernels (GEPP finish of the block row) */
+  PRRP_K_GEPP = 7,       /* gepp_diag_kernel (b x b diagonal block GEPP)   */
+  PRRP_K_OTHER = 8,      /* init kernels                                   */
+  PRRP_K_COUNT = 9
 };
 
 typedef struct prrp_timing {

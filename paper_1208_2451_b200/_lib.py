@@ -34,11 +34,11 @@ class PrrpStats(ctypes.Structure):
                 ("total_swaps", ctypes.c_int64)]
 
 
-KCLASSES = ("panel", "trsm", "finalize", "permute", "schur", "compose", "blockrow", "other")
+KCLASSES = ("panel", "trsm", "finalize", "permute", "schur", "compose", "blockrow", "gepp", "other")
 
 
 class PrrpTiming(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 8), ("launches", ctypes.c_int32 * 8),
+    _fields_ = [("ms", ctypes.c_double * 9), ("launches", ctypes.c_int32 * 9),
                 ("schur_flops", ctypes.c_double), ("total_ms", ctypes.c_double)]
 
 

@@ -134,17 +134,22 @@ __global__ void __launch_bounds__(TRSM_TW) trsm_kernel(const double* Rbuf, int64
 // ---------------------------------------------------------------------------
 __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, int b, double* c /* smem b*b */,
                           double* D, int32_t* piv, int32_t* gperm, DevState* st, int panel, double* red) {
+  // thread j owns column j for the swaps and the rank-1 updates (consecutive
+  // threads touch consecutive words: no bank conflicts, no index division);
+  // warp 0 runs the first-max pivot search of column k.
   const int t = threadIdx.x, T = blockDim.x;
+  const int bp = b + 1;   // odd pitch: row and column walks are both bank-conflict free
   __shared__ int s_piv;
   __shared__ double s_colmax;
   __shared__ int s_gp[PRRP_MAXH];
   double mx = 0.0;
-  for (int idx = t; idx < b * b; idx += T) {
-    const int i = idx / b, j = idx % b;
+  for (int i = 0; i < b; ++i) {
     const int64_t row = rowmap ? rowmap[i] : i;
-    const double v = src[row * ld + j];
-    c[idx] = v;
-    mx = fmax(mx, fabs(v));
+    for (int j = t; j < b; j += T) {
+      const double v = src[row * ld + j];
+      c[i * bp + j] = v;
+      mx = fmax(mx, fabs(v));
+    }
   }
   if (t < b) s_gp[t] = t;
   __syncthreads();
@@ -153,7 +158,7 @@ __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, 
       double best = -1.0;
       int bi = INT_MAX;
       for (int i = k + t; i < b; i += 32) {
-        const double v = fabs(c[i * b + k]);
+        const double v = fabs(c[i * bp + k]);
         if (v > best) { best = v; bi = i; }
       }
       for (int o = 16; o; o >>= 1) {
@@ -171,29 +176,43 @@ __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, 
     }
     if (pv != k) {
       for (int j = t; j < b; j += T) {
-        const double x = c[k * b + j];
-        c[k * b + j] = c[pv * b + j];
-        c[pv * b + j] = x;
+        const double x = c[k * bp + j];
+        c[k * bp + j] = c[pv * bp + j];
+        c[pv * bp + j] = x;
       }
       if (t == 0) { const int g = s_gp[k]; s_gp[k] = s_gp[pv]; s_gp[pv] = g; }
     }
     if (t == 0) piv[k] = pv;
     __syncthreads();
     if (k + 1 < b) {
-      const double ckk = c[k * b + k];
-      for (int i = k + 1 + t; i < b; i += T) c[i * b + k] = div_rn(c[i * b + k], ckk);
+      const double ckk = c[k * bp + k];
+      for (int i = k + 1 + t; i < b; i += T) c[i * bp + k] = div_rn(c[i * bp + k], ckk);
       __syncthreads();
-      const int w = b - k - 1;
-      for (int idx = t; idx < w * w; idx += T) {
-        const int i = k + 1 + idx / w, j = k + 1 + idx % w;
-        const double v = sub_rn(c[i * b + j], mul_rn(c[i * b + k], c[k * b + j]));
-        c[i * b + j] = v;
-        mx = fmax(mx, fabs(v));
+      for (int j = k + 1 + t; j < b; j += T) {
+        const double ckj = c[k * bp + j];
+        int i = k + 1;
+        for (; i + 8 <= b; i += 8) {       // batch the loads: no smem load->store chains
+          double cv[8], lv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) { cv[u] = c[(i + u) * bp + j]; lv[u] = c[(i + u) * bp + k]; }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            cv[u] = sub_rn(cv[u], mul_rn(lv[u], ckj));
+            mx = fmax(mx, fabs(cv[u]));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) c[(i + u) * bp + j] = cv[u];
+        }
+        for (; i < b; ++i) {
+          const double v = sub_rn(c[i * bp + j], mul_rn(c[i * bp + k], ckj));
+          c[i * bp + j] = v;
+          mx = fmax(mx, fabs(v));
+        }
       }
     }
     __syncthreads();
   }
-  for (int idx = t; idx < b * b; idx += T) D[idx] = c[idx];
+  for (int idx = t; idx < b * b; idx += T) D[idx] = c[(idx / b) * bp + idx % b];
   if (t < b) gperm[t] = s_gp[t];
   const double m = block_max(mx, red);
   if (t == 0) atomic_max_abs(&st->finish_max, m);

@@ -98,8 +98,17 @@ __device__ __forceinline__ double warp_pairwise_sq(const double* x, int n) {
     const int full = n - (n % 8);
     double r = 0.0;
     if (lane < 8) {
-      r = sq_rn(x[lane]);
-      for (int i = lane + 8; i < full; i += 8) r = add_rn(r, sq_rn(x[i]));
+      // loads first (independent), then the dependent chain
+      double v[PRRP_MAXH / 8];
+#pragma unroll
+      for (int u = 0; u < PRRP_MAXH / 8; ++u) {
+        const int i = lane + 8 * u;
+        v[u] = i < full ? x[i] : 0.0;
+      }
+      r = sq_rn(v[0]);
+#pragma unroll
+      for (int u = 1; u < PRRP_MAXH / 8; ++u)
+        if (lane + 8 * u < full) r = add_rn(r, sq_rn(v[u]));
     }
     r = add_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
     r = add_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));

@@ -313,7 +313,9 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
       }
       __syncwarp();
       const int L = P64_H - k;
-      const double normx = __dsqrt_rn(warp_pairwise_sq(S.xs + k, L));
+      // mode 0: the winner's key IS (x*x).sum() over rows k..63 in numpy's
+      // pairwise order (same elements, same order as _reflect's normx)
+      const double normx = __dsqrt_rn(mode == 0 ? r.key : warp_pairwise_sq(S.xs + k, L));
       int skip = normx == 0.0;
       double alpha = 0.0, beta = 0.0;
       if (!skip) {
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
     const bool mine = S.wc == c;
     const int wjl = S.wjl;
     const long long wpos = S.wpos;
-    {
+    // warps whose columns are all absent or finished skip the work (warp-uniform)
+    if (__any_sync(0xffffffffu, on_r && pos_r >= k)) {
       const bool live = on_r && pos_r >= k;
       const bool win = live && mine && wjl == jl_r;
       if (live && !win && pos_r == k) pos_r = wpos;        // displaced by the interchange
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
         key_r = pos_r == k + 1 ? 1.0 : -1.0;
       }
     }
-    if (has_s) {
+    if (has_s && __any_sync(0xffffffffu, on_s && pos_s >= k)) {
       const bool live = on_s && pos_s >= k;
       const bool win = live && mine && wjl == jl_s;
       if (live && !win && pos_s == k) pos_s = wpos;

@@ -20,6 +20,7 @@
 #include "panel.cuh"
 #include "lsolve.cuh"
 #include "panel64.cuh"
+#include "panel1.cuh"
 #include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
@@ -79,7 +80,7 @@ DeviceCaps& caps() {
     CU_TRY(cudaGetDevice(&dev));
     CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
-                           (const void*)panel_qrcp64_kernel}) {
+                           (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel}) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
     }
@@ -344,17 +345,18 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.prof = tl_prof;
   tbegin(PRRP_K_PANEL, s);
   const int maxc = caps().max_cluster;
-  const int64_t c64 = std::max<int64_t>((p + P64_MAXCOLS - 1) / P64_MAXCOLS,
-                                        std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 127) / 128)));
-  if (h == P64_H && c64 <= maxc && !force_generic_panel()) {
-    // register-resident fast engine (h = 64)
-    PanelCfg g64 = g;
-    g64.C = (int)c64;
-    g64.T = P64_T;
-    PanelArgs a64 = a;
-    a64.per = (p + c64 - 1) / c64;
-    const size_t dyn = a64.per > P64_GROUPS ? (size_t)P64_E * P64_T * 8 : 0;
-    launch_cluster(panel_qrcp64_kernel, g64, dyn, s, a64);
+  const int64_t c1 = std::max<int64_t>((p + P1_MAXCOLS - 1) / P1_MAXCOLS,
+                                       std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 31) / 32)));
+  const bool aligned = ((uintptr_t)src % 16 == 0) && (ld % 2 == 0);
+  if (h == P1_H && c1 <= maxc && aligned && !force_generic_panel()) {
+    // thread-per-column register engine (h = 64)
+    PanelCfg g1 = g;
+    g1.C = (int)c1;
+    g1.T = P1_T;
+    PanelArgs a1 = a;
+    a1.per = (p + c1 - 1) / c1;
+    const size_t dyn = a1.per > P1_T ? (size_t)P1_H * P1_T * 8 : 0;
+    launch_cluster(panel_qrcp1_kernel, g1, dyn, s, a1);
   } else {
     launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
   }
@@ -362,16 +364,16 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   CU_TRY(cudaGetLastError());
 
   const int64_t ncol = p - bsel;
-  const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TW_WARPS - 1) / TW_WARPS) : 0;
+  const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TC - 1) / TC) : 0;
   if (nblk > 0) {
     tbegin(PRRP_K_TRSM, s);
-    const size_t dyn = (size_t)bsel * (bsel + 1) / 2 * 8;
+    const size_t dyn = (((size_t)bsel * (bsel + 1) / 2 + 1) / 2 * 2 + (size_t)bsel * TCP) * 8;
     if (force_generic_panel()) {
       const int tw = 128;
       const int nb = (int)((ncol + tw - 1) / tw);
       // generic path keeps one candidate per 128 positions: at most kMaxCand blocks
       if (nb > kMaxCand) fail(PRRP_ERR_UNSUPPORTED, "generic trsm path limited to 131072 rows");
-      trsm_kernel<<<nb, tw, dyn + (size_t)bsel * tw * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+      trsm_kernel<<<nb, tw, ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
@@ -413,8 +415,8 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
   tend(s);
   CU_TRY(cudaGetLastError());
   if (do_gepp) {
-    tbegin(PRRP_K_BLOCKROW, s);
-    gepp_diag_kernel<<<1, 256, (size_t)h * h * 8, s>>>(a.src, a.ld, B.perm, h, D, piv, gperm, st, panel);
+    tbegin(PRRP_K_GEPP, s);
+    gepp_diag_kernel<<<1, 128, (size_t)h * (h + 1) * 8, s>>>(a.src, a.ld, B.perm, h, D, piv, gperm, st, panel);
     tend(s);
     CU_TRY(cudaGetLastError());
   }
@@ -543,8 +545,8 @@ DevState* new_state(Arena& ar, cudaStream_t s) {
 void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const double* D, const int32_t* gperm,
                       double* out, int64_t ldo, DevState* st, cudaStream_t s) {
   if (M <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 8, (M + TW_WARPS - 1) / TW_WARPS);
-  const size_t dyn = (size_t)b * b * 8;
+  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 4, (M + TC - 1) / TC);
+  const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
     case 1: compose_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
     case 2: compose_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
@@ -555,14 +557,40 @@ void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const do
 
 void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, const double* D, const int32_t* gperm,
                        int64_t* perm, DevState* st, cudaStream_t s) {
-  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 8, (n + TW_WARPS - 1) / TW_WARPS);
-  const size_t dyn = (size_t)b * b * 8;
+  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 4, (n + TC - 1) / TC);
+  const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
     case 1: blockrow_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
     case 2: blockrow_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
     case 3: blockrow_w_kernel<3><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
     default: blockrow_w_kernel<4><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
   }
+}
+
+// Per-thread internal streams (main: high priority, side: low priority) and a
+// reusable pool of dependency events.
+struct Streams {
+  cudaStream_t main = nullptr, side = nullptr;
+  std::vector<cudaEvent_t> evs;
+  cudaEvent_t ev(int i) {
+    while ((int)evs.size() <= i) {
+      cudaEvent_t e;
+      CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+    }
+    return evs[i];
+  }
+};
+
+Streams& streams() {
+  thread_local Streams s;
+  if (!s.main) {
+    int lo = 0, hi = 0;
+    CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU_TRY(cudaStreamCreateWithPriority(&s.main, cudaStreamNonBlocking, hi));
+    CU_TRY(cudaStreamCreateWithPriority(&s.side, cudaStreamNonBlocking, lo));
+  }
+  return s;
 }
 
 // ---------------------------------------------------------------- LU_PRRP driver
@@ -610,45 +638,91 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   tend(s);
   CU_TRY(cudaGetLastError());
 
+  // ---- look-ahead schedule over two streams:
+  //   main (high priority, critical path): QRCP(k) -> trsm -> finalize ->
+  //        [wait side(k-1)] -> permute(k) -> narrow Schur(k) (panel k+1's columns)
+  //   side (low priority): [wait permute(k)] wide Schur(k) -> GEPP of A11 ->
+  //        compose(k) -> [wait narrow(k)] blockrow(k)
+  // so QRCP(k+1) overlaps the trailing update and the finish of panel k.
+  Streams& ss = streams();
+  cudaStream_t sm = ss.main, sd = ss.side;
+  {
+    cudaEvent_t e0 = ss.ev(0);
+    CU_TRY(cudaEventRecord(e0, s));
+    CU_TRY(cudaStreamWaitEvent(sm, e0, 0));
+    CU_TRY(cudaStreamWaitEvent(sd, e0, 0));
+  }
+  double* L21b[2] = {L21, ar.get<double>((size_t)b * ldl)};
+  cudaEvent_t side_done = nullptr;
+  int evi = 1;
   int panel = 0;
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
     const int64_t rows = m - col0;
     const int64_t width = n - col0 - bj;
     double* blk = A + col0 * lda + col0;
+    double* L = L21b[panel & 1];
     if (rows > bj) {
-      strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L21, ldl, B, st, swaps_dev, D, piv, gperm, true, s);
-      tbegin(PRRP_K_PERMUTE, s);
-      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
+      strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L, ldl, B, st, swaps_dev, D, piv, gperm, false, sm);
+      if (side_done) CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
+      tbegin(PRRP_K_PERMUTE, sm);
+      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, sm>>>(
           A, lda, col0, n, B.moved, perm, st, panel);
-      tend(s);
+      tend(sm);
       CU_TRY(cudaGetLastError());
-      if (width > 0)
-        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L21, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
-                     width, bj, st, s);
+      cudaEvent_t ev_perm = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_perm, sm));
+      // narrow update: the next panel's b columns, on the critical path
+      const int64_t wn = std::min<int64_t>(width, b);
+      if (wn > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
+                     bj, st, sm);
+      cudaEvent_t ev_narrow = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_narrow, sm));
+      // side stream: wide update, diagonal-block GEPP, compose, block row
+      CU_TRY(cudaStreamWaitEvent(sd, ev_perm, 0));
+      if (width > wn)
+        schur_update(A + (col0 + bj) * lda + col0 + bj + wn, lda, L, ldl, A + col0 * lda + col0 + bj + wn, lda,
+                     rows - bj, width - wn, bj, st, sd);
+      tbegin(PRRP_K_GEPP, sd);
+      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, sd>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      tend(sd);
+      CU_TRY(cudaGetLastError());
       const int ctw = bj > 64 ? 64 : 128;
-      tbegin(PRRP_K_COMPOSE, s);
+      tbegin(PRRP_K_COMPOSE, sd);
       if (!force_generic_panel())
-        launch_compose_w(L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
+        launch_compose_w(L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, sd);
       else
-        compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, s>>>(
-            L21, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
-      tend(s);
+        compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, sd>>>(
+            L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
+      tend(sd);
       CU_TRY(cudaGetLastError());
+      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
     } else {
-      tbegin(PRRP_K_BLOCKROW, s);
-      gepp_diag_kernel<<<1, 256, (size_t)bj * bj * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
-      tend(s);
+      if (side_done) CU_TRY(cudaStreamWaitEvent(sd, side_done, 0));
+      tbegin(PRRP_K_GEPP, sd);
+      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, sd>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      tend(sd);
       CU_TRY(cudaGetLastError());
     }
-    tbegin(PRRP_K_BLOCKROW, s);
+    tbegin(PRRP_K_BLOCKROW, sd);
     if (!force_generic_panel())
-      launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+      launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, sd);
     else
-      blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, s>>>(
+      blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)bj * bj + (size_t)bj * BR_TW) * 8, sd>>>(
           A, lda, col0, bj, n, D, piv, gperm, perm, st);
-    tend(s);
+    tend(sd);
     CU_TRY(cudaGetLastError());
+    side_done = ss.ev(evi++);
+    CU_TRY(cudaEventRecord(side_done, sd));
+  }
+  CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
+  tbegin(PRRP_K_OTHER, sm);   // closing mark for the timer span
+  tend(sm);
+  {
+    cudaEvent_t e1 = ss.ev(evi++);
+    CU_TRY(cudaEventRecord(e1, sm));
+    CU_TRY(cudaStreamWaitEvent(s, e1, 0));
   }
   DevState hs;
   read_state(st, hs, s);
@@ -873,7 +947,7 @@ int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* pe
     int32_t* gperm = ar.get<int32_t>(m);
     iota_kernel<<<1, 128, 0, s>>>(perm, m);
     maxabs_kernel<<<caps().sms, 256, 0, s>>>(A, lda, m, n, st);
-    gepp_diag_kernel<<<1, 256, (size_t)m * m * 8, s>>>(A, lda, nullptr, m, D, piv, gperm, st, 0);
+    gepp_diag_kernel<<<1, 128, (size_t)m * (m + 1) * 8, s>>>(A, lda, nullptr, m, D, piv, gperm, st, 0);
     blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)m * m + (size_t)m * BR_TW) * 8, s>>>(
         A, lda, 0, m, n, D, piv, gperm, perm, st);
     CU_TRY(cudaGetLastError());
