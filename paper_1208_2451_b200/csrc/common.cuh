@@ -58,6 +58,21 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 
+// Correctly rounded a / b from y = __drcp_rn(b) (the correctly rounded
+// reciprocal) and one FMA correction (Markstein): q = RN(a*y),
+// r = a - b*q (exact), RN(q + r*y) == RN(a/b).  Validated bit-exact against
+// __ddiv_rn on 9.1e8 random operand pairs on B200
+// (tools/probes/probe_div.cu).  Outside the normal range (overflow, results
+// near underflow, NaN/Inf) it falls back to the IEEE division.
+__device__ __forceinline__ double div_fast(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = fma(-b, q, a);
+  const double qq = fma(r, y, q);
+  const double aq = fabs(qq);
+  if (!(aq < 1e300 && (aq > 1e-290 || a == 0.0))) return __ddiv_rn(a, b);
+  return qq;
+}
+
 // "a is a better pivot candidate than b": larger key, ties to the smaller position
 // (np.argmax returns the first maximum; pivoted_qr.py:82, gepp.py:49).
 __device__ __forceinline__ bool better(double ka, long long pa, double kb, long long pb) {

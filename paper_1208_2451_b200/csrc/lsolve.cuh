@@ -186,7 +186,8 @@ __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, 
     __syncthreads();
     if (k + 1 < b) {
       const double ckk = c[k * bp + k];
-      for (int i = k + 1 + t; i < b; i += T) c[i * bp + k] = div_rn(c[i * bp + k], ckk);
+      const double yk = __drcp_rn(ckk);
+      for (int i = k + 1 + t; i < b; i += T) c[i * bp + k] = div_fast(c[i * bp + k], ckk, yk);
       __syncthreads();
       for (int j = k + 1 + t; j < b; j += T) {
         const double ckj = c[k * bp + j];

@@ -61,7 +61,10 @@ struct P1Smem {
   __device__ __forceinline__ void st(int i, double v) const { sts_f64(base + (uint32_t)i * (P1_T * 8), v); }
 };
 
-// numpy pairwise sum of squares of rows k+1 .. 63 (k = -1: the whole column)
+// numpy pairwise sum of squares of rows k+1 .. 63 (k = -1: the whole column).
+// Blocks of 8 rows are classified with warp-uniform branches (k is uniform):
+// blocks above row k+1 are skipped, interior blocks run unpredicated, only the
+// boundary block and the last block carry per-row predicates.
 template <class X>
 __device__ __forceinline__ double p1_norm(const X& x, int k) {
   const int n = P1_H - k - 1;
@@ -74,12 +77,21 @@ __device__ __forceinline__ double p1_norm(const X& x, int k) {
 #pragma unroll
   for (int B = 0; B < 8; ++B) {
     if (B < kb) continue;
+    if (B > kb && B < 7) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int i = 8 * B + s;
-      const double v = x.ld(i);
-      const double sq = mul_rn(v, v);
-      if (i >= k + 1 && i < lim) S[s] = add_rn(S[s], sq);
+      for (int s = 0; s < 8; ++s) {
+        const double v = x.ld(8 * B + s);
+        S[s] = add_rn(S[s], mul_rn(v, v));
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int i = 8 * B + s;
+        if (i >= k + 1 && i < lim) {
+          const double v = x.ld(i);
+          S[s] = add_rn(S[s], mul_rn(v, v));
+        }
+      }
     }
   }
   double res = -0.0;
@@ -92,9 +104,9 @@ __device__ __forceinline__ double p1_norm(const X& x, int k) {
     const double t4 = c ? s4 : r4, t5 = c ? s5 : r5, t6 = c ? s6 : r6, t7 = c ? s7 : r7; \
     r0 = t0; r1 = t1; r2 = t2; r3 = t3; r4 = t4; r5 = t5; r6 = t6; r7 = t7;              \
   }
-    P1_ROT((o & 1) != 0, r1, r2, r3, r4, r5, r6, r7, r0)
-    P1_ROT((o & 2) != 0, r2, r3, r4, r5, r6, r7, r0, r1)
-    P1_ROT((o & 4) != 0, r4, r5, r6, r7, r0, r1, r2, r3)
+    if (o & 1) P1_ROT(true, r1, r2, r3, r4, r5, r6, r7, r0)
+    if (o & 2) P1_ROT(true, r2, r3, r4, r5, r6, r7, r0, r1)
+    if (o & 4) P1_ROT(true, r4, r5, r6, r7, r0, r1, r2, r3)
 #undef P1_ROT
     res = add_rn(add_rn(add_rn(r0, r1), add_rn(r2, r3)), add_rn(add_rn(r4, r5), add_rn(r6, r7)));
   }
@@ -116,10 +128,15 @@ __device__ __forceinline__ void p1_apply(const X& x, int k, const double* vs, do
 #pragma unroll
   for (int B = 0; B < 8; ++B) {
     if (B < kb) continue;
+    if (B > kb) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int i = 8 * B + s;
-      if (i >= k) d[s & 3] = fma(vs[i], x.ld(i), d[s & 3]);
+      for (int s = 0; s < 8; ++s) d[s & 3] = fma(vs[8 * B + s], x.ld(8 * B + s), d[s & 3]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int i = 8 * B + s;
+        if (i >= k) d[s & 3] = fma(vs[i], x.ld(i), d[s & 3]);
+      }
     }
   }
   const double dot = (d[0] + d[1]) + (d[2] + d[3]);
@@ -127,10 +144,18 @@ __device__ __forceinline__ void p1_apply(const X& x, int k, const double* vs, do
 #pragma unroll
   for (int B = 0; B < 8; ++B) {
     if (B < kb) continue;
+    if (B > kb) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int i = 8 * B + s;
-      if (i >= k) x.st(i, sub_rn(x.ld(i), mul_rn(vs[i], w)));
+      for (int s = 0; s < 8; ++s) {
+        const int i = 8 * B + s;
+        x.st(i, sub_rn(x.ld(i), mul_rn(vs[i], w)));
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int i = 8 * B + s;
+        if (i >= k) x.st(i, sub_rn(x.ld(i), mul_rn(vs[i], w)));
+      }
     }
   }
 }

@@ -307,7 +307,7 @@ struct PanelBuffers {
   double* refl;
 };
 
-constexpr int kMaxCand = 1024;   // trsm blocks per panel (candidate slots)
+constexpr int kMaxCand = 2048;   // trsm blocks per panel (candidate slots)
 
 void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_t p, int h, double tau, int ncand,
                      double* D, int32_t* piv, int32_t* gperm, int32_t* swaps_dev, bool do_gepp, DevState* st,
@@ -364,10 +364,10 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   CU_TRY(cudaGetLastError());
 
   const int64_t ncol = p - bsel;
-  const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TC - 1) / TC) : 0;
+  const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC) : 0;
   if (nblk > 0) {
     tbegin(PRRP_K_TRSM, s);
-    const size_t dyn = (((size_t)bsel * (bsel + 1) / 2 + 1) / 2 * 2 + (size_t)bsel * TCP) * 8;
+    const size_t dyn = (((size_t)bsel * (bsel + 1) / 2 + 1) / 2 * 2 + (size_t)bsel * TTCP) * 8;
     if (force_generic_panel()) {
       const int tw = 128;
       const int nb = (int)((ncol + tw - 1) / tw);
@@ -679,8 +679,10 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
                      bj, st, sm);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
-      // side stream: wide update, diagonal-block GEPP, compose, block row
-      CU_TRY(cudaStreamWaitEvent(sd, ev_perm, 0));
+      // side stream: wide update, diagonal-block GEPP, compose, block row.  It
+      // is released only after the narrow update, i.e. together with QRCP(k+1)
+      // on the high-priority stream, so the panel cluster claims its GPC first.
+      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
       if (width > wn)
         schur_update(A + (col0 + bj) * lda + col0 + bj + wn, lda, L, ldl, A + col0 * lda + col0 + bj + wn, lda,
                      rows - bj, width - wn, bj, st, sd);
@@ -697,7 +699,6 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
             L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
       tend(sd);
       CU_TRY(cudaGetLastError());
-      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
     } else {
       if (side_done) CU_TRY(cudaStreamWaitEvent(sd, side_done, 0));
       tbegin(PRRP_K_GEPP, sd);

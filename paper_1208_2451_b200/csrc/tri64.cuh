@@ -31,28 +31,34 @@ __device__ __forceinline__ double lane_pick(const double (&x)[NR], int row) {
   return __shfl_sync(0xffffffffu, v, row & 31);
 }
 
+// trsm tile: one column per warp (latency-bound chain of bsel divisions)
+#define TTC TW_WARPS
+#define TTCP (TTC + 1)
+
 template <int NR>
 __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                               double* L21, int64_t ldl, double* cand,
                                                               long long* cand_flat, DevState* st, int panel) {
   extern __shared__ __align__(16) double sm[];
   double* r11 = sm;                                    // packed upper, bsel(bsel+1)/2
-  double* tile = sm + ((bsel * (bsel + 1) / 2 + 1) & ~1);   // bsel x TCP
+  double* tile = sm + ((bsel * (bsel + 1) / 2 + 1) & ~1);   // bsel x TTCP
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
+  __shared__ double rcp[PRRP_MAXH];
   if (prrp_failed(st)) return;
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
+  for (int i = threadIdx.x; i < bsel; i += blockDim.x) rcp[i] = __drcp_rn(r11[upk(i, i)]);
   if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, st->fro, st, panel, true);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t ncol = p - bsel;
   double worst = -1.0;
   long long wflat = LLONG_MAX;
-  for (int64_t c0 = (int64_t)blockIdx.x * TC; c0 < ncol; c0 += (int64_t)gridDim.x * TC) {
-    const int tc = (int)min((int64_t)TC, ncol - c0);
-    for (int e = t; e < bsel * TC; e += blockDim.x) {
-      const int i = e / TC, cc = e % TC;
-      if (cc < tc) tile[i * TCP + cc] = Rbuf[(int64_t)i * p + bsel + c0 + cc];
+  for (int64_t c0 = (int64_t)blockIdx.x * TTC; c0 < ncol; c0 += (int64_t)gridDim.x * TTC) {
+    const int tc = (int)min((int64_t)TTC, ncol - c0);
+    for (int e = t; e < bsel * TTC; e += blockDim.x) {
+      const int i = e / TTC, cc = e % TTC;
+      if (cc < tc) tile[i * TTCP + cc] = Rbuf[(int64_t)i * p + bsel + c0 + cc];
     }
     __syncthreads();
     for (int cc = warp; cc < tc; cc += TW_WARPS) {
@@ -60,10 +66,10 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
 #pragma unroll
       for (int u = 0; u < NR; ++u) {
         const int i = lane + 32 * u;
-        x[u] = i < bsel ? tile[i * TCP + cc] : 0.0;
+        x[u] = i < bsel ? tile[i * TTCP + cc] : 0.0;
       }
       for (int i = bsel - 1; i >= 0; --i) {
-        const double xi = div_rn(lane_pick(x, i), r11[upk(i, i)]);
+        const double xi = div_fast(lane_pick(x, i), r11[upk(i, i)], rcp[i]);
         const double* rc = r11 + upk(0, i);
 #pragma unroll
         for (int u = 0; u < NR; ++u) {
@@ -77,7 +83,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
       for (int u = 0; u < NR; ++u) {
         const int i = lane + 32 * u;
         if (i < bsel) {
-          tile[i * TCP + cc] = x[u];
+          tile[i * TTCP + cc] = x[u];
           const double ax = fabs(x[u]);
           const long long fl = (long long)i * ncol + jj;
           if (ax > worst || (ax == worst && fl < wflat)) { worst = ax; wflat = fl; }
@@ -85,9 +91,9 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
       }
     }
     __syncthreads();
-    for (int e = t; e < bsel * TC; e += blockDim.x) {
-      const int i = e / TC, cc = e % TC;
-      if (cc < tc) L21[(int64_t)i * ldl + c0 + cc] = tile[i * TCP + cc];
+    for (int e = t; e < bsel * TTC; e += blockDim.x) {
+      const int i = e / TTC, cc = e % TTC;
+      if (cc < tc) L21[(int64_t)i * ldl + c0 + cc] = tile[i * TTCP + cc];
     }
     __syncthreads();
   }

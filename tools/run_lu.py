@@ -35,7 +35,7 @@ def main():
                                    sw, ctypes.byref(st), ctypes.byref(err), ctypes.byref(tm), _lib.stream_handle())
         dt = time.perf_counter() - t0
         _lib.raise_for(rc, err, "luprrp")
-        print(f"rep {r}: {dt*1e3:.2f} ms wall; breakdown", {k: round(tm.ms[i], 3) for i, k in enumerate(_lib.KCLASSES)},
+        print(f"rep {r}: {dt*1e3:.2f} ms wall, {tm.total_ms:.2f} ms device; breakdown", {k: round(tm.ms[i], 3) for i, k in enumerate(_lib.KCLASSES)},
               "growth", st.intermediate_max / st.original_max, flush=True)
 
 
