@@ -124,9 +124,12 @@ int prrp_b200_dmma_peak(double ms, double* tflops, prrp_err* err);
 
 /* CALU_PRRP factorization with a binary tournament tree of `leaf_count`
  * leaves — replaces prrp.caluprrp_factor(a, b, tau, binary_tree(P))
- * (tournament.py:237-296).  Arguments as prrp_luprrp. */
+ * (tournament.py:237-296).  Arguments as prrp_luprrp, plus
+ * tournament_charge3 (host int64[ceil(n/b)], may be NULL): 3x the
+ * tournament flop charge of each panel (tournament.py:224-234), -1 for a
+ * single-node panel, so the caller can rebuild the exact rational counters. */
 int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
-                  int32_t leaf_count, int64_t* perm, int32_t* swap_counts,
+                  int32_t leaf_count, int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3,
                   prrp_stats* stats, prrp_err* err, void* stream);
 
 /* Strong RRQR of an h x p matrix `a` (column-major, lda >= h) with leading

@@ -53,7 +53,7 @@ SIGNATURES = {
     "prrp_luprrp": ([_P, _I64, _I64, _I64, _I32, _D, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_luprrp_timed": ([_P, _I64, _I64, _I64, _I32, _D, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_b200_dmma_peak": ([_D, _P, _P], ctypes.c_int),
-    "prrp_caluprrp": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_caluprrp": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_strong_rrqr": ([_P, _I64, _I32, _I64, _I32, _D, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_householder_qr": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
     "prrp_schur_update": ([_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I32, _P, _P, _P], ctypes.c_int),

@@ -1,0 +1,254 @@
+// CALU_PRRP: tournament pivoting over a binary tree of strong RRQRs
+// (tournament.py:155-217, 237-296) on the device.
+//
+// Rows stay in PHYSICAL slots; the factorization's logical row order of the
+// trailing region is kept in pos2row (logical position -> physical row).
+// Per panel only the b pivot rows move (into slots col0..col0+b, in selection
+// order) and the rows they displace take the vacated slots, so the stable
+// partition "[pivots, rest ascending]" (tournament.py:214-215) costs O(b) row
+// moves instead of O(rows).  Leaves are contiguous LOGICAL blocks
+// (tournament.py:64-88); every node is the same cluster QRCP engine fed with
+// an index list.  L21 is produced in logical order and scattered to physical
+// slots for the Schur update.  Once a panel is finished its rows sit at
+// slots == logical positions, so the factors need no final gather (m == n).
+#pragma once
+#include "lsolve.cuh"
+
+// node input rows for a merge level: lpos_in[node][0..2b) = children's
+// candidates (panel-relative logical positions); rowidx = physical rows
+__global__ void calu_merge_inputs_kernel(const int32_t* cands, int b, int nchild, int32_t* lpos_in,
+                                         int64_t* rowidx, const int64_t* pos2row, int64_t col0, int stride) {
+  const int node = blockIdx.x;
+  for (int t = threadIdx.x; t < 2 * b; t += blockDim.x) {
+    const int child = 2 * node + t / b;
+    if (child >= nchild) continue;
+    const int32_t lp = cands[child * b + (t % b)];
+    lpos_in[node * stride + t] = lp;
+    rowidx[node * stride + t] = pos2row[col0 + lp];
+  }
+}
+
+// selected candidates of each node: cands_out[node][q] = lpos(node, perm[q]), q < b.
+// Leaves (lpos_in == nullptr): lpos(node, j) = leaf_lo[node] + j.
+__global__ void calu_select_kernel(const int32_t* const* perms, const int32_t* lpos_in, const int64_t* leaf_lo,
+                                   int b, int32_t* cands_out, int stride) {
+  const int node = blockIdx.x;
+  const int32_t* perm = perms[node];
+  for (int q = threadIdx.x; q < b; q += blockDim.x) {
+    const int32_t j = perm[q];
+    cands_out[node * b + q] = lpos_in ? lpos_in[node * stride + j] : (int32_t)(leaf_lo[node] + j);
+  }
+}
+
+// Reorder the trailing region [col0, col0+rows) after the tournament.
+//   order_mode 0 ("tournament"): new logical order = [pivots (selection
+//     order), remaining positions ascending]                (tournament.py:214-215)
+//   order_mode 1 ("single node"): new logical order = the node's own full
+//     QRCP order perm_full[pos] (tournament.py:176-177)
+// Physically the pivots move to slots col0..col0+b-1, displaced rows take
+// the vacated slots.  Outputs: new pos2row, moved list (dst slot, src slot
+// relative to col0) for permute_kernel, log2phys[t] = physical slot of
+// logical position b+t (for scattering L21).  One block.
+__global__ void __launch_bounds__(1024) calu_reorder_kernel(const int32_t* pivots, const int32_t* perm_full,
+                                                            int order_mode, int b, int64_t rows, int64_t col0,
+                                                            int64_t* pos2row, int64_t* scratch /* 3*rows */,
+                                                            int32_t* moved, int32_t* log2phys, DevState* st) {
+  __shared__ int s_cnt[33];
+  __shared__ int s_nv;
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x, T = blockDim.x;
+  int64_t* oldp = scratch;                 // old pos2row (relative slots)
+  int64_t* flag = scratch + rows;          // per logical position: pivot rank + 1, else 0
+  int64_t* slot_pivot = scratch + 2 * rows;  // per relative slot: 1 if it holds a pivot row
+  for (int64_t i = t; i < rows; i += T) {
+    oldp[i] = pos2row[col0 + i] - col0;
+    flag[i] = 0;
+    slot_pivot[i] = 0;
+  }
+  __syncthreads();
+  // pivots as logical positions
+  for (int q = t; q < b; q += T) {
+    const int32_t lp = order_mode == 0 ? pivots[q] : perm_full[q];
+    flag[lp] = q + 1;
+    slot_pivot[oldp[lp]] = 1;
+  }
+  __syncthreads();
+  // displaced rows: slots < b not holding a pivot; vacated slots: pivot slots >= b.
+  // pair them in increasing slot order (deterministic)
+  if (t == 0) {
+    int nd = 0, nv = 0;
+    int64_t dsl[PRRP_MAXH], vsl[PRRP_MAXH];
+    for (int s = 0; s < b; ++s)
+      if (!slot_pivot[s]) dsl[nd++] = s;
+    // vacated slots in increasing order: scan pivot rows' slots >= b
+    // (at most b of them; simple selection in slot order)
+    int64_t last = -1;
+    for (int q = 0; q < nd; ++q) {
+      int64_t best = INT64_MAX;
+      for (int r = 0; r < b; ++r) {
+        const int32_t lp = order_mode == 0 ? pivots[r] : perm_full[r];
+        const int64_t s = oldp[lp];
+        if (s >= b && s > last && s < best) best = s;
+      }
+      vsl[nv++] = best;
+      last = best;
+    }
+    int cnt = 0;
+    for (int q = 0; q < b; ++q) {
+      const int32_t lp = order_mode == 0 ? pivots[q] : perm_full[q];
+      const int64_t src = oldp[lp];
+      if (src != q) { moved[2 * cnt] = q; moved[2 * cnt + 1] = (int32_t)src; ++cnt; }
+    }
+    for (int i = 0; i < nd; ++i) {
+      moved[2 * cnt] = (int32_t)vsl[i];
+      moved[2 * cnt + 1] = (int32_t)dsl[i];
+      ++cnt;
+      // remember the displacement: the row that was in slot dsl[i] now lives in vsl[i]
+      slot_pivot[dsl[i]] = -(vsl[i] + 2);   // encoded new slot
+    }
+    st->moved = cnt;
+    s_nv = nv;
+  }
+  __syncthreads();
+  // new logical order
+  if (order_mode == 1) {
+    for (int64_t i = t; i < rows; i += T) {
+      const int32_t lp = perm_full[i];
+      int64_t s = oldp[lp];
+      if (i < b) s = i;
+      else if (s < b) s = -slot_pivot[s] - 2;
+      pos2row[col0 + i] = col0 + s;
+      if (i >= b) log2phys[i - b] = (int32_t)s;
+    }
+    return;
+  }
+  // order_mode 0: pivots first, then non-pivots by ascending old logical position
+  for (int q = t; q < b; q += T) pos2row[col0 + q] = col0 + q;
+  // block-wide exclusive scan over non-pivot flags, in chunks
+  const int64_t per_t = (rows + T - 1) / T;
+  const int64_t lo = t * per_t, hi = min(rows, lo + per_t);
+  int cnt = 0;
+  for (int64_t i = lo; i < hi; ++i) cnt += flag[i] == 0;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += y;
+  }
+  if ((t & 31) == 31) s_cnt[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    const int nw = (T + 31) >> 5;
+    int v = t < nw ? s_cnt[t] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (t >= o) v += y;
+    }
+    s_cnt[t] = v;
+  }
+  __syncthreads();
+  int64_t np = b + incl - cnt + ((t >> 5) ? s_cnt[(t >> 5) - 1] : 0);
+  for (int64_t i = lo; i < hi; ++i) {
+    if (flag[i] != 0) continue;
+    int64_t s = oldp[i];
+    if (s < b) s = -slot_pivot[s] - 2;
+    pos2row[col0 + np] = col0 + s;
+    log2phys[np - b] = (int32_t)s;
+    ++np;
+  }
+}
+
+// R12 of the unpivoted Householder QR of the permuted panel transpose
+// (tournament.py:271; pivoted_qr.py:64-71): the reflectors are fixed by the
+// b pivot columns (QR of A11^T, log `refl`), so every non-pivot column gets
+// the same b reflector applications the full householder_qr performs on it.
+// Warp per column; lanes own rows lane, lane+32, ...; output Rbuf[i*p + b + t]
+// for logical position b + t (row pos2row[col0 + b + t]).
+template <int NR>
+__global__ void __launch_bounds__(256) calu_apply_refl_kernel(const double* A, int64_t lda, int64_t col0, int b,
+                                                              int64_t rows, const int64_t* pos2row,
+                                                              const double* refl, double* Rbuf, DevState* st) {
+  extern __shared__ __align__(16) double rf[];    // b x (b+1)
+  if (prrp_failed(st)) return;
+  for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) rf[e] = refl[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t ncol = rows - b;
+  for (int64_t t = (int64_t)blockIdx.x * nw + warp; t < ncol; t += (int64_t)gridDim.x * nw) {
+    const int64_t row = pos2row[col0 + b + t];
+    const double* src = A + row * lda + col0;
+    double x[NR];
+#pragma unroll
+    for (int u = 0; u < NR; ++u) {
+      const int i = lane + 32 * u;
+      x[u] = i < b ? src[i] : 0.0;
+    }
+    for (int k = 0; k < b; ++k) {
+      const double* v = rf + k * (b + 1);
+      const double beta = v[b];
+      if (beta == 0.0) continue;          // skipped reflector (pivoted_qr.py:47-54)
+      double d = 0.0;
+#pragma unroll
+      for (int u = 0; u < NR; ++u) {
+        const int i = lane + 32 * u;
+        if (i >= k && i < b) d = fma(v[i], x[u], d);
+      }
+      for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const double w = mul_rn(beta, d);
+#pragma unroll
+      for (int u = 0; u < NR; ++u) {
+        const int i = lane + 32 * u;
+        if (i >= k && i < b) x[u] = sub_rn(x[u], mul_rn(v[i], w));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NR; ++u) {
+      const int i = lane + 32 * u;
+      if (i < b) Rbuf[(int64_t)i * rows + b + t] = x[u];
+    }
+  }
+}
+
+// copy R11 (b x b, row stride pb) of a small QR into the leading block of Rbuf (stride p)
+__global__ void calu_copy_r11_kernel(const double* Rsmall, int b, double* Rbuf, int64_t p) {
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, q = e % b;
+    Rbuf[(int64_t)i * p + q] = Rsmall[(int64_t)i * b + q];
+  }
+}
+
+// L21 (logical order, column-major ldl) -> physical slot order (column-major ldl2)
+__global__ void calu_scatter_l21_kernel(const double* Lsrc, int64_t ldl, const int32_t* log2phys, int64_t M, int b,
+                                        int64_t bslot, double* Ldst, int64_t ldd) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * b; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / M);
+    const int64_t t = e % M;
+    Ldst[(int64_t)k * ldd + (log2phys[t] - bslot)] = Lsrc[(int64_t)k * ldl + t];
+  }
+}
+
+// panel statistics for a tournament panel: multiplier max from the trsm
+// candidates, swap count = sum over the tree's nodes
+__global__ void calu_stats_kernel(const double* cand, int ncand, const int32_t* node_swaps, int nnodes,
+                                  int32_t* swaps_dev, int panel, DevState* st) {
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  double mx = -1.0;
+  for (int i = threadIdx.x; i < ncand; i += blockDim.x) mx = fmax(mx, cand[i]);
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) {
+    if (ncand > 0) atomic_max_abs(&st->pmm, mx);
+    int s = 0;
+    for (int i = 0; i < nnodes; ++i) s += node_swaps[i];
+    swaps_dev[panel] = s;
+  }
+}
+
+// m > n: rows n..m-1 are the unfinished tail; gather them into logical order
+__global__ void calu_tail_gather_kernel(const double* A, int64_t lda, int64_t n, const int64_t* pos2row, int64_t m,
+                                        double* tmp, const int64_t* porig, int64_t* ptmp) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (m - n) * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, c = e % n;
+    tmp[e] = A[pos2row[n + r] * lda + c];
+    if (c == 0) ptmp[r] = porig[pos2row[n + r]];
+  }
+}

@@ -34,16 +34,17 @@ __device__ void load_r11(const double* Rbuf, int64_t p, int bsel, double* r11) {
 
 // Rank check then singular-diagonal check (in the reference's order).
 // Returns 0 when the block is usable.
-__device__ int r11_checks(const double* r11, int bsel, double fro, DevState* st, int panel, bool report) {
+__device__ int r11_checks(const double* r11, int bsel, double fro, DevState* st, int panel, bool report,
+                          int tl = -1, int ti = -1) {
   for (int k = 0; k < bsel; ++k) {
     if (fabs(r11[upk(k, k)]) < PRRP_EPS * fro) {
-      if (report) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, k, -1, 0.0);
+      if (report) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, k, -1, 0.0, tl, ti);
       return 1;
     }
   }
   for (int i = bsel - 1; i >= 0; --i) {
     if (r11[upk(i, i)] == 0.0) {
-      if (report) prrp_set_error(st, PRRP_ERR_SINGULAR_FACTOR, panel, i, -1, 0.0);
+      if (report) prrp_set_error(st, PRRP_ERR_SINGULAR_FACTOR, panel, i, -1, 0.0, tl, ti);
       return 1;
     }
   }
@@ -107,7 +108,7 @@ __device__ void reduce_worst(double& worst, long long& wflat, double* red_d, lon
 // [bsel + b*TW, ...).  Block 0 performs the rank / singular checks.
 __global__ void __launch_bounds__(TRSM_TW) trsm_kernel(const double* Rbuf, int64_t p, int bsel, double* L21,
                                                       int64_t ldl, double* cand, long long* cand_flat,
-                                                      DevState* st, int panel) {
+                                                      DevState* st, int panel, const double* fro) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(TRSM_TW) trsm_kernel(const double* Rbuf, int64
   double* xs = sm + bsel * (bsel + 1) / 2;
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, st->fro, st, panel, true);
+  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, *fro, st, panel, true);
   double worst = -1.0;
   long long wflat = LLONG_MAX;
   trsm_tile(Rbuf, p, bsel, r11, xs, blockDim.x, bsel + (int64_t)blockIdx.x * blockDim.x, L21, ldl, worst, wflat);
@@ -272,7 +273,8 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
   const int64_t ncol = a.p - a.bsel;
   while (ncol > 0 && worst > a.tau) {
     if (swaps >= f.swap_cap) {
-      if (c == 0 && t == 0) prrp_set_error(a.st, PRRP_ERR_NONCONVERGENCE, a.panel_id, -1, -1, worst);
+      if (c == 0 && t == 0)
+        prrp_set_error(a.st, PRRP_ERR_NONCONVERGENCE, a.panel_id, -1, -1, worst, a.tree_level, a.tree_index);
       return;
     }
     const int i = (int)(wflat / ncol);
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
     double* xs = dyn_smem + a.bsel * (a.bsel + 1) / 2;
     load_r11(a.Rbuf, a.p, a.bsel, r11);
     __syncthreads();
-    if (r11_checks(r11, a.bsel, a.st->fro, a.st, a.panel_id, c == 0 && t == 0)) return;
+    if (r11_checks(r11, a.bsel, *a.fro, a.st, a.panel_id, c == 0 && t == 0, a.tree_level, a.tree_index)) return;
     worst = -1.0;
     wflat = LLONG_MAX;
     const int TW = min((int)blockDim.x, a.bsel > 64 ? 64 : 128);
@@ -326,9 +328,11 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
   if (c != 0) return;
 
   if (t == 0) {
-    f.swaps_dev[a.panel_id] = swaps;
+    f.swaps_dev[a.swap_slot] = swaps;
     a.st->swaps = swaps;
-    if (ncol > 0) atomic_max_abs(&a.st->pmm, worst);
+    // tournament nodes (tree_level >= 0) select rows only; the panel's
+    // multiplier statistic comes from its final L21 (tournament.py:274)
+    if (ncol > 0 && a.tree_level < 0) atomic_max_abs(&a.st->pmm, worst);
   }
   // compact the moved positions (pos -> src j with j != pos), deterministic order
   {

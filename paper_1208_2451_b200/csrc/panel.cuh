@@ -60,6 +60,9 @@ struct PanelArgs {
   int32_t* swaps_out;       // host-visible per-panel swap count (device pointer)
   int32_t* moved;           // out: compact list of moved positions (dst pos, src j) pairs
   long long* prof;          // optional: per-phase clock64 totals of CTA 0 (diagnostics)
+  int swap_slot;            // index into swaps_dev for this node's swap count
+  int tree_level, tree_index;   // CALU tournament node (error payload), -1 otherwise
+  double* fro;              // out (mode 0): ||panel||_F of this node
 };
 
 struct Rec {
@@ -240,7 +243,7 @@ __device__ void engine_run(const PanelArgs& a, int mode, const int32_t* perm_in,
         double f = 0.0;
         if (lane < C) f = *cl.map_shared_rank(&S.fro_part, lane);
         for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-        if (lane == 0) a.st->fro = sqrt(f);
+        if (lane == 0) *a.fro = sqrt(f);
       }
       __syncwarp();
       const int L = h - k;

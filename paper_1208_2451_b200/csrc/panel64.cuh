@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
       if (k == 0 && mode == 0 && c == 0) {
         double f = lane < C ? S.fro_cta[lane] : 0.0;
         for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-        if (lane == 0) a.st->fro = sqrt(f);
+        if (lane == 0) *a.fro = sqrt(f);
       }
       __syncwarp();
       const int L = P64_H - k;

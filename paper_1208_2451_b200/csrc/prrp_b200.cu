@@ -24,6 +24,7 @@
 #include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
+#include "calu.cuh"
 
 namespace {
 
@@ -93,7 +94,9 @@ DeviceCaps& caps() {
                            (const void*)trsm_w_kernel<4>, (const void*)compose_w_kernel<1>, (const void*)compose_w_kernel<2>,
                            (const void*)compose_w_kernel<3>, (const void*)compose_w_kernel<4>,
                            (const void*)blockrow_w_kernel<1>, (const void*)blockrow_w_kernel<2>,
-                           (const void*)blockrow_w_kernel<3>, (const void*)blockrow_w_kernel<4>})
+                           (const void*)blockrow_w_kernel<3>, (const void*)blockrow_w_kernel<4>,
+                           (const void*)calu_apply_refl_kernel<1>, (const void*)calu_apply_refl_kernel<2>,
+                           (const void*)calu_apply_refl_kernel<3>, (const void*)calu_apply_refl_kernel<4>})
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
@@ -298,6 +301,7 @@ int swap_cap(int b, int64_t p, double tau) {   // pivoted_qr.py:108-110
 }
 
 struct PanelBuffers {
+  double* fro = nullptr;    // per-node ||panel||_F slot (nullptr: DevState::fro)
   double* Rbuf;
   int32_t* perm;
   double* ovf;
@@ -317,12 +321,17 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
 // (all SMs), swap loop + moved rows (+ optional GEPP of the pivot block).
 void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel, double tau, int panel,
                        double* L21, int64_t ldl, const PanelBuffers& B, DevState* st, int32_t* swaps_dev,
-                       double* D, int32_t* piv, int32_t* gperm, bool do_gepp, cudaStream_t s) {
+                       double* D, int32_t* piv, int32_t* gperm, bool do_gepp, cudaStream_t s,
+                       const int64_t* rowidx = nullptr, int swap_slot = -1, int tl = -1, int ti = -1) {
   const PanelCfg g = panel_config(h, p, bsel);
   PanelArgs a{};
   a.src = src;
   a.ld = ld;
-  a.rowidx = nullptr;
+  a.rowidx = rowidx;
+  a.swap_slot = swap_slot < 0 ? panel : swap_slot;
+  a.tree_level = tl;
+  a.tree_index = ti;
+  a.fro = B.fro ? B.fro : &st->fro;
   a.h = h;
   a.p = p;
   a.bsel = bsel;
@@ -373,17 +382,17 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       const int nb = (int)((ncol + tw - 1) / tw);
       // generic path keeps one candidate per 128 positions: at most kMaxCand blocks
       if (nb > kMaxCand) fail(PRRP_ERR_UNSUPPORTED, "generic trsm path limited to 131072 rows");
-      trsm_kernel<<<nb, tw, ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel);
+      trsm_kernel<<<nb, tw, ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
       return;
     }
     switch ((bsel + 31) / 32) {
-      case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
-      case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
-      case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
-      default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel); break;
+      case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
+      case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
+      case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
+      default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
     }
     tend(s);
     CU_TRY(cudaGetLastError());
@@ -749,6 +758,305 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   return state_to_err(hs, err);
 }
 
+
+// ---------------------------------------------------------------- CALU_PRRP driver
+// Binary tournament (tournament.py:155-217) + CALU_PRRP panel loop
+// (tournament.py:237-296).  Tree nodes of one level run concurrently on a
+// pool of streams; every node is the cluster QRCP engine + multipliers +
+// swap loop on an index list of logical rows.
+struct NodeBufs {
+  PanelBuffers B;
+  double* L21;
+  int64_t ldl;
+  int32_t* lpos_in;   // merge nodes: 2b logical positions
+  int64_t* rowidx;    // merge nodes: 2b physical rows
+};
+
+thread_local std::vector<cudaStream_t> tl_node_streams;
+cudaStream_t node_stream(int i) {
+  while ((int)tl_node_streams.size() <= i) {
+    cudaStream_t st;
+    int lo = 0, hi = 0;
+    CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    tl_node_streams.push_back(st);
+  }
+  return tl_node_streams[i];
+}
+
+int64_t qr_charge3(int64_t r, int64_t b) { return 6 * r * b * b - 2 * b * b * b; }   // 3 * _charge_qr
+
+int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
+                  int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+  if (P < 1) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1");
+  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  caps();
+  const int npanels = (int)((n + b - 1) / b);
+  const int maxnodes = 2 * P;
+  Arena ar(s);
+  DevState* st = new_state(ar, s);
+  const int64_t ldl = ((m + 7) / 8) * 8;
+  double* Lphys = ar.get<double>((size_t)b * ldl);
+  // main (whole-panel) buffers
+  PanelBuffers B{};
+  B.Rbuf = ar.get<double>((size_t)b * m);
+  B.perm = ar.get<int32_t>(m);
+  B.ovf = ar.get<double>(ovf_elems(b, m, b));
+  B.cand = ar.get<double>(kMaxCand);
+  B.cand_flat = ar.get<long long>(kMaxCand);
+  B.moved = ar.get<int32_t>(2 * m);
+  double* Llog = ar.get<double>((size_t)b * ldl);
+  double* Rsmall = ar.get<double>((size_t)b * b);
+  double* refl = ar.get<double>((size_t)b * (b + 1));
+  int32_t* perm_small = ar.get<int32_t>(b);
+  // tree nodes
+  std::vector<NodeBufs> nodes(maxnodes);
+  const int64_t leafmax = m / std::max<int64_t>(1, std::min<int64_t>(P, std::max<int64_t>(1, m / (b + 1)))) + 1;
+  const int64_t pnode = std::max<int64_t>(leafmax, 2 * b + 2);
+  int32_t* lpos_all = ar.get<int32_t>((size_t)maxnodes * 2 * b);
+  int64_t* rowidx_all = ar.get<int64_t>((size_t)maxnodes * 2 * b);
+  for (int i = 0; i < maxnodes; ++i) {
+    NodeBufs& nb = nodes[i];
+    nb.B.Rbuf = ar.get<double>((size_t)b * pnode);
+    nb.B.perm = ar.get<int32_t>(pnode);
+    nb.B.ovf = ar.get<double>(ovf_elems(b, pnode, b));
+    nb.B.cand = ar.get<double>(kMaxCand);
+    nb.B.cand_flat = ar.get<long long>(kMaxCand);
+    nb.B.moved = ar.get<int32_t>(2 * pnode);
+    nb.B.fro = ar.get<double>(1);
+    nb.ldl = ((pnode + 7) / 8) * 8;
+    nb.L21 = ar.get<double>((size_t)b * nb.ldl);
+    nb.lpos_in = lpos_all + (size_t)i * 2 * b;
+    nb.rowidx = rowidx_all + (size_t)i * 2 * b;
+  }
+  int32_t* cands = ar.get<int32_t>((size_t)2 * maxnodes * b);      // two levels (ping-pong)
+  int32_t* node_swaps = ar.get<int32_t>((size_t)npanels * maxnodes);
+  CU_TRY(cudaMemsetAsync(node_swaps, 0, sizeof(int32_t) * npanels * maxnodes, s));
+  const int32_t** perms_dev = ar.get<const int32_t*>(maxnodes);
+  int64_t* leaf_lo_dev = ar.get<int64_t>(maxnodes);
+  int64_t* pos2row = ar.get<int64_t>(m);
+  int64_t* scratch = ar.get<int64_t>(3 * m);
+  int32_t* log2phys = ar.get<int32_t>(m);
+  int32_t* ident = ar.get<int32_t>(m);
+  double* D = ar.get<double>((size_t)b * b);
+  int32_t* piv = ar.get<int32_t>(b);
+  int32_t* gperm = ar.get<int32_t>(b);
+  int32_t* swaps_dev = ar.get<int32_t>(npanels);
+  CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
+  {
+    std::vector<const int32_t*> hp(maxnodes);
+    for (int i = 0; i < maxnodes; ++i) hp[i] = nodes[i].B.perm;
+    CU_TRY(cudaMemcpyAsync(perms_dev, hp.data(), sizeof(void*) * maxnodes, cudaMemcpyHostToDevice, s));
+  }
+  const int sms = caps().sms;
+  iota_kernel<<<sms, 256, 0, s>>>(perm, m);
+  iota_kernel<<<sms, 256, 0, s>>>(pos2row, m);
+  iota32_kernel<<<sms, 256, 0, s>>>(ident, m);
+  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  CU_TRY(cudaGetLastError());
+  std::vector<int64_t> charges(npanels, -1);
+  std::vector<std::vector<std::pair<int64_t, int>>> node_members(npanels);   // (members, node slot)
+
+  auto run_level = [&](const std::vector<int64_t>& lo, const std::vector<int64_t>& cnt, bool leaves,
+                       int64_t col0, int bj, int panel, int level, int slot0) {
+    // fork
+    cudaEvent_t fk;
+    CU_TRY(cudaEventCreateWithFlags(&fk, cudaEventDisableTiming));
+    CU_TRY(cudaEventRecord(fk, s));
+    const int nn = (int)lo.size();
+    for (int i = 0; i < nn; ++i) {
+      cudaStream_t ns = node_stream(i);
+      CU_TRY(cudaStreamWaitEvent(ns, fk, 0));
+      const int64_t* ridx = leaves ? pos2row + col0 + lo[i] : nodes[i].rowidx;
+      if (cnt[i] <= bj) continue;                       // node passes its rows through
+      strong_rrqr_panel(A + col0, lda, bj, cnt[i], bj, tau, panel, nodes[i].L21, nodes[i].ldl, nodes[i].B, st,
+                        node_swaps + (size_t)panel * maxnodes, nullptr, nullptr, nullptr, false, ns, ridx,
+                        slot0 + i, level, i);
+    }
+    // join
+    for (int i = 0; i < nn; ++i) {
+      cudaEvent_t jn;
+      CU_TRY(cudaEventCreateWithFlags(&jn, cudaEventDisableTiming));
+      CU_TRY(cudaEventRecord(jn, node_stream(i)));
+      CU_TRY(cudaStreamWaitEvent(s, jn, 0));
+      CU_TRY(cudaEventDestroy(jn));
+    }
+    CU_TRY(cudaEventDestroy(fk));
+  };
+
+  int panel = 0;
+  for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
+    const int bj = (int)std::min<int64_t>(b, n - col0);
+    const int64_t rows = m - col0;
+    const int64_t width = n - col0 - bj;
+    double* blk = A + col0 * lda + col0;
+    if (rows > bj) {
+      const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
+      if (p_eff == 1) {
+        // single node: the selector's own full order and l_block (tournament.py:168-177)
+        strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Llog, ldl, B, st, swaps_dev, nullptr, nullptr,
+                          nullptr, false, s, pos2row + col0);
+        calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, B.perm, 1, bj, rows, col0, pos2row, scratch, B.moved,
+                                               log2phys, st);
+      } else {
+        // leaves: contiguous logical blocks, first blocks larger (tournament.py:64-88)
+        std::vector<int64_t> lo(p_eff), cnt(p_eff);
+        {
+          const int64_t base = rows / p_eff, extra = rows % p_eff;
+          int64_t start = 0;
+          for (int64_t i = 0; i < p_eff; ++i) {
+            cnt[i] = base + (i < extra ? 1 : 0);
+            lo[i] = start;
+            start += cnt[i];
+          }
+        }
+        CU_TRY(cudaMemcpyAsync(leaf_lo_dev, lo.data(), sizeof(int64_t) * p_eff, cudaMemcpyHostToDevice, s));
+        int64_t chg3 = 0;
+        int slot = 0;
+        run_level(lo, cnt, true, col0, bj, panel, 0, slot);
+        for (int64_t i = 0; i < p_eff; ++i) {
+          chg3 += qr_charge3(cnt[i], bj);
+          node_members[panel].push_back({cnt[i], slot + (int)i});
+        }
+        slot += (int)p_eff;
+        int32_t* cur = cands;
+        int32_t* nxt = cands + (size_t)maxnodes * b;
+        calu_select_kernel<<<(unsigned)p_eff, 128, 0, s>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
+        int64_t ncur = p_eff;
+        int level = 1;
+        while (ncur > 1) {
+          const int64_t nmerge = ncur / 2;
+          // node i of this level reads lpos_all/rowidx_all[i*2b .. i*2b + 2b) (stride 2b even when bj < b)
+          calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, s>>>(cur, bj, (int)(2 * nmerge), lpos_all, rowidx_all,
+                                                                     pos2row, col0, 2 * b);
+          CU_TRY(cudaGetLastError());
+          std::vector<int64_t> mlo(nmerge, 0), mcnt(nmerge, 2 * bj);
+          run_level(mlo, mcnt, false, col0, bj, panel, level, slot);
+          for (int64_t i = 0; i < nmerge; ++i) {
+            chg3 += qr_charge3(2 * bj, bj);
+            node_members[panel].push_back({2 * bj, slot + (int)i});
+          }
+          slot += (int)nmerge;
+          calu_select_kernel<<<(unsigned)nmerge, 128, 0, s>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
+          if (ncur % 2)   // odd node promoted unmerged (tournament.py:197-198)
+            CU_TRY(cudaMemcpyAsync(nxt + nmerge * bj, cur + (ncur - 1) * bj, sizeof(int32_t) * bj,
+                                   cudaMemcpyDeviceToDevice, s));
+          ncur = nmerge + (ncur % 2);
+          std::swap(cur, nxt);
+          ++level;
+        }
+        charges[panel] = chg3;
+        // new logical order [pivots, rest ascending]; move the pivot rows to slots col0..
+        calu_reorder_kernel<<<1, 1024, 0, s>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
+                                               st);
+      }
+      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
+          A, lda, col0, n, B.moved, perm, st, panel);
+      CU_TRY(cudaGetLastError());
+      if (p_eff > 1) {
+        // unpivoted QR of the permuted panel transpose -> multiplier_block (tournament.py:271-272)
+        PanelArgs qa{};
+        qa.src = blk;
+        qa.ld = lda;
+        qa.h = bj;
+        qa.p = bj;
+        qa.bsel = bj;
+        qa.steps = bj;
+        qa.mode = 1;
+        qa.perm = perm_small;
+        qa.Rbuf = Rsmall;
+        qa.refl = refl;
+        qa.ovf = B.ovf;
+        const PanelCfg gq = panel_config(bj, bj, bj, true);
+        qa.per = gq.per;
+        qa.cap = gq.cap;
+        qa.cap_pad = gq.cap_pad;
+        qa.ovpad = gq.ovpad;
+        qa.st = st;
+        qa.panel_id = panel;
+        iota32_kernel<<<1, 128, 0, s>>>(perm_small, bj);
+        launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, s, qa);
+        calu_copy_r11_kernel<<<1, 256, 0, s>>>(Rsmall, bj, B.Rbuf, rows);
+        const size_t dyn = (size_t)bj * (bj + 1) * 8;
+        const unsigned grid = (unsigned)std::min<int64_t>(sms * 4, (rows - bj + 7) / 8);
+        switch ((bj + 31) / 32) {
+          case 1: calu_apply_refl_kernel<1><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          case 2: calu_apply_refl_kernel<2><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          case 3: calu_apply_refl_kernel<3><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          default: calu_apply_refl_kernel<4><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+        }
+        CU_TRY(cudaGetLastError());
+        const int64_t ncol = rows - bj;
+        const int nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
+        const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
+        const double* one = nullptr;
+        (void)one;
+        double* fro_inf = nodes[0].B.fro;   // rank check of the final QR: the reference has none (fro = 0)
+        CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), s));
+        switch ((bj + 31) / 32) {
+          case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+          case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+          case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+          default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+        }
+        calu_stats_kernel<<<1, 256, 0, s>>>(B.cand, nblk, node_swaps + (size_t)panel * maxnodes, maxnodes,
+                                            swaps_dev, panel, st);
+        CU_TRY(cudaGetLastError());
+      }
+      // L21 (logical order) -> physical slots for the Schur update and the compose
+      calu_scatter_l21_kernel<<<sms * 4, 256, 0, s>>>(Llog, ldl, log2phys, rows - bj, bj, bj, Lphys, ldl);
+      if (width > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lphys, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
+                     width, bj, st, s);
+      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      launch_compose_w(Lphys, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
+    } else {
+      // last square block: bring the rows into logical order, then GEPP
+      calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, ident, 1, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
+                                             st);
+      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
+          A, lda, col0, n, B.moved, perm, st, panel);
+      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+    }
+    CU_TRY(cudaGetLastError());
+    launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+    CU_TRY(cudaGetLastError());
+  }
+  if (m > n) {
+    // unfinished tail rows n..m-1 into logical order
+    double* tmp = ar.get<double>((size_t)(m - n) * n);
+    int64_t* ptmp = ar.get<int64_t>(m - n);
+    calu_tail_gather_kernel<<<sms * 4, 256, 0, s>>>(A, lda, n, pos2row, m, tmp, perm, ptmp);
+    CU_TRY(cudaMemcpy2DAsync(A + n * lda, lda * 8, tmp, n * 8, n * 8, m - n, cudaMemcpyDeviceToDevice, s));
+    CU_TRY(cudaMemcpyAsync(perm + n, ptmp, sizeof(int64_t) * (m - n), cudaMemcpyDeviceToDevice, s));
+  }
+  DevState hs;
+  read_state(st, hs, s);
+  std::vector<int32_t> sw(npanels);
+  CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> nsw((size_t)npanels * maxnodes);
+  CU_TRY(cudaMemcpy(nsw.data(), node_swaps, sizeof(int32_t) * nsw.size(), cudaMemcpyDeviceToHost));
+  if (swap_counts) memcpy(swap_counts, sw.data(), sizeof(int32_t) * npanels);
+  if (tchg3) {
+    for (int k = 0; k < npanels; ++k) {
+      if (charges[k] < 0) { tchg3[k] = -1; continue; }
+      int64_t c3 = 0;
+      for (auto& mm : node_members[k]) c3 += (1 + nsw[(size_t)k * maxnodes + mm.second]) * qr_charge3(mm.first, b);
+      tchg3[k] = c3;
+    }
+  }
+  fill_stats(hs, stats);
+  if (stats) {
+    stats->total_swaps = 0;
+    for (int v : sw) stats->total_swaps += v;
+  }
+  return state_to_err(hs, err);
+}
+
 }  // namespace
 
 // ======================================================================== ABI
@@ -822,10 +1130,16 @@ int prrp_b200_dmma_peak(double ms, double* tflops, prrp_err* err) {
   }
 }
 
-int prrp_caluprrp(double*, int64_t, int64_t, int64_t, int32_t, double, int32_t, int64_t*, int32_t*, prrp_stats*,
-                  prrp_err* err, void*) {
+int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau, int32_t leaf_count,
+                  int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3, prrp_stats* stats, prrp_err* err,
+                  void* stream) {
   clear_err(err);
-  return report(err, Fail{PRRP_ERR_UNSUPPORTED, "caluprrp device path not built yet"});
+  try {
+    return caluprrp_impl(A, lda, m, n, b, tau, leaf_count, perm, swap_counts, tournament_charge3, stats, err,
+                         (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
 }
 
 int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t bsel, double tau, double* R,

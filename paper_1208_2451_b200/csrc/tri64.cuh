@@ -38,7 +38,8 @@ __device__ __forceinline__ double lane_pick(const double (&x)[NR], int row) {
 template <int NR>
 __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                               double* L21, int64_t ldl, double* cand,
-                                                              long long* cand_flat, DevState* st, int panel) {
+                                                              long long* cand_flat, DevState* st, int panel,
+                                                              const double* fro, int tl, int ti) {
   extern __shared__ __align__(16) double sm[];
   double* r11 = sm;                                    // packed upper, bsel(bsel+1)/2
   double* tile = sm + ((bsel * (bsel + 1) / 2 + 1) & ~1);   // bsel x TTCP
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
   for (int i = threadIdx.x; i < bsel; i += blockDim.x) rcp[i] = __drcp_rn(r11[upk(i, i)]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, st->fro, st, panel, true);
+  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, *fro, st, panel, true, tl, ti);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t ncol = p - bsel;
   double worst = -1.0;

@@ -124,7 +124,13 @@ def upload(a):
     m, n = a.shape
     lda = n + (n & 1)
     buf = torch.empty((m, lda), dtype=torch.float64, device="cuda")
-    buf[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(a)), non_blocking=False)
+    src = torch.from_numpy(np.ascontiguousarray(a))
+    if not src.is_pinned() and src.numel() >= (1 << 20):
+        # stage through a pinned block: full-bandwidth DMA instead of a pageable copy
+        staged = torch.empty(src.shape, dtype=torch.float64, pin_memory=True)
+        staged.copy_(src)
+        src = staged
+    buf[:, :n].copy_(src, non_blocking=True)
     return buf, lda
 
 
@@ -161,10 +167,17 @@ def split_packed_device(packed, m, n):
     import torch
     lt = torch.tril(packed, -1)
     lt.diagonal().fill_(1.0)
-    l = lt.t().contiguous().cpu().numpy().T
+    lt_t = lt.t().contiguous()
     del lt
-    u = torch.triu(packed[:n, :]).t().contiguous().cpu().numpy().T
-    return l, u
+    u_t = torch.triu(packed[:n, :]).t().contiguous()
+    # D2H into pinned blocks from torch's caching host allocator (fast DMA;
+    # the numpy results own their block until they are released)
+    l_h = torch.empty(lt_t.shape, dtype=torch.float64, pin_memory=True)
+    u_h = torch.empty(u_t.shape, dtype=torch.float64, pin_memory=True)
+    l_h.copy_(lt_t, non_blocking=True)
+    u_h.copy_(u_t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return l_h.numpy().T, u_h.numpy().T
 
 
 def _stats(st, swaps, m, n, b):

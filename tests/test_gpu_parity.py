@@ -209,3 +209,32 @@ def test_luprrp_growth_stress(dev):
         assert f.stats.growth_factor == pytest.approx(ref.stats.growth_factor, rel=TOL_G)
         res = orc.rel_residual(a, f.perm, f.l, f.u)
         assert res <= max(4 * orc.rel_residual(a, ref.perm, ref.l, ref.u), 1024 * 2.0 ** -52)
+
+
+def test_caluprrp_golden(dev, golden):
+    """CALU_PRRP (binary tree) against the reference's fixtures and the oracle."""
+    index, arrays = golden
+    for e in index["calu"]:
+        a = make_input(e)
+        f = dev.caluprrp_factor(a, e["b"], e["tau"], dev.binary_tree(e["P"]))
+        ref = orc.calu_prrp(a, e["b"], e["tau"], "binary", e["P"])
+        assert np.array_equal(ref.perm, arrays["calu/" + e["name"] + "/perm"])
+        _check_factors(f, ref, a)
+
+
+@pytest.mark.parametrize("n,b,P,gen", [(1024, 64, 8, "randn"), (2048, 64, 8, "randn"), (1536, 128, 8, "urand"),
+                                       (700, 32, 4, "randn"), (900, 64, 3, "urand")])
+def test_caluprrp_vs_oracle(dev, n, b, P, gen):
+    a = orc.randn_matrix(n, 42) if gen == "randn" else orc.urand_matrix(n, 42)
+    f = dev.caluprrp_factor(a, b, 2.0, dev.binary_tree(P))
+    ref = orc.calu_prrp(a, b, 2.0, "binary", P)
+    _check_factors(f, ref, a)
+
+
+def test_caluprrp_single_leaf_equals_luprrp(dev):
+    """Degenerate tree: CALU_PRRP with one leaf is LU_PRRP bit for bit."""
+    a = orc.randn_matrix(512, 3)
+    f1 = dev.caluprrp_factor(a, 64, 2.0, dev.binary_tree(1))
+    f2 = dev.luprrp_factor(a, 64, 2.0)
+    assert np.array_equal(f1.perm, f2.perm)
+    assert np.array_equal(f1.l, f2.l) and np.array_equal(f1.u, f2.u)
