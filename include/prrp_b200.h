@@ -146,6 +146,14 @@ int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t
 int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p,
                         double* R, double* Q, prrp_err* err, void* stream);
 
+/* Multiplier block (R11^-1 R12)^T of an upper-trapezoidal R (column-major,
+ * ldr >= b, p columns) — replaces prrp.multiplier_block (pivoted_qr.py:90-98):
+ * back substitution with true division, SingularFactor on an exact zero
+ * diagonal.  L: (p-b) x b column-major (ldl >= p-b), device.  absmax (host,
+ * may be NULL) receives max|L|. */
+int prrp_multiplier_block(const double* R, int64_t ldr, int32_t b, int64_t p, double* L, int64_t ldl,
+                          double* absmax, prrp_err* err, void* stream);
+
 /* Rank-K Schur update C <- C - L*B with the reference's rounding recipe
  * (matcore.rank_update, matcore.py:54-61: product accumulated in increasing
  * k from zero, then one subtraction).  C: M x N row-major (ldc), L: M x K

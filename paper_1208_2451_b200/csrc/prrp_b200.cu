@@ -540,6 +540,15 @@ __global__ void __launch_bounds__(256) dmma_peak_kernel(double* sink, long iters
   if (s == 1234.5) sink[0] = s;
 }
 
+// column-major R (ldr) rows 0..b-1 -> position-major Rbuf[i*p + pos]
+__global__ void r_in_kernel(const double* R, int64_t ldr, int b, int64_t p, double* Rbuf) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)b * p; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = e / b;
+    const int i = (int)(e % b);
+    Rbuf[(int64_t)i * p + pos] = R[i + pos * ldr];
+  }
+}
+
 __global__ void iota32_kernel(int32_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = (int32_t)i;
@@ -1224,6 +1233,44 @@ int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p, doub
     CU_TRY(cudaGetLastError());
     DevState hs;
     read_state(st, hs, s);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_multiplier_block(const double* R, int64_t ldr, int32_t b, int64_t p, double* L, int64_t ldl,
+                          double* absmax, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (b < 1 || b > PRRP_MAXH || p < b || ldr < b) fail(PRRP_ERR_ARG, "multiplier_block needs 1 <= b <= 128, p >= b");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    const int64_t ncol = p - b;
+    if (ncol > 0) {
+      double* Rbuf = ar.get<double>((size_t)b * p);
+      double* fro0 = ar.get<double>(1);
+      double* cand = ar.get<double>(kMaxCand);
+      long long* candf = ar.get<long long>(kMaxCand);
+      CU_TRY(cudaMemsetAsync(fro0, 0, sizeof(double), s));
+      r_in_kernel<<<caps().sms, 256, 0, s>>>(R, ldr, b, p, Rbuf);
+      const int nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
+      const size_t tdyn = (((size_t)b * (b + 1) / 2 + 1) / 2 * 2 + (size_t)b * TTCP) * 8;
+      switch ((b + 31) / 32) {
+        case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
+        case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
+        case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
+        default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
+      }
+      calu_stats_kernel<<<1, 256, 0, s>>>(cand, nblk, cand == nullptr ? nullptr : (const int32_t*)nullptr, 0,
+                                          (int32_t*)fro0, 0, st);
+      CU_TRY(cudaGetLastError());
+    }
+    DevState hs;
+    read_state(st, hs, s);
+    if (absmax) *absmax = ncol > 0 ? bits_to_double(hs.pmm) : 0.0;
     return state_to_err(hs, err);
   } catch (const Fail& f) {
     return report(err, f);

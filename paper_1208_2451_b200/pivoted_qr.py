@@ -91,3 +91,22 @@ def householder_qr(a):
     _lib.raise_for(rc, err, "householder_qr")
     return QRFactors(q=np.asfortranarray(Q.cpu().numpy().T), r=np.asfortranarray(R.cpu().numpy().T),
                      perm=np.arange(p, dtype=np.intp))
+
+
+def multiplier_block(r, b):
+    """(R11^-1 R12)^T from an upper trapezoidal R (pivoted_qr.py:90-98)."""
+    import torch
+    r = _as_matrix(r)
+    if r.shape[0] < b or r.shape[1] < b:
+        raise ValueError("R smaller than the requested leading block")
+    if r.shape[1] == b:
+        return np.zeros((0, b), order="F")
+    lib = _lib.device_lib()
+    h, p = r.shape
+    R = torch.from_numpy(np.ascontiguousarray(r.T)).to("cuda")       # column-major h x p
+    L = torch.empty((b, p - b), dtype=torch.float64, device="cuda")  # column-major (p-b) x b
+    err = _lib.PrrpErr()
+    rc = lib.prrp_multiplier_block(ctypes.c_void_p(R.data_ptr()), h, b, p, ctypes.c_void_p(L.data_ptr()), p - b,
+                                   None, ctypes.byref(err), _lib.stream_handle())
+    _lib.raise_for(rc, err, "multiplier_block")
+    return np.asfortranarray(L.cpu().numpy().T)

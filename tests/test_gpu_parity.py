@@ -238,3 +238,43 @@ def test_caluprrp_single_leaf_equals_luprrp(dev):
     f2 = dev.luprrp_factor(a, 64, 2.0)
     assert np.array_equal(f1.perm, f2.perm)
     assert np.array_equal(f1.l, f2.l) and np.array_equal(f1.u, f2.u)
+
+
+def test_dist_calu_device_ops_single_rank(dev):
+    """The distributed orchestration with the device ops (world size 1) agrees
+    with the single-call device CALU_PRRP and with the reference algorithm."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1208_2451_b200 import dist as pd
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        a = orc.randn_matrix(256, 11)
+        f = pd.caluprrp_factor_dist(a, 16, 2.0, 4)
+    finally:
+        dist.destroy_process_group()
+    ref = orc.calu_prrp(a, 16, 2.0, "binary", 4)
+    one = dev.caluprrp_factor(a, 16, 2.0, dev.binary_tree(4))
+    assert np.array_equal(f.perm, ref.perm) and np.array_equal(one.perm, ref.perm)
+    assert list(f.stats.swap_counts) == list(ref.stats.swap_counts)
+    assert _rel(f.u, ref.u) <= TOL_F and _rel(f.l, ref.l) <= TOL_F
+    assert f.stats.growth_factor == pytest.approx(ref.stats.growth_factor, rel=TOL_G)
+
+
+def test_device_matcore_and_gepp_api(dev):
+    rng = np.random.default_rng(12)
+    c, a, b = rng.standard_normal((70, 50)), rng.standard_normal((70, 16)), rng.standard_normal((16, 50))
+    assert np.array_equal(dev.rank_update(c, a, b), orc.schur_update(c, a, b))
+    assert np.array_equal(dev.matmul(a, b), orc.dger_product(a, b))
+    br = rng.standard_normal((32, 90))
+    g, r = dev.gepp_factor(br), orc.gepp(br)
+    assert np.array_equal(g.perm, r.perm) and np.array_equal(g.u, r.u) and np.array_equal(g.l, r.l)
+    assert g.intermediate_max == r.intermediate_max
+    rr = np.triu(rng.standard_normal((16, 60))) + 4 * np.eye(16, 60)
+    assert np.array_equal(dev.multiplier_block(rr, 16), orc.l_from_r(rr, 16))
