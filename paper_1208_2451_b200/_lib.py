@@ -8,7 +8,8 @@ import os
 from .errors import (DeviceUnavailable, DimensionMismatch, NonConvergence,
                      RankDeficient, SingularFactor, SingularMatrix)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libprrp_b200.so")
+# PRRP_B200_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("PRRP_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libprrp_b200.so")
 
 PRRP_OK = 0
 PRRP_ERR_DIM = 1

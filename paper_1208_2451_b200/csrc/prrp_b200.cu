@@ -74,6 +74,14 @@ struct DeviceCaps {
   int max_cluster = 8;
 };
 
+// opt in to all the dynamic shared memory the kernel's static footprint leaves
+void set_max_dyn(const void* fn) {
+  cudaFuncAttributes fa;
+  CU_TRY(cudaFuncGetAttributes(&fa, fn));
+  CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kSmemOptin - fa.sharedSizeBytes)));
+}
+
 DeviceCaps& caps() {
   static DeviceCaps c;
   if (!c.init) {
@@ -83,13 +91,13 @@ DeviceCaps& caps() {
     for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
                            (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel}) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
+      set_max_dyn((const void*)fn);
     }
-    CU_TRY(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
-    CU_TRY(cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 16 * 1024)));
-    CU_TRY(cudaFuncSetAttribute(blockrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
-    CU_TRY(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
-    CU_TRY(cudaFuncSetAttribute(gepp_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 4 * 1024)));
+    set_max_dyn((const void*)trsm_kernel);
+    set_max_dyn((const void*)permute_kernel);
+    set_max_dyn((const void*)blockrow_kernel);
+    set_max_dyn((const void*)compose_kernel);
+    set_max_dyn((const void*)gepp_diag_kernel);
     for (const void* fn : {(const void*)trsm_w_kernel<1>, (const void*)trsm_w_kernel<2>, (const void*)trsm_w_kernel<3>,
                            (const void*)trsm_w_kernel<4>, (const void*)compose_w_kernel<1>, (const void*)compose_w_kernel<2>,
                            (const void*)compose_w_kernel<3>, (const void*)compose_w_kernel<4>,
@@ -97,7 +105,7 @@ DeviceCaps& caps() {
                            (const void*)blockrow_w_kernel<3>, (const void*)blockrow_w_kernel<4>,
                            (const void*)calu_apply_refl_kernel<1>, (const void*)calu_apply_refl_kernel<2>,
                            (const void*)calu_apply_refl_kernel<3>, (const void*)calu_apply_refl_kernel<4>})
-      CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemOptin - 8 * 1024)));
+      set_max_dyn((const void*)fn);
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
@@ -258,7 +266,9 @@ PanelCfg panel_config(int h, int64_t p, int bsel, bool few_ctas = false) {
 // overflow scratch large enough for both the panel engine and the finalize config
 size_t ovf_elems(int h, int64_t p, int bsel) {
   const PanelCfg a = panel_config(h, p, bsel), b = panel_config(h, p, bsel, true);
-  return std::max((size_t)a.C * h * std::max<int64_t>(1, a.ovpad), (size_t)b.C * h * std::max<int64_t>(1, b.ovpad));
+  // (h x p: the row-save area of the h = 64 register engine, panel1.cuh)
+  return std::max({(size_t)a.C * h * std::max<int64_t>(1, a.ovpad), (size_t)b.C * h * std::max<int64_t>(1, b.ovpad),
+                   (size_t)h * p});
 }
 
 template <typename K, typename... Args>
@@ -647,8 +657,11 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   const int sms = caps().sms;
   tl_prof = nullptr;
   if (panel_prof_enabled()) {
-    tl_prof = ar.get<long long>(8);
-    CU_TRY(cudaMemsetAsync(tl_prof, 0, 8 * sizeof(long long), s));
+    tl_prof = ar.get<long long>(8 + PRRP_CLUSTER_MAX * 64 * 8 + 16 * 64 * 8);
+    CU_TRY(cudaMemsetAsync(tl_prof, 0, (8 + PRRP_CLUSTER_MAX * 64 * 8 + 16 * 64 * 8) * sizeof(long long), s));
+    const char* e = getenv("PRRP_PANEL_TL");
+    const long long target = e ? atoll(e) : -1;
+    CU_TRY(cudaMemcpyAsync(tl_prof + 6, &target, sizeof(long long), cudaMemcpyHostToDevice, s));
   }
   tbegin(PRRP_K_OTHER, s);
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
@@ -750,6 +763,12 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     CU_TRY(cudaMemcpy(pr, tl_prof, sizeof(pr), cudaMemcpyDeviceToHost));
     fprintf(stderr, "[prrp panel prof] launches=%lld cycles: reduce=%lld publish+cluster_sync=%lld "
             "winner+reflector=%lld apply=%lld total=%lld\n", pr[5], pr[0], pr[1], pr[2], pr[3], pr[4]);
+    if (getenv("PRRP_PANEL_TL")) {
+      std::vector<long long> tl(PRRP_CLUSTER_MAX * 64 * 8 + 16 * 64 * 8);
+      CU_TRY(cudaMemcpy(tl.data(), tl_prof + 8, tl.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      FILE* f = fopen(getenv("PRRP_PANEL_TL_OUT") ? getenv("PRRP_PANEL_TL_OUT") : "panel_tl.bin", "wb");
+      if (f) { fwrite(tl.data(), sizeof(long long), tl.size(), f); fclose(f); }
+    }
     tl_prof = nullptr;
   }
   std::vector<int32_t> sw(npanels);
