@@ -229,6 +229,134 @@ __global__ void __launch_bounds__(1024) gepp_diag_kernel(const double* src, int6
   gepp_diag(src, ld, rowmap, b, sm, D, piv, gperm, st, panel, red);
 }
 
+// Register GEPP of a b x b block, b <= 64 (gepp.py:39-65, same arithmetic as
+// gepp_diag).  256 threads: thread (i, q) = (t >> 2, t & 3) holds row i,
+// columns 16q .. 16q+15 in registers.  Per step: the owners of column k
+// publish it, every warp finds the first-max pivot redundantly, the pivot
+// row and row k trade places through shared memory, and each thread updates
+// its 16 entries (product, then subtraction).  Two barriers per step.
+#define GR_T 256
+__global__ void __launch_bounds__(GR_T, 1) gepp_reg_kernel(const double* src, int64_t ld, const int32_t* rowmap, int b,
+                                                          double* D, int32_t* piv, int32_t* gperm, DevState* st,
+                                                          int panel) {
+  __shared__ double colk[2][64];
+  __shared__ __align__(16) double prow[64], krow[64];
+  __shared__ int s_gp[64];
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x, lane = t & 31;
+  const int i = t >> 2, q = t & 3;
+  double a[16];
+  double mx = 0.0;
+  {
+    const bool rowok = i < b;
+    const int64_t row = rowok ? (rowmap ? rowmap[i] : i) : 0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 16 * q + s;
+      a[s] = rowok && j < b ? src[row * ld + j] : 0.0;
+      mx = fmax(mx, fabs(a[s]));
+    }
+  }
+  if (t < 64) s_gp[t] = t;
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    const int ks = k & 15, kq = k >> 4, cb = k & 1;
+    // 1. column k, rows >= k, published by its owners
+    double ak = a[0];
+#pragma unroll
+    for (int s = 1; s < 16; ++s)
+      if (s == ks) ak = a[s];
+    if (q == kq && i < b) colk[cb][i] = ak;
+    __syncthreads();
+    // 2. first-max pivot (every warp, redundantly)
+    double best = -1.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = k + lane + 32 * u;
+      if (r < b) {
+        const double v = fabs(colk[cb][r]);
+        if (v > best) { best = v; bi = r; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (best == 0.0) {
+      if (t == 0) prrp_set_error(st, PRRP_ERR_SINGULAR_MATRIX, panel, -1, k, 0.0);
+      return;
+    }
+    const int pv = bi;
+    // 3. rows k and pv trade places through shared memory
+    if (i == pv) {
+#pragma unroll
+      for (int s = 0; s < 16; s += 2) *reinterpret_cast<double2*>(&prow[16 * q + s]) = make_double2(a[s], a[s + 1]);
+    }
+    if (i == k && pv != k) {
+#pragma unroll
+      for (int s = 0; s < 16; s += 2) *reinterpret_cast<double2*>(&krow[16 * q + s]) = make_double2(a[s], a[s + 1]);
+    }
+    if (t == 0) {
+      piv[k] = pv;
+      if (pv != k) { const int g = s_gp[k]; s_gp[k] = s_gp[pv]; s_gp[pv] = g; }
+    }
+    __syncthreads();
+    if (pv != k) {
+      if (i == k) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) a[s] = prow[16 * q + s];
+      } else if (i == pv) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) a[s] = krow[16 * q + s];
+      }
+    }
+    // 4. multiplier and rank-1 update of rows k+1 .. b-1
+    if (i > k && i < b) {
+      const double ckk = colk[cb][pv];
+      const double cik = colk[cb][i == pv ? k : i];
+      const double l = div_fast(cik, ckk, __drcp_rn(ckk));
+      // columns >= b are zero in a[] and prow[]: updating them is exact and harmless
+      if (16 * q > k) {
+#pragma unroll
+        for (int s = 0; s < 16; s += 2) {
+          const double2 pr = *reinterpret_cast<const double2*>(&prow[16 * q + s]);
+          a[s] = sub_rn(a[s], mul_rn(l, pr.x));
+          a[s + 1] = sub_rn(a[s + 1], mul_rn(l, pr.y));
+          const double m0 = fabs(a[s]), m1 = fabs(a[s + 1]);
+          const double m01 = m0 > m1 ? m0 : m1;
+          mx = m01 > mx ? m01 : mx;
+        }
+      } else if (16 * q + 15 >= k) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const int j = 16 * q + s;
+          if (j == k) a[s] = l;
+          if (j > k) {
+            a[s] = sub_rn(a[s], mul_rn(l, prow[j]));
+            const double m0 = fabs(a[s]);
+            mx = m0 > mx ? m0 : mx;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (i < b) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int j = 16 * q + s;
+      if (j < b) D[(int64_t)i * b + j] = a[s];
+    }
+  }
+  if (t < b) gperm[t] = s_gp[t];
+  const double m = block_max(mx, red);
+  if (t == 0) atomic_max_abs(&st->finish_max, m);
+}
+
 // ---------------------------------------------------------------------------
 // Finalize a panel after the fast multiplier kernel: reduce the candidates,
 // run the strong-RRQR swap loop if the tau bound is violated (rare; QR from

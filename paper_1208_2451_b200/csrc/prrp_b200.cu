@@ -288,6 +288,13 @@ void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Arg
   CU_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
+// GEPP of a b x b block (register kernel for b <= 64, shared-memory kernel above)
+void launch_gepp(const double* src, int64_t ld, const int32_t* rowmap, int b, double* D, int32_t* piv,
+                 int32_t* gperm, DevState* st, int panel, cudaStream_t s) {
+  if (b <= 64) gepp_reg_kernel<<<1, GR_T, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
+  else gepp_diag_kernel<<<1, 128, (size_t)b * (b + 1) * 8, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
+}
+
 // PRRP_GENERIC_PANEL=1 forces the generic shared-memory engine (A/B testing)
 bool force_generic_panel() {
   static int v = -1;
@@ -435,7 +442,7 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
   CU_TRY(cudaGetLastError());
   if (do_gepp) {
     tbegin(PRRP_K_GEPP, s);
-    gepp_diag_kernel<<<1, 128, (size_t)h * (h + 1) * 8, s>>>(a.src, a.ld, B.perm, h, D, piv, gperm, st, panel);
+    launch_gepp(a.src, a.ld, B.perm, h, D, piv, gperm, st, panel, s);
     tend(s);
     CU_TRY(cudaGetLastError());
   }
@@ -598,7 +605,7 @@ void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, c
 // Per-thread internal streams (main: high priority, side: low priority) and a
 // reusable pool of dependency events.
 struct Streams {
-  cudaStream_t main = nullptr, side = nullptr;
+  cudaStream_t main = nullptr, side = nullptr, fin = nullptr;
   std::vector<cudaEvent_t> evs;
   cudaEvent_t ev(int i) {
     while ((int)evs.size() <= i) {
@@ -617,6 +624,7 @@ Streams& streams() {
     CU_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU_TRY(cudaStreamCreateWithPriority(&s.main, cudaStreamNonBlocking, hi));
     CU_TRY(cudaStreamCreateWithPriority(&s.side, cudaStreamNonBlocking, lo));
+    CU_TRY(cudaStreamCreateWithPriority(&s.fin, cudaStreamNonBlocking, hi));
   }
   return s;
 }
@@ -672,16 +680,19 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   // ---- look-ahead schedule over two streams:
   //   main (high priority, critical path): QRCP(k) -> trsm -> finalize ->
   //        [wait side(k-1)] -> permute(k) -> narrow Schur(k) (panel k+1's columns)
-  //   side (low priority): [wait permute(k)] wide Schur(k) -> GEPP of A11 ->
-  //        compose(k) -> [wait narrow(k)] blockrow(k)
-  // so QRCP(k+1) overlaps the trailing update and the finish of panel k.
+  //   fin (high priority): [wait permute(k)] GEPP of A11 -> compose(k)
+  //   side (low priority): [wait narrow(k)] wide Schur(k) -> [wait fin(k)] blockrow(k)
+  // so QRCP(k+1), the trailing update and the finish of panel k overlap.
+  // D / piv / gperm are single buffers: GEPP(k+1) waits for permute(k+1),
+  // which waits for blockrow(k).
   Streams& ss = streams();
-  cudaStream_t sm = ss.main, sd = ss.side;
+  cudaStream_t sm = ss.main, sd = ss.side, sf = ss.fin;
   {
     cudaEvent_t e0 = ss.ev(0);
     CU_TRY(cudaEventRecord(e0, s));
     CU_TRY(cudaStreamWaitEvent(sm, e0, 0));
     CU_TRY(cudaStreamWaitEvent(sd, e0, 0));
+    CU_TRY(cudaStreamWaitEvent(sf, e0, 0));
   }
   double* L21b[2] = {L21, ar.get<double>((size_t)b * ldl)};
   cudaEvent_t side_done = nullptr;
@@ -717,23 +728,29 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
       if (width > wn)
         schur_update(A + (col0 + bj) * lda + col0 + bj + wn, lda, L, ldl, A + col0 * lda + col0 + bj + wn, lda,
                      rows - bj, width - wn, bj, st, sd);
-      tbegin(PRRP_K_GEPP, sd);
-      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, sd>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
-      tend(sd);
+      // fin stream: GEPP of the pivot block and the multiplier compose,
+      // concurrent with the trailing update
+      CU_TRY(cudaStreamWaitEvent(sf, ev_perm, 0));
+      tbegin(PRRP_K_GEPP, sf);
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, sf);
+      tend(sf);
       CU_TRY(cudaGetLastError());
       const int ctw = bj > 64 ? 64 : 128;
-      tbegin(PRRP_K_COMPOSE, sd);
+      tbegin(PRRP_K_COMPOSE, sf);
       if (!force_generic_panel())
-        launch_compose_w(L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, sd);
+        launch_compose_w(L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, sf);
       else
-        compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, sd>>>(
+        compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, sf>>>(
             L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
-      tend(sd);
+      tend(sf);
       CU_TRY(cudaGetLastError());
+      cudaEvent_t ev_fin = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_fin, sf));
+      CU_TRY(cudaStreamWaitEvent(sd, ev_fin, 0));
     } else {
       if (side_done) CU_TRY(cudaStreamWaitEvent(sd, side_done, 0));
       tbegin(PRRP_K_GEPP, sd);
-      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, sd>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, sd);
       tend(sd);
       CU_TRY(cudaGetLastError());
     }
@@ -1040,7 +1057,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
       if (width > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lphys, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
                      width, bj, st, s);
-      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
       launch_compose_w(Lphys, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
     } else {
       // last square block: bring the rows into logical order, then GEPP
@@ -1048,7 +1065,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
                                              st);
       permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
           A, lda, col0, n, B.moved, perm, st, panel);
-      gepp_diag_kernel<<<1, 128, (size_t)bj * (bj + 1) * 8, s>>>(blk, lda, nullptr, bj, D, piv, gperm, st, panel);
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
     }
     CU_TRY(cudaGetLastError());
     launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
@@ -1328,7 +1345,7 @@ int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* pe
     int32_t* gperm = ar.get<int32_t>(m);
     iota_kernel<<<1, 128, 0, s>>>(perm, m);
     maxabs_kernel<<<caps().sms, 256, 0, s>>>(A, lda, m, n, st);
-    gepp_diag_kernel<<<1, 128, (size_t)m * (m + 1) * 8, s>>>(A, lda, nullptr, m, D, piv, gperm, st, 0);
+    launch_gepp(A, lda, nullptr, m, D, piv, gperm, st, 0, s);
     blockrow_kernel<<<(unsigned)((n + BR_TW - 1) / BR_TW), BR_TW, ((size_t)m * m + (size_t)m * BR_TW) * 8, s>>>(
         A, lda, 0, m, n, D, piv, gperm, perm, st);
     CU_TRY(cudaGetLastError());
