@@ -26,9 +26,22 @@
 __device__ __forceinline__ int upk(int i, int q) { return q * (q + 1) / 2 + i; }
 
 __device__ void load_r11(const double* Rbuf, int64_t p, int bsel, double* r11) {
-  for (int idx = threadIdx.x; idx < bsel * bsel; idx += blockDim.x) {
-    const int i = idx / bsel, q = idx % bsel;
-    if (i <= q) r11[upk(i, q)] = Rbuf[(int64_t)i * p + q];
+  // 8 independent loads in flight per thread (the loop is L2-latency bound)
+  const int T = blockDim.x, tot = bsel * bsel;
+  for (int base = threadIdx.x; base < tot; base += 8 * T) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * T;
+      const int i = idx / bsel, q = idx - i * bsel;
+      v[u] = (idx < tot && i <= q) ? Rbuf[(int64_t)i * p + q] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * T;
+      const int i = idx / bsel, q = idx - i * bsel;
+      if (idx < tot && i <= q) r11[upk(i, q)] = v[u];
+    }
   }
 }
 
@@ -492,7 +505,10 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
       const int32_t j = a.perm[q];
       if (j != q) { a.moved[2 * off] = (int32_t)q; a.moved[2 * off + 1] = j; ++off; }
     }
-    if (t == blockDim.x - 1) a.st->moved = off;
+    if (t == blockDim.x - 1) {
+      a.st->moved = off;
+      if (a.moved_cnt) *a.moved_cnt = off;
+    }
   }
   __syncthreads();
   if (f.do_gepp) {

@@ -59,6 +59,7 @@ struct PanelArgs {
   int64_t ldl;
   int32_t* swaps_out;       // host-visible per-panel swap count (device pointer)
   int32_t* moved;           // out: compact list of moved positions (dst pos, src j) pairs
+  int32_t* moved_cnt;       // optional out: number of moved pairs (besides DevState::moved)
   long long* prof;          // optional: per-phase clock64 totals of CTA 0 (diagnostics)
   int swap_slot;            // index into swaps_dev for this node's swap count
   int tree_level, tree_index;   // CALU tournament node (error payload), -1 otherwise

@@ -184,7 +184,7 @@ struct Arena {
 // Optional per-kernel-class device timing: CUDA events recorded around every
 // launch on the launching stream, summed after the final synchronisation.
 struct Timer {
-  struct Span { int cls; cudaEvent_t a, b; };
+  struct Span { int cls; cudaEvent_t a, b; cudaStream_t s; };
   std::vector<Span> spans;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
@@ -197,7 +197,7 @@ struct Timer {
     return pool[used++];
   }
   void begin(int cls, cudaStream_t s) {
-    Span sp{cls, ev(), nullptr};
+    Span sp{cls, ev(), nullptr, s};
     CU_TRY(cudaEventRecord(sp.a, s));
     spans.push_back(sp);
   }
@@ -218,6 +218,24 @@ struct Timer {
       float ms = 0.f;
       CU_TRY(cudaEventElapsedTime(&ms, spans.front().a, spans.back().b));
       t->total_ms = ms;
+    }
+    // PRRP_TRACE=<file>: one CSV line per timed span (class, stream, start, end in ms)
+    if (const char* path = getenv("PRRP_TRACE")) {
+      if (FILE* f = fopen(path, "w")) {
+        static const char* names[PRRP_K_COUNT] = {"panel", "trsm", "finalize", "permute", "schur",
+                                                  "compose", "blockrow", "gepp", "other"};
+        std::vector<cudaStream_t> ids;
+        fprintf(f, "class,stream,start_ms,end_ms\n");
+        for (const Span& sp : spans) {
+          size_t id = std::find(ids.begin(), ids.end(), sp.s) - ids.begin();
+          if (id == ids.size()) ids.push_back(sp.s);
+          float a = 0.f, b = 0.f;
+          CU_TRY(cudaEventElapsedTime(&a, spans.front().a, sp.a));
+          CU_TRY(cudaEventElapsedTime(&b, spans.front().a, sp.b));
+          fprintf(f, "%s,%zu,%.4f,%.4f\n", names[sp.cls], id, a, b);
+        }
+        fclose(f);
+      }
     }
   }
   ~Timer() {
@@ -326,6 +344,7 @@ struct PanelBuffers {
   long long* cand_flat;
   int32_t* moved;
   double* refl;
+  int32_t* moved_cnt = nullptr;
 };
 
 constexpr int kMaxCand = 2048;   // trsm blocks per panel (candidate slots)
@@ -368,6 +387,7 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.L21 = L21;
   a.ldl = ldl;
   a.moved = B.moved;
+  a.moved_cnt = B.moved_cnt;
   a.prof = tl_prof;
   tbegin(PRRP_K_PANEL, s);
   const int maxc = caps().max_cluster;
@@ -656,9 +676,12 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   B.cand_flat = ar.get<long long>(kMaxCand);
   B.moved = ar.get<int32_t>(2 * m);
   B.refl = nullptr;
-  double* D = ar.get<double>((size_t)b * b);
-  int32_t* piv = ar.get<int32_t>(b);
-  int32_t* gperm = ar.get<int32_t>(b);
+  // per-panel-parity buffers (the three streams overlap consecutive panels)
+  int32_t* movedb[2] = {B.moved, ar.get<int32_t>(2 * m)};
+  int32_t* mcntb = ar.get<int32_t>(2);
+  double* Db[2] = {ar.get<double>((size_t)b * b), ar.get<double>((size_t)b * b)};
+  int32_t* pivb[2] = {ar.get<int32_t>(b), ar.get<int32_t>(b)};
+  int32_t* gpermb[2] = {ar.get<int32_t>(b), ar.get<int32_t>(b)};
   int32_t* swaps_dev = ar.get<int32_t>(npanels);
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
 
@@ -677,14 +700,21 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   tend(s);
   CU_TRY(cudaGetLastError());
 
-  // ---- look-ahead schedule over two streams:
-  //   main (high priority, critical path): QRCP(k) -> trsm -> finalize ->
-  //        [wait side(k-1)] -> permute(k) -> narrow Schur(k) (panel k+1's columns)
-  //   fin (high priority): [wait permute(k)] GEPP of A11 -> compose(k)
-  //   side (low priority): [wait narrow(k)] wide Schur(k) -> [wait fin(k)] blockrow(k)
-  // so QRCP(k+1), the trailing update and the finish of panel k overlap.
-  // D / piv / gperm are single buffers: GEPP(k+1) waits for permute(k+1),
-  // which waits for blockrow(k).
+  // ---- look-ahead schedule over three streams.  Panel
+  // k's row moves are applied by column range, each part on the stream that
+  // next touches those columns:
+  //   main (high priority, critical path): [wait side(k-2), fin(k-2)] QRCP(k)
+  //        -> trsm -> finalize -> [wait W1(k-1)] -> permute(k) of columns
+  //        [col0, col0+2b) -> narrow Schur(k) (panel k+1's columns)
+  //   fin (high priority): [wait permute(k)] permute(k) of columns [0, col0)
+  //        + row order -> GEPP of A11 -> compose(k)
+  //   side (low priority): [wait narrow(k)] permute(k) of columns >= col0+2b
+  //        -> W1(k) (the next narrow region) -> W2(k) (the rest) -> [wait
+  //        fin(k)] blockrow(k)
+  // Panel k's moved rows are >= col0 and blockrow(k-1) writes rows < col0,
+  // so the three parts never touch the same words.  L21, the moved list and
+  // the GEPP outputs are double-buffered by panel parity; the waits on
+  // side(k-2) / fin(k-2) guard their reuse.
   Streams& ss = streams();
   cudaStream_t sm = ss.main, sd = ss.side, sf = ss.fin;
   {
@@ -695,42 +725,56 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     CU_TRY(cudaStreamWaitEvent(sf, e0, 0));
   }
   double* L21b[2] = {L21, ar.get<double>((size_t)b * ldl)};
-  cudaEvent_t side_done = nullptr;
+  std::vector<cudaEvent_t> side_ev(npanels, nullptr), fin_ev(npanels, nullptr);
+  cudaEvent_t w1_prev = nullptr, side_done = nullptr;
   int evi = 1;
   int panel = 0;
+  auto permute_cols = [&](int64_t c_lo, int64_t c_hi, int64_t row0, const int32_t* mv, const int32_t* mc,
+                          int64_t* pp, cudaStream_t q) {
+    if (c_hi <= c_lo && !pp) return;
+    const int64_t nc = std::max<int64_t>(c_hi - c_lo, 1);
+    const unsigned grid = (unsigned)std::min<int64_t>((nc + 31) / 32, 2 * sms);
+    permute_cols_kernel<<<grid, 256, 0, q>>>(A, lda, row0, c_lo, std::max(c_lo, c_hi), mv, mc, pp, st, panel);
+    CU_TRY(cudaGetLastError());
+  };
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
     const int64_t rows = m - col0;
     const int64_t width = n - col0 - bj;
+    const int par = panel & 1;
     double* blk = A + col0 * lda + col0;
-    double* L = L21b[panel & 1];
+    double* L = L21b[par];
+    double* D = Db[par];
+    int32_t* piv = pivb[par];
+    int32_t* gperm = gpermb[par];
     if (rows > bj) {
-      strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L, ldl, B, st, swaps_dev, D, piv, gperm, false, sm);
-      if (side_done) CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
+      if (panel >= 2) {
+        CU_TRY(cudaStreamWaitEvent(sm, side_ev[panel - 2], 0));
+        CU_TRY(cudaStreamWaitEvent(sm, fin_ev[panel - 2], 0));
+      }
+      PanelBuffers Bk = B;
+      Bk.moved = movedb[par];
+      Bk.moved_cnt = mcntb + par;
+      strong_rrqr_panel(blk, lda, bj, rows, bj, tau, panel, L, ldl, Bk, st, swaps_dev, D, piv, gperm, false, sm);
+      if (w1_prev) CU_TRY(cudaStreamWaitEvent(sm, w1_prev, 0));
+      const int64_t wn = std::min<int64_t>(width, b);
       tbegin(PRRP_K_PERMUTE, sm);
-      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, sm>>>(
-          A, lda, col0, n, B.moved, perm, st, panel);
+      permute_cols(col0, col0 + bj + wn, col0, Bk.moved, Bk.moved_cnt, nullptr, sm);
       tend(sm);
-      CU_TRY(cudaGetLastError());
       cudaEvent_t ev_perm = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_perm, sm));
       // narrow update: the next panel's b columns, on the critical path
-      const int64_t wn = std::min<int64_t>(width, b);
       if (wn > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
                      bj, st, sm);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
-      // side stream: wide update, diagonal-block GEPP, compose, block row.  It
-      // is released only after the narrow update, i.e. together with QRCP(k+1)
-      // on the high-priority stream, so the panel cluster claims its GPC first.
-      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
-      if (width > wn)
-        schur_update(A + (col0 + bj) * lda + col0 + bj + wn, lda, L, ldl, A + col0 * lda + col0 + bj + wn, lda,
-                     rows - bj, width - wn, bj, st, sd);
-      // fin stream: GEPP of the pivot block and the multiplier compose,
-      // concurrent with the trailing update
+      // fin stream: L-part row moves + row order, GEPP of the pivot block,
+      // multiplier compose -- concurrent with the trailing update
       CU_TRY(cudaStreamWaitEvent(sf, ev_perm, 0));
+      tbegin(PRRP_K_PERMUTE, sf);
+      permute_cols(0, col0, col0, Bk.moved, Bk.moved_cnt, perm, sf);
+      tend(sf);
       tbegin(PRRP_K_GEPP, sf);
       launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, sf);
       tend(sf);
@@ -744,11 +788,27 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
             L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
       tend(sf);
       CU_TRY(cudaGetLastError());
-      cudaEvent_t ev_fin = ss.ev(evi++);
-      CU_TRY(cudaEventRecord(ev_fin, sf));
-      CU_TRY(cudaStreamWaitEvent(sd, ev_fin, 0));
+      fin_ev[panel] = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(fin_ev[panel], sf));
+      // side stream: trailing row moves, wide update (next narrow region
+      // first), block row
+      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
+      const int64_t cw0 = col0 + bj + wn;
+      tbegin(PRRP_K_PERMUTE, sd);
+      permute_cols(cw0, n, col0, Bk.moved, Bk.moved_cnt, nullptr, sd);
+      tend(sd);
+      const int64_t w1 = std::min<int64_t>(n - cw0, b);
+      if (w1 > 0)
+        schur_update(A + (col0 + bj) * lda + cw0, lda, L, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd);
+      w1_prev = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(w1_prev, sd));
+      if (n - cw0 > w1)
+        schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, L, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
+                     n - cw0 - w1, bj, st, sd);
+      CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
     } else {
-      if (side_done) CU_TRY(cudaStreamWaitEvent(sd, side_done, 0));
+      // last block (rows == bj): all its updates and row moves came through main
+      // (narrow) and fin (L part), both already awaited by the side stream
       tbegin(PRRP_K_GEPP, sd);
       launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, sd);
       tend(sd);
@@ -764,6 +824,7 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     CU_TRY(cudaGetLastError());
     side_done = ss.ev(evi++);
     CU_TRY(cudaEventRecord(side_done, sd));
+    side_ev[panel] = side_done;
   }
   CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
   tbegin(PRRP_K_OTHER, sm);   // closing mark for the timer span

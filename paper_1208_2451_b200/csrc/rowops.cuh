@@ -73,6 +73,47 @@ __global__ void __launch_bounds__(256) permute_kernel(double* A, int64_t lda, in
     for (int r = threadIdx.x; r < cnt; r += blockDim.x) p[row0 + moved[2 * r]] = ptmp[r];
 }
 
+// Column-range variant for the look-ahead schedule: the moved rows of one
+// panel, columns [c_lo, c_hi) only (three launches on three streams cover
+// the panel + next panel, the trailing columns and the L part); the pair
+// count comes from moved_cnt (double-buffered per panel).  Blocks stage up
+// to PC_CAP doubles: cpb = min(32, PC_CAP / cnt) columns per pass.  The
+// launch with p != nullptr also moves the global row order.
+#define PC_CAP 6144
+__global__ void __launch_bounds__(256) permute_cols_kernel(double* A, int64_t lda, int64_t row0, int64_t c_lo,
+                                                          int64_t c_hi, const int32_t* moved, const int32_t* moved_cnt,
+                                                          int64_t* p, DevState* st, int panel) {
+  __shared__ __align__(16) double tmp[PC_CAP];
+  if (prrp_failed(st)) return;
+  const int cnt = *moved_cnt;
+  if (cnt == 0) return;
+  if (cnt > PC_CAP) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) prrp_set_error(st, PRRP_ERR_UNSUPPORTED, panel, -1, -1, 0.0);
+    return;
+  }
+  const int t = threadIdx.x;
+  const int cpb = min(32, PC_CAP / cnt);
+  for (int64_t c0 = c_lo + (int64_t)blockIdx.x * cpb; c0 < c_hi; c0 += (int64_t)gridDim.x * cpb) {
+    const int cw = (int)min((int64_t)cpb, c_hi - c0);
+    for (int e = t; e < cnt * cw; e += blockDim.x) {
+      const int r = e / cw, cc = e - r * cw;
+      tmp[e] = A[(row0 + moved[2 * r + 1]) * lda + c0 + cc];
+    }
+    __syncthreads();
+    for (int e = t; e < cnt * cw; e += blockDim.x) {
+      const int r = e / cw, cc = e - r * cw;
+      A[(row0 + moved[2 * r]) * lda + c0 + cc] = tmp[e];
+    }
+    __syncthreads();
+  }
+  if (p && blockIdx.x == 0) {
+    int64_t* pt = reinterpret_cast<int64_t*>(tmp);
+    for (int r = t; r < cnt; r += blockDim.x) pt[r] = p[row0 + moved[2 * r + 1]];
+    __syncthreads();
+    for (int r = t; r < cnt; r += blockDim.x) p[row0 + moved[2 * r]] = pt[r];
+  }
+}
+
 // Block row finish.  Columns [0, col0): rows col0.. permuted by gperm.
 // Columns [col0, col0+b): packed L11\U11 from D.  Columns [col0+b, n):
 // pivots + elimination with L11 (strictly lower part of D), running max.
