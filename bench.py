@@ -238,17 +238,20 @@ def run_device(args):
     err = _lib.PrrpErr()
     lib.prrp_b200_dmma_peak(1500.0, ctypes.byref(pk), ctypes.byref(err))
     achieved = schur_flops / (schur_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_note = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_schur_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            ps = json.load(open(prof))
+            traffic = ps.get("dram_bytes_per_launch")
+            traffic_note = (f"dram read+write of {ps.get('reference_launch')} from {ps.get('report')}; "
+                            f"algorithmic bytes of that launch {ps.get('algorithmic_bytes_reference_launch')}")
         except Exception:
             traffic = None
     breakdown = {k: round(sum(t.ms[i] for t in tms) / len(tms), 4) for i, k in enumerate(_lib.KCLASSES)}
     roofline = {"bound": "tensor", "kernel": "schur_dmma_kernel (DMMA.8x8x4, TMA-fed)", "achieved": achieved,
                 "peak": pk.value, "unit": "TFLOP/s", "frac": achieved / pk.value if pk.value else None,
-                "traffic": traffic,
+                "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "measured live: register-resident mma.sync.m8n8k4.f64 loop on all SMs, 1.5 s "
                                "(MEASURED_PEAKS.json has no FP64 entry)",
                 "achieved_def": "sum over panels of 2*M*N*b / summed schur_dmma_kernel event time per step",
