@@ -79,30 +79,49 @@ __global__ void __launch_bounds__(256) permute_kernel(double* A, int64_t lda, in
 // count comes from moved_cnt (double-buffered per panel).  Blocks stage up
 // to PC_CAP doubles: cpb = min(32, PC_CAP / cnt) columns per pass.  The
 // launch with p != nullptr also moves the global row order.
-#define PC_CAP 6144
+#define PC_CAP 4096
+#define PC_ROWS 1024
 __global__ void __launch_bounds__(256) permute_cols_kernel(double* A, int64_t lda, int64_t row0, int64_t c_lo,
                                                           int64_t c_hi, const int32_t* moved, const int32_t* moved_cnt,
                                                           int64_t* p, DevState* st, int panel) {
   __shared__ __align__(16) double tmp[PC_CAP];
+  __shared__ int64_t srow[PC_ROWS], drow[PC_ROWS];   // source / destination row offsets (elements)
   if (prrp_failed(st)) return;
   const int cnt = *moved_cnt;
   if (cnt == 0) return;
-  if (cnt > PC_CAP) {
+  if (cnt > PC_ROWS) {
     if (blockIdx.x == 0 && threadIdx.x == 0) prrp_set_error(st, PRRP_ERR_UNSUPPORTED, panel, -1, -1, 0.0);
     return;
   }
   const int t = threadIdx.x;
+  for (int r = t; r < cnt; r += blockDim.x) {
+    srow[r] = (row0 + moved[2 * r + 1]) * lda;
+    drow[r] = (row0 + moved[2 * r]) * lda;
+  }
+  __syncthreads();
   const int cpb = min(32, PC_CAP / cnt);
   for (int64_t c0 = c_lo + (int64_t)blockIdx.x * cpb; c0 < c_hi; c0 += (int64_t)gridDim.x * cpb) {
     const int cw = (int)min((int64_t)cpb, c_hi - c0);
-    for (int e = t; e < cnt * cw; e += blockDim.x) {
-      const int r = e / cw, cc = e - r * cw;
-      tmp[e] = A[(row0 + moved[2 * r + 1]) * lda + c0 + cc];
+    const int tot = cnt * cw;
+    // 8 independent loads in flight per thread, then the staging stores
+    for (int e0 = t; e0 < tot; e0 += 8 * blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        const int r = e / cw, cc = e - r * cw;
+        v[u] = e < tot ? A[srow[r] + c0 + cc] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < tot) tmp[e] = v[u];
+      }
     }
     __syncthreads();
-    for (int e = t; e < cnt * cw; e += blockDim.x) {
+    for (int e = t; e < tot; e += blockDim.x) {
       const int r = e / cw, cc = e - r * cw;
-      A[(row0 + moved[2 * r]) * lda + c0 + cc] = tmp[e];
+      A[drow[r] + c0 + cc] = tmp[e];
     }
     __syncthreads();
   }
