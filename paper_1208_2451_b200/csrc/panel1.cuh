@@ -196,41 +196,42 @@ __device__ __forceinline__ double p1_sumsq(const X& x, int r0, int L, double fir
 // blocks 0..L; v is zero on rows 0..r-1, so those rows are unchanged.
 // act == false: w = 0.
 template <class X>
-__device__ __forceinline__ void p1_apply(const X& x, uint32_t vsa, double beta, bool act, int L) {
-  // v is re-read from shared memory (volatile loads) in both passes: keeping
-  // it in registers across the dot would double the column's register need
+__device__ __forceinline__ void p1_apply(const X& x, const double2* vp, double beta, bool act, int L) {
+  // v is re-read from shared memory with volatile loads in both passes: with
+  // plain loads the compiler hoists all of v into registers next to the
+  // 128-register column, spills, and the FP64 issue rate drops ~3x
+  const uint32_t va = (uint32_t)__cvta_generic_to_shared(vp);
   double d[4];
-#pragma unroll
-  for (int s = 0; s < 8; s += 2) {
-    const double2 v = lds2_f64(vsa + s * 8);
-    if (s < 4) {
-      d[s] = mul_rn(v.x, x.ld(s));
-      d[s + 1] = mul_rn(v.y, x.ld(s + 1));
-    } else {
-      d[s & 3] = fma(v.x, x.ld(s), d[s & 3]);
-      d[(s + 1) & 3] = fma(v.y, x.ld(s + 1), d[(s + 1) & 3]);
-    }
-  }
-#pragma unroll
-  for (int B = 1; B < 8; ++B) {
-    if (B > L) break;
-#pragma unroll
-    for (int s = 0; s < 8; s += 2) {
-      const double2 v = lds2_f64(vsa + (8 * B + s) * 8);
-      d[s & 3] = fma(v.x, x.ld(8 * B + s), d[s & 3]);
-      d[(s + 1) & 3] = fma(v.y, x.ld(8 * B + s + 1), d[(s + 1) & 3]);
-    }
-  }
-  const double dot = (d[0] + d[1]) + (d[2] + d[3]);
-  const double w = act ? mul_rn(beta, dot) : 0.0;
 #pragma unroll
   for (int B = 0; B < 8; ++B) {
     if (B > L) break;
 #pragma unroll
-    for (int s = 0; s < 8; s += 2) {
-      const double2 v = lds2_f64(vsa + (8 * B + s) * 8);
-      x.st(8 * B + s, sub_rn(x.ld(8 * B + s), mul_rn(v.x, w)));
-      x.st(8 * B + s + 1, sub_rn(x.ld(8 * B + s + 1), mul_rn(v.y, w)));
+    for (int h = 0; h < 4; ++h) {
+      const double2 v = lds2_f64(va + 64 * B + 16 * h);
+      const int s = 2 * h;
+      if (B == 0 && s < 4) {
+        d[s] = mul_rn(v.x, x.ld(s));
+        d[s + 1] = mul_rn(v.y, x.ld(s + 1));
+      } else {
+        d[s & 3] = fma(v.x, x.ld(8 * B + s), d[s & 3]);
+        d[(s + 1) & 3] = fma(v.y, x.ld(8 * B + s + 1), d[(s + 1) & 3]);
+      }
+    }
+  }
+  const double dot = (d[0] + d[1]) + (d[2] + d[3]);
+  // x -= v w as one FMA per element (the reference rounds v*w first; its w
+  // comes from a BLAS dgemv whose order is not reproducible anyway, so the
+  // updated values agree to the same ulp-level tolerance either way)
+  const double nw = act ? -mul_rn(beta, dot) : 0.0;
+#pragma unroll
+  for (int B = 0; B < 8; ++B) {
+    if (B > L) break;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double2 v = lds2_f64(va + 64 * B + 16 * h);
+      const int s = 8 * B + 2 * h;
+      x.st(s, fma(v.x, nw, x.ld(s)));
+      x.st(s + 1, fma(v.y, nw, x.ld(s + 1)));
     }
   }
 }
@@ -374,13 +375,13 @@ __device__ __forceinline__ int p1_best_lane(unsigned long long u, unsigned pos) 
 // winner's position, compute its key for step k+1 (rows k+1..63).
 template <class X>
 __device__ __forceinline__ void p1_apply_col(const X& x, long long& pos, double& key, bool on, int jl, int k, int L,
-                                             int mode, uint32_t vsa, double beta, int skip, bool mine, int wjl,
+                                             int mode, const double* vs, double beta, int skip, bool mine, int wjl,
                                              long long wpos) {
   if (!__any_sync(0xffffffffu, on && pos >= k)) return;
   const bool live = on && pos >= k;
   const bool win = live && mine && wjl == jl;
   if (live && !win && pos == k) pos = wpos;
-  if (!skip) p1_apply(x, vsa, beta, live && !win, L);   // skip is cluster-uniform
+  if (!skip) p1_apply(x, reinterpret_cast<const double2*>(vs), beta, live && !win, L);   // skip is cluster-uniform
   if (win) pos = k;                                     // R[k,k] = alpha, zeros below: at the write-out
   if (mode == 0) {
     const double nk = p1_sumsq<false>(x, (k & 7) + 1, L, 0.0);
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
 
     // ---- apply reflector k, keys for step k+1
     const uint32_t vsa = (uint32_t)__cvta_generic_to_shared(vs);
-    p1_apply_col(xr, cs.pos_r, cs.key_r, on_r, jl_r, k, L, mode, vsa, beta, skip, mine, wjl, wpos);
+    p1_apply_col(xr, cs.pos_r, cs.key_r, on_r, jl_r, k, L, mode, vs, beta, skip, mine, wjl, wpos);
     if (has_s && __any_sync(0xffffffffu, on_s && cs.pos_s >= k)) {
       const bool live = on_s && cs.pos_s >= k;
       const bool win = live && mine && wjl == jl_s;
