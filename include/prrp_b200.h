@@ -170,6 +170,29 @@ int prrp_schur_update(double* C, int64_t ldc, const double* L, int64_t ldl,
 int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* perm,
                        double* intermediate_max, prrp_err* err, void* stream);
 
+/* QR with column pivoting over min(h, p) steps of an h x p column-major
+ * matrix — replaces prrp.qr_column_pivoting (pivoted_qr.py:74-87): exact
+ * numpy-pairwise column norms each step, first maximum, Householder steps
+ * of _reflect.  R h x p, Q h x h (column-major), perm int64[p] (device).
+ * Requires h <= 128. */
+int prrp_qrcp(const double* a, int64_t lda, int32_t h, int64_t p, double* R, double* Q,
+              int64_t* perm, prrp_err* err, void* stream);
+
+/* Verification: resid_sq = ||Pi A - L U||_F^2 and
+ * a_sq = ||A||_F^2 (host doubles) for packed factors LU (m x n row-major,
+ * unit lower L below the diagonal, U on and above) of the m x n row-major A
+ * with row order perm (device int64[m]) — the quantities of
+ * prrp.metrics.rel_factorization_error (metrics.py:56-63). */
+int prrp_lu_residual(const double* A, int64_t lda, const double* LU, int64_t ldlu,
+                     const int64_t* perm, int64_t m, int64_t n, double* resid_sq, double* a_sq,
+                     prrp_err* err, void* stream);
+
+/* Solve A X = B with the packed square factors — replaces prrp.luprrp_solve
+ * (luprrp.py:204-214).  B, X: n x nrhs column-major (device); SingularFactor
+ * on an exact-zero U diagonal. */
+int prrp_lu_solve(const double* LU, int64_t ldlu, int64_t n, const int64_t* perm, const double* B,
+                  int64_t ldb, double* X, int64_t ldx, int32_t nrhs, prrp_err* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,9 @@ SIGNATURES = {
     "prrp_caluprrp": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_strong_rrqr": ([_P, _I64, _I32, _I64, _I32, _D, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_householder_qr": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_qrcp": ([_P, _I64, _I32, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_lu_residual": ([_P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_lu_solve": ([_P, _I64, _I64, _P, _P, _I64, _P, _I64, _I32, _P, _P], ctypes.c_int),
     "prrp_multiplier_block": ([_P, _I64, _I32, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
     "prrp_schur_update": ([_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I32, _P, _P, _P], ctypes.c_int),
     "prrp_gepp_blockrow": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),

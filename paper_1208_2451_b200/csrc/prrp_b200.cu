@@ -19,6 +19,7 @@
 
 #include "panel.cuh"
 #include "lsolve.cuh"
+#include "verify.cuh"
 #include "panel64.cuh"
 #include "panel1.cuh"
 #include "tri64.cuh"
@@ -1327,6 +1328,119 @@ int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p, doub
     int64_t* dummy_perm = ar.get<int64_t>(p);
     r_out_kernel<<<caps().sms, 256, 0, s>>>(Rbuf, h, p, permb, R, dummy_perm);
     form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(refl, h, steps, Q);
+    CU_TRY(cudaGetLastError());
+    DevState hs;
+    read_state(st, hs, s);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+// QR with column pivoting over min(h, p) steps (pivoted_qr.py:74-87): the
+// cluster engine in pivoted mode, reflector log -> explicit Q.
+int prrp_qrcp(const double* a, int64_t lda, int32_t h, int64_t p, double* R, double* Q, int64_t* perm, prrp_err* err,
+              void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "h > 128 is outside the device panel engine");
+    if (h < 1 || p < 1) fail(PRRP_ERR_ARG, "empty matrix");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    const PanelCfg g = panel_config(h, p, 1);
+    double* Rbuf = ar.get<double>((size_t)h * p);
+    int32_t* permb = ar.get<int32_t>(p);
+    const int steps = (int)std::min<int64_t>(h, p);
+    double* refl = ar.get<double>((size_t)steps * (h + 1));
+    double* ovf = ar.get<double>((size_t)g.C * h * std::max<int64_t>(1, g.ovpad));
+    PanelArgs pa{};
+    pa.src = a;
+    pa.ld = lda;
+    pa.h = h;
+    pa.p = p;
+    pa.bsel = 1;
+    pa.steps = steps;
+    pa.mode = 0;
+    pa.perm = permb;
+    pa.Rbuf = Rbuf;
+    pa.refl = refl;
+    pa.ovf = ovf;
+    pa.per = g.per;
+    pa.cap = g.cap;
+    pa.cap_pad = g.cap_pad;
+    pa.ovpad = g.ovpad;
+    pa.st = st;
+    pa.fro = &st->fro;
+    pa.tree_level = pa.tree_index = -1;
+    launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
+    r_out_kernel<<<caps().sms, 256, 0, s>>>(Rbuf, h, p, permb, R, perm);
+    form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(refl, h, steps, Q);
+    CU_TRY(cudaGetLastError());
+    DevState hs;
+    read_state(st, hs, s);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+// ||Pi A - L U||_F^2 and ||A||_F^2 from the packed factors (metrics.py:56-63)
+int prrp_lu_residual(const double* A, int64_t lda, const double* LU, int64_t ldlu, const int64_t* perm, int64_t m,
+                     int64_t n, double* resid_sq, double* a_sq, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (m < n || n < 1) fail(PRRP_ERR_DIM, "need m >= n >= 1");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    const int64_t ldc = n + (n & 1);
+    double* C = ar.get<double>((size_t)m * ldc);
+    const int KB = 64;
+    const int64_t ldlk = ((m + 7) / 8) * 8, lduk = ((n + 7) / 8) * 8;
+    double* Lk = ar.get<double>((size_t)KB * ldlk);
+    double* Uk = ar.get<double>((size_t)KB * lduk);
+    double* sums = ar.get<double>(2);
+    CU_TRY(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
+    const int sms = caps().sms;
+    gather_rows_kernel<<<sms * 8, 256, 0, s>>>(A, lda, perm, m, n, C, ldc);
+    for (int64_t k0 = 0; k0 < n; k0 += KB) {
+      const int kb = (int)std::min<int64_t>(KB, n - k0);
+      const int Kp = (kb + 3) / 4 * 4;
+      build_lk_kernel<<<sms * 4, 256, 0, s>>>(LU, ldlu, m, k0, kb, Kp, Lk, ldlk);
+      build_uk_kernel<<<sms * 4, 256, 0, s>>>(LU, ldlu, n, k0, kb, Kp, Uk, lduk);
+      CU_TRY(cudaGetLastError());
+      schur_update(C + k0 * ldc + k0, ldc, Lk, ldlk, Uk, lduk, m - k0, n - k0, Kp, st, s);
+    }
+    sumsq_kernel<<<sms * 4, 256, 0, s>>>(C, ldc, m, n, sums);
+    sumsq_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, sums + 1);
+    CU_TRY(cudaGetLastError());
+    double h[2];
+    CU_TRY(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, s));
+    DevState hs;
+    read_state(st, hs, s);
+    if (resid_sq) *resid_sq = h[0];
+    if (a_sq) *a_sq = h[1];
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+// X = A^-1 B from the packed square factors (luprrp.py:204-214)
+int prrp_lu_solve(const double* LU, int64_t ldlu, int64_t n, const int64_t* perm, const double* B, int64_t ldb,
+                  double* X, int64_t ldx, int32_t nrhs, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || nrhs < 1) fail(PRRP_ERR_DIM, "empty system");
+    if (ldb < n || ldx < n) fail(PRRP_ERR_ARG, "leading dimension < n");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    lu_solve_kernel<<<nrhs, LS_T, 0, s>>>(LU, ldlu, n, perm, B, ldb, X, ldx, st);
     CU_TRY(cudaGetLastError());
     DevState hs;
     read_state(st, hs, s);

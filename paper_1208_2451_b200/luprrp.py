@@ -275,6 +275,43 @@ def luprrp_factor_device(buf, b, tau=2.0, n=None, stream=None):
     return DeviceLU(perm=perm, lu=buf[:, :n], panel_width=b, stats=_stats(st, swaps, m, n, b))
 
 
+def _pack_lu_device(l, u):
+    """Packed L\\U (row-major, device) from host l (m x n unit lower) and u (n x n)."""
+    import torch
+    lt = torch.from_numpy(np.ascontiguousarray(l, dtype=np.float64)).cuda()
+    ut = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).cuda()
+    n = ut.shape[0]
+    packed = torch.tril(lt, -1)
+    packed[:n, :] += torch.triu(ut)
+    return packed.contiguous()
+
+
+def luprrp_solve(f, rhs):
+    """Solve A x = rhs from square block factors (luprrp.py:204-214): forward
+    substitution with the unit lower L on P rhs, back substitution with U, on
+    the device (prrp_lu_solve)."""
+    import torch
+    if f.l.shape[0] != f.l.shape[1]:
+        raise DimensionMismatch("solve needs factors of a square matrix")
+    vec = np.asarray(rhs, dtype=np.float64)
+    b2 = vec.reshape(-1, 1) if vec.ndim == 1 else vec
+    if b2.shape[0] != f.l.shape[0]:
+        raise DimensionMismatch("right-hand side row count mismatch")
+    n, nrhs = b2.shape
+    lib = _lib.device_lib()
+    lu = _pack_lu_device(f.l, f.u)
+    perm = torch.from_numpy(np.asarray(f.perm, dtype=np.int64)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(b2.T)).cuda()          # column-major n x nrhs
+    X = torch.empty_like(B)
+    err = _lib.PrrpErr()
+    rc = lib.prrp_lu_solve(ctypes.c_void_p(lu.data_ptr()), lu.shape[1], n, ctypes.c_void_p(perm.data_ptr()),
+                           ctypes.c_void_p(B.data_ptr()), n, ctypes.c_void_p(X.data_ptr()), n, nrhs,
+                           ctypes.byref(err), _lib.stream_handle())
+    _lib.raise_for(rc, err, "luprrp_solve")
+    x = np.asfortranarray(X.cpu().numpy().T)
+    return x[:, 0] if vec.ndim == 1 else x
+
+
 def growth_bound_luprrp_log2(n, b, tau):
     """log2 of the growth envelope (1 + tau b)^ceil(n/b) (luprrp.py:217-221)."""
     if not (n >= b >= 1) or tau <= 0:

@@ -76,6 +76,26 @@ def strong_rrqr(a, b, tau):
                        swap_count=int(sw.value), l_block=lblk)
 
 
+def qr_column_pivoting(a):
+    """QR with column pivoting, exact column norms recomputed each step
+    (pivoted_qr.py:74-87), on the device (prrp_qrcp)."""
+    import torch
+    a = _as_matrix(a)
+    h, p = a.shape
+    lib = _lib.device_lib()
+    dev = _to_device_colmajor(a)
+    R = torch.empty((p, h), dtype=torch.float64, device="cuda")
+    Q = torch.empty((h, h), dtype=torch.float64, device="cuda")
+    perm = torch.empty(p, dtype=torch.int64, device="cuda")
+    err = _lib.PrrpErr()
+    rc = lib.prrp_qrcp(ctypes.c_void_p(dev.data_ptr()), h, h, p, ctypes.c_void_p(R.data_ptr()),
+                       ctypes.c_void_p(Q.data_ptr()), ctypes.c_void_p(perm.data_ptr()), ctypes.byref(err),
+                       _lib.stream_handle())
+    _lib.raise_for(rc, err, "qr_column_pivoting")
+    return QRFactors(q=np.asfortranarray(Q.cpu().numpy().T), r=np.asfortranarray(R.cpu().numpy().T),
+                     perm=perm.cpu().numpy().astype(np.intp))
+
+
 def householder_qr(a):
     """Unpivoted Householder QR with Q assembled explicitly (pivoted_qr.py:64-71)."""
     import torch

@@ -51,6 +51,133 @@ def tree_height(tree, m, b):
     return len(range(first, m, b))
 
 
+def _partition(m, p):
+    """m rows into p contiguous blocks, as equal as possible, first larger
+    (tournament.py:64-73)."""
+    base, extra = divmod(m, p)
+    out, start = [], 0
+    for i in range(p):
+        size = base + (1 if i < extra else 0)
+        out.append((start, start + size))
+        start += size
+    return out
+
+
+def leaf_blocks(tree, m, b):
+    """Leaf row ranges for a panel of m rows; (blocks, effective P)
+    (tournament.py:76-88)."""
+    if tree.shape == "binary":
+        p_eff = max(1, min(tree.leaf_count, m // (b + 1)))
+        return _partition(m, p_eff), p_eff
+    first = min(m, 2 * b)
+    blocks, start = [(0, first)], first
+    while start < m:
+        stop = min(m, start + b)
+        blocks.append((start, stop))
+        start = stop
+    return blocks, len(blocks)
+
+
+@dataclass
+class TournamentNode:
+    level: int
+    index: int
+    members: np.ndarray      # panel-relative row indices entering the node
+    selected: np.ndarray     # the b survivors, in selection order
+    swap_count: int
+
+
+@dataclass
+class TournamentTrace:
+    nodes: list
+    pivot_rows: np.ndarray
+    leaf_count: int
+    requested_leaf_count: int | None
+    single_node: bool
+    srr: object = None       # SrrqrResult when single_node with the srrqr selector
+
+
+def _select(panel, idx, b, tau, selector):
+    """Up to b candidate rows among panel[idx] -> (selected, full_order,
+    swap_count, srr_or_none) (tournament.py:118-152).  Every node is a device
+    strong RRQR (prrp_strong_rrqr); a numerically rank-deficient node passes
+    on only its independent rows."""
+    from .errors import RankDeficient
+    from .pivoted_qr import strong_rrqr
+    if idx.shape[0] <= b:
+        return idx, idx, 0, None
+    sub = panel[idx, :]
+    if selector == "srrqr":
+        want = b
+        while want:
+            try:
+                srr = strong_rrqr(sub.T, want, tau)
+            except RankDeficient as exc:
+                want = exc.index
+                continue
+            order = srr.qr.perm
+            return idx[order[:want]], idx[order], srr.swap_count, (srr if want == b else None)
+        return idx[:0], idx, 0, None
+    if selector == "gepp":
+        raise NotImplementedError("the GEPP tournament selector (calu_factor) is SURVEY 8(f) rank 2, not built yet")
+    raise ValueError(f"unknown selector {selector!r}")
+
+
+def tournament_select(panel, b, tau, tree, selector="srrqr"):
+    """Reduce an m x b panel to b pivot rows; returns (perm, trace)
+    (tournament.py:155-217).  Same tree walk, node numbering, odd-node
+    promotion and rank-deficiency handling as the reference; each node's
+    selection runs on the device."""
+    from .errors import RankDeficient
+    panel = as_matrix(panel)
+    m = panel.shape[0]
+    if panel.shape[1] != b:
+        raise DimensionMismatch(f"panel has {panel.shape[1]} columns, expected {b}")
+    blocks, p_eff = leaf_blocks(tree, m, b)
+    nodes = []
+    if len(blocks) == 1:
+        idx = np.arange(m, dtype=np.intp)
+        selected, order, swaps, srr = _select(panel, idx, b, tau, selector)
+        if selected.shape[0] < b:
+            raise RankDeficient(f"panel supplied only {selected.shape[0]} independent rows",
+                                index=selected.shape[0])
+        nodes.append(TournamentNode(0, 0, idx, selected, swaps))
+        return np.asarray(order, dtype=np.intp), TournamentTrace(nodes, selected, p_eff, tree.leaf_count, True, srr)
+
+    def run_node(level, index, idx):
+        try:
+            selected, _, swaps, _ = _select(panel, idx, b, tau, selector)
+        except ArithmeticError as exc:
+            exc.tree_node = (level, index)
+            raise
+        nodes.append(TournamentNode(level, index, idx, selected, swaps))
+        return selected
+
+    if tree.shape == "binary":
+        cands = [run_node(0, i, np.arange(lo, hi, dtype=np.intp)) for i, (lo, hi) in enumerate(blocks)]
+        level = 1
+        while len(cands) > 1:
+            merged = []
+            for i in range(0, len(cands) - 1, 2):
+                merged.append(run_node(level, i // 2, np.concatenate([cands[i], cands[i + 1]])))
+            if len(cands) % 2:
+                merged.append(cands[-1])
+            cands = merged
+            level += 1
+        pivots = cands[0]
+    else:
+        lo, hi = blocks[0]
+        cand = run_node(0, 0, np.arange(lo, hi, dtype=np.intp))
+        for i, (lo, hi) in enumerate(blocks[1:], start=1):
+            cand = run_node(i, 0, np.concatenate([cand, np.arange(lo, hi, dtype=np.intp)]))
+        pivots = cand
+    if pivots.shape[0] < b:
+        raise RankDeficient(f"tournament supplied only {pivots.shape[0]} independent rows", index=pivots.shape[0])
+    rest = np.setdiff1d(np.arange(m, dtype=np.intp), pivots)
+    perm = np.concatenate([pivots, rest]).astype(np.intp)
+    return perm, TournamentTrace(nodes, pivots, p_eff, tree.leaf_count, False, None)
+
+
 def growth_bound_caluprrp_log2(n, b, tau, h):
     if not (n >= b >= 1) or h < 0:
         raise ValueError("need n >= b >= 1 and h >= 0")

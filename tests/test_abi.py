@@ -99,3 +99,16 @@ def test_product_package_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", src).replace('"""', ""), f
+
+
+def test_reference_api_surface():
+    """The package exports the reference entry points of SURVEY 8(b) and 8(f)
+    (same names as prrp/__init__.py)."""
+    import paper_1208_2451_b200 as p
+    for name in ("luprrp_factor", "luprrp_solve", "caluprrp_factor", "strong_rrqr", "qr_column_pivoting",
+                 "householder_qr", "multiplier_block", "tournament_select", "TournamentTrace", "BlockLUFactors",
+                 "ElimStats", "QRFactors", "SrrqrResult", "ReductionTree", "binary_tree", "flat_tree",
+                 "tree_height", "growth_bound_luprrp", "growth_bound_caluprrp", "growth_condition",
+                 "gepp_factor", "rel_factorization_error", "RankDeficient", "NonConvergence", "SingularMatrix",
+                 "SingularFactor", "DimensionMismatch"):
+        assert hasattr(p, name), name

@@ -278,3 +278,53 @@ def test_device_matcore_and_gepp_api(dev):
     assert g.intermediate_max == r.intermediate_max
     rr = np.triu(rng.standard_normal((16, 60))) + 4 * np.eye(16, 60)
     assert np.array_equal(dev.multiplier_block(rr, 16), orc.l_from_r(rr, 16))
+
+
+# ---------------------------------------------------------------- API surface of 8(b) and 8(f)
+def test_qr_column_pivoting(dev):
+    """Device QRCP (prrp_qrcp) against the oracle restatement of pivoted_qr.py:74-87."""
+    rng = np.random.Generator(np.random.PCG64(21))
+    for h, p in ((8, 40), (32, 300), (64, 700)):
+        a = np.asfortranarray(rng.standard_normal((h, p)))
+        q = dev.qr_column_pivoting(a)
+        ref = orc.qr_pivoted(a)
+        assert np.array_equal(q.perm, ref.perm)
+        assert _rel(q.r, ref.r) <= TOL_F and _rel(q.q, ref.q) <= TOL_F
+        assert np.linalg.norm(q.q @ q.r - a[:, q.perm]) <= 1e-12 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("shape,m,b,leaf", [("binary", 600, 16, 8), ("binary", 257, 32, 4),
+                                           ("flat", 300, 16, None), ("binary", 40, 16, 8)])
+def test_tournament_select(dev, shape, m, b, leaf):
+    """tournament_select (tournament.py:155-217) node for node against the oracle."""
+    rng = np.random.Generator(np.random.PCG64(m + b))
+    panel = np.asfortranarray(rng.standard_normal((m, b)))
+    tree = dev.binary_tree(leaf) if shape == "binary" else dev.flat_tree()
+    perm, trace = dev.tournament_select(panel, b, 2.0, tree, "srrqr")
+    rperm, rtrace = orc.tournament(panel, b, 2.0, shape, leaf if leaf else 8)
+    assert np.array_equal(perm, rperm)
+    assert trace.single_node == rtrace.single_node and trace.leaf_count == rtrace.leaf_count
+    assert [(n.level, n.index, n.swap_count) for n in trace.nodes] == \
+        [(n.level, n.index, n.swap_count) for n in rtrace.nodes]
+    for n, r in zip(trace.nodes, rtrace.nodes):
+        assert np.array_equal(n.members, r.members) and np.array_equal(n.selected, r.selected)
+
+
+def test_luprrp_solve_and_residual(dev):
+    """luprrp_solve (luprrp.py:204-214) and rel_factorization_error
+    (metrics.py:56-63) on the device against numpy / the oracle."""
+    a = orc.randn_matrix(300, 5)
+    f = dev.luprrp_factor(a, 32, 2.0)
+    rng = np.random.Generator(np.random.PCG64(6))
+    x_true = rng.standard_normal(300)
+    rhs = a @ x_true
+    x = dev.luprrp_solve(f, rhs)
+    assert x.shape == (300,)
+    assert np.linalg.norm(x - x_true) <= 1e-10 * np.linalg.norm(x_true)
+    X = dev.luprrp_solve(f, np.stack([rhs, 2 * rhs], axis=1))
+    assert X.shape == (300, 2) and np.allclose(X[:, 1], 2 * x, rtol=1e-12, atol=1e-12)
+    e = dev.rel_factorization_error(a, f.perm, f.l, f.u)
+    e_ref = orc.rel_residual(a, f.perm, f.l, f.u)
+    assert 0 < e <= 4 * e_ref + 1e-15 and e_ref <= 4 * e + 1e-15
+    with pytest.raises(dev.DimensionMismatch):
+        dev.luprrp_solve(f, np.ones(7))
