@@ -392,8 +392,12 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.prof = tl_prof;
   tbegin(PRRP_K_PANEL, s);
   const int maxc = caps().max_cluster;
+  // CTAs: enough for the columns (one per thread in registers, a second in
+  // shared memory above 4096), at least ceil(p / cpc) -- PRRP_P1_COLS
+  // (default 256) columns per CTA before the cluster grows
+  static const int64_t cpc = getenv("PRRP_P1_COLS") ? atoll(getenv("PRRP_P1_COLS")) : 256;
   const int64_t c1 = std::max<int64_t>((p + P1_MAXCOLS - 1) / P1_MAXCOLS,
-                                       std::min<int64_t>(maxc, std::max<int64_t>(1, (p + 31) / 32)));
+                                       std::min<int64_t>(maxc, std::max<int64_t>(1, (p + cpc - 1) / cpc)));
   const bool aligned = ((uintptr_t)src % 16 == 0) && (ld % 2 == 0);
   if (h == P1_H && c1 <= maxc && aligned && !force_generic_panel()) {
     // thread-per-column register engine (h = 64)
