@@ -430,6 +430,14 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
       return;
     }
+    if (bsel <= 64) {
+      const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + TV_COLS - 1) / TV_COLS);
+      trsm_v_kernel<<<nbv, TV_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
+      tend(s);
+      CU_TRY(cudaGetLastError());
+      launch_finalize(a, B, bsel, p, h, tau, nbv, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
+      return;
+    }
     switch ((bsel + 31) / 32) {
       case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
       case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;

@@ -102,6 +102,83 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
   if (threadIdx.x == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
 }
 
+// trsm, four columns per warp (8 lanes per column; lane j of a group holds
+// rows j, j+8, ..., j+56 in registers).  Per step i (descending): the owner
+// lane's value is broadcast within the group, every lane divides it
+// (div_fast = true division), and each lane updates its rows l < i with the
+// reference's product-then-subtract (matcore.py:78-94).  ~10 instructions per
+// column-step instead of ~80 for a warp per column.  Requires bsel <= 64.
+#define TV_WARPS 8
+#define TV_T (TV_WARPS * 32)
+#define TV_COLS (TV_WARPS * 4)
+__global__ void __launch_bounds__(TV_T) trsm_v_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
+                                                      double* L21, int64_t ldl, double* cand, long long* cand_flat,
+                                                      DevState* st, int panel, const double* fro, int tl, int ti) {
+  __shared__ double r11[64 * 65 / 2];
+  __shared__ double rcp[64], dg[64];
+  __shared__ double red_d[33];
+  __shared__ long long red_l[33];
+  if (prrp_failed(st)) return;
+  load_r11(Rbuf, p, bsel, r11);
+  __syncthreads();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < bsel; i += blockDim.x) {
+    dg[i] = r11[upk(i, i)];
+    rcp[i] = __drcp_rn(dg[i]);
+  }
+  if (blockIdx.x == 0 && t == 0) r11_checks(r11, bsel, *fro, st, panel, true, tl, ti);
+  __syncthreads();
+  const int64_t ncol = p - bsel;
+  const int g = lane >> 3, j = lane & 7;
+  const unsigned gmask = 0xffu << (8 * g);
+  double worst = -1.0;
+  long long wflat = LLONG_MAX;
+  for (int64_t cb = ((int64_t)blockIdx.x * TV_WARPS + warp) * 4; cb < ncol; cb += (int64_t)gridDim.x * TV_COLS) {
+    const int64_t c = cb + g;
+    const bool on = c < ncol;
+    double x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int row = j + 8 * q;
+      x[q] = (on && row < bsel) ? Rbuf[(int64_t)row * p + bsel + c] : 0.0;
+    }
+#pragma unroll 1
+    for (int i = bsel - 1; i >= 0; --i) {
+      // x[i >> 3] by a select tree (a dynamic index would put x in local memory)
+      const int qi = i >> 3;
+      const bool b0 = qi & 1, b1 = qi & 2, b2 = qi & 4;
+      const double s01 = b0 ? x[1] : x[0], s23 = b0 ? x[3] : x[2];
+      const double s45 = b0 ? x[5] : x[4], s67 = b0 ? x[7] : x[6];
+      const double s03 = b1 ? s23 : s01, s47 = b1 ? s67 : s45;
+      const double xo = b2 ? s47 : s03;
+      double xi = __shfl_sync(0xffffffffu, xo, (lane & ~7) | (i & 7));
+      xi = div_fast(xi, dg[i], rcp[i]);
+      const double* u = r11 + i * (i + 1) / 2;   // column i of R11, rows 0..i-1
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int row = j + 8 * q;
+        if (row < i) x[q] = sub_rn(x[q], mul_rn(u[row], xi));
+        else if (row == i) x[q] = xi;
+      }
+    }
+    (void)gmask;
+    if (on) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int row = j + 8 * q;
+        if (row < bsel) {
+          L21[(int64_t)row * ldl + c] = x[q];
+          const double ax = fabs(x[q]);
+          const long long fl = (long long)row * ncol + c;
+          if (ax > worst || (ax == worst && fl < wflat)) { worst = ax; wflat = fl; }
+        }
+      }
+    }
+  }
+  reduce_worst(worst, wflat, red_d, red_l);
+  if (t == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
+}
+
 // out[r][j] = sum_{k >= j} L21[r][gperm[k]] * L11[k][j]
 template <int NR>
 __global__ void __launch_bounds__(TW_WARPS * 32) compose_w_kernel(const double* __restrict__ L21, int64_t ldl,
