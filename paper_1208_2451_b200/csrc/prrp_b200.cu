@@ -108,6 +108,7 @@ DeviceCaps& caps() {
                            (const void*)calu_apply_refl_kernel<3>, (const void*)calu_apply_refl_kernel<4>})
       set_max_dyn((const void*)fn);
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurPSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
@@ -151,11 +152,11 @@ EncodeFn encode_fn() {
 }
 
 // 2-D FP64 map: `inner` contiguous elements, `outer` lines `pitch` elements apart; box {8, KC}
-CUtensorMap make_map(const double* base, uint64_t inner, uint64_t outer, uint64_t pitch) {
+CUtensorMap make_map(const double* base, uint64_t inner, uint64_t outer, uint64_t pitch, uint32_t box_k = SCH_KC) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {pitch * 8};
-  cuuint32_t box[2] = {8, SCH_KC};
+  cuuint32_t box[2] = {8, box_k};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -481,14 +482,25 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
   }
 }
 
+// max_ctas > 0 selects the persistent kernel with at most that many CTAs
+// (K <= 64); 0 the classic one-tile-per-CTA kernel, whose short CTAs let a
+// concurrent high-priority stream claim SMs quickly
 void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* Bm, int64_t ldb, int64_t M,
-                  int64_t N, int K, DevState* st, cudaStream_t s) {
+                  int64_t N, int K, DevState* st, cudaStream_t s, int max_ctas = 0) {
   if (M <= 0 || N <= 0) return;
   tl_schur_flops += 2.0 * (double)M * (double)N * (double)K;
   tbegin(PRRP_K_SCHUR, s);
   const bool tma_ok = ((uintptr_t)L % 16 == 0) && ((uintptr_t)Bm % 16 == 0) && (ldl % 2 == 0) && (ldb % 2 == 0) &&
                       K <= 4 * SCH_KC && M < (1ll << 31) && N < (1ll << 31);
-  if (tma_ok) {
+  if (tma_ok && max_ctas > 0 && K <= SP_K) {
+    const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl, SP_K);
+    const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, SP_K);
+    const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
+    const int64_t tiles = ((M + SCH_BM - 1) / SCH_BM) * ((N + SCH_BN - 1) / SCH_BN);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, max_ctas);
+    schur_persist_kernel<<<grid, SCH_THREADS, sizeof(SchurPSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok,
+                                                                        st);
+  } else if (tma_ok) {
     const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl);
     const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb);
     const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
@@ -779,7 +791,7 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
       // narrow update: the next panel's b columns, on the critical path
       if (wn > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, L, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
-                     bj, st, sm);
+                     bj, st, sm, sms);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
       // fin stream: L-part row moves + row order, GEPP of the pivot block,
@@ -811,13 +823,19 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
       permute_cols(cw0, n, col0, Bk.moved, Bk.moved_cnt, nullptr, sd);
       tend(sd);
       const int64_t w1 = std::min<int64_t>(n - cw0, b);
+      // persistent trailing update on all but 24 SMs: the high-priority stream
+      // keeps room for the panel cluster (16 SMs of one GPC) and its kernels
+      // (PRRP_SCHUR_WIDE_CTAS overrides; 0 = one tile per CTA)
+      static const int wide_ctas = getenv("PRRP_SCHUR_WIDE_CTAS") ? atoi(getenv("PRRP_SCHUR_WIDE_CTAS"))
+                                                                  : std::max(1, sms - 24);
       if (w1 > 0)
-        schur_update(A + (col0 + bj) * lda + cw0, lda, L, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd);
+        schur_update(A + (col0 + bj) * lda + cw0, lda, L, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd,
+                     wide_ctas);
       w1_prev = ss.ev(evi++);
       CU_TRY(cudaEventRecord(w1_prev, sd));
       if (n - cw0 > w1)
         schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, L, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
-                     n - cw0 - w1, bj, st, sd);
+                     n - cw0 - w1, bj, st, sd, wide_ctas);
       CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
     } else {
       // last block (rows == bj): all its updates and row moves came through main
@@ -1424,7 +1442,7 @@ int prrp_lu_residual(const double* A, int64_t lda, const double* LU, int64_t ldl
       build_lk_kernel<<<sms * 4, 256, 0, s>>>(LU, ldlu, m, k0, kb, Kp, Lk, ldlk);
       build_uk_kernel<<<sms * 4, 256, 0, s>>>(LU, ldlu, n, k0, kb, Kp, Uk, lduk);
       CU_TRY(cudaGetLastError());
-      schur_update(C + k0 * ldc + k0, ldc, Lk, ldlk, Uk, lduk, m - k0, n - k0, Kp, st, s);
+      schur_update(C + k0 * ldc + k0, ldc, Lk, ldlk, Uk, lduk, m - k0, n - k0, Kp, st, s, caps().sms);
     }
     sumsq_kernel<<<sms * 4, 256, 0, s>>>(C, ldc, m, n, sums);
     sumsq_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, sums + 1);
@@ -1508,7 +1526,7 @@ int prrp_schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, cons
     caps();
     Arena ar(s);
     DevState* st = new_state(ar, s);
-    schur_update(C, ldc, L, ldl, B, ldb, M, N, K, st, s);
+    schur_update(C, ldc, L, ldl, B, ldb, M, N, K, st, s, caps().sms);
     DevState hs;
     read_state(st, hs, s);
     if (absmax) *absmax = bits_to_double(hs.inter_max);

@@ -161,6 +161,120 @@ schur_dmma_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constan
   if (t == 0) atomic_max_abs(&st->inter_max, mx);
 }
 
+// Persistent variant for K <= 64 (the b = 64 trailing updates): one CTA per SM
+// walks the 128 x 64 tiles; the whole K of a tile is one TMA stage, the next
+// tile's stage is in flight while the current one multiplies, and each
+// thread's 32 C elements are loaded into registers before the MMA loop so the
+// epilogue never waits on HBM.  Same fragments, same k order, same epilogue
+// rounding as schur_dmma_kernel (bit-identical results).
+#define SP_K 64
+struct SchurPSmem {
+  double a[2][SCH_BM * SP_K];
+  double b[2][SCH_BN * SP_K];
+  unsigned long long full[2];
+  double red[40];
+};
+
+__global__ void __launch_bounds__(SCH_THREADS, 1)
+schur_persist_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
+                     double* C, int64_t ldc, int M, int N, int K, int vec_ok, DevState* st) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  SchurPSmem& S = *reinterpret_cast<SchurPSmem*>(sbuf);
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ntN = (N + SCH_BN - 1) / SCH_BN, ntM = (M + SCH_BM - 1) / SCH_BM;
+  const int ntiles = ntM * ntN;
+  constexpr uint32_t kTileBytes = (SCH_BM + SCH_BN) * SP_K * 8;
+  if (t == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapL) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapB) : "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int tile, int s) {
+    const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+    mbar_expect_tx(&S.full[s], kTileBytes);
+    for (int g = 0; g < SCH_BM / 8; ++g) tma_load_2d(&S.a[s][g * SP_K * 8], &mapL, &S.full[s], m0 + 8 * g, 0);
+    for (int g = 0; g < SCH_BN / 8; ++g) tma_load_2d(&S.b[s][g * SP_K * 8], &mapB, &S.full[s], n0 + 8 * g, 0);
+  };
+  const int first = blockIdx.x;
+  if (t == 0 && first < ntiles) issue(first, 0);
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int fr = lane & 3, fc = lane >> 2;
+  double mx = 0.0;
+  int it = 0;
+  for (int tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+    if (t == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
+    // this tile's C into registers (in flight during the MMA loop)
+    double cv[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + fc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c0 = n0 + wn + j * 8 + 2 * fr;
+        const double* cp = C + (int64_t)r * ldc + c0;
+        if (r < M && vec_ok && c0 + 1 < N) {
+          const double2 v = *reinterpret_cast<const double2*>(cp);
+          cv[i][j][0] = v.x;
+          cv[i][j][1] = v.y;
+        } else {
+          cv[i][j][0] = (r < M && c0 < N) ? cp[0] : 0.0;
+          cv[i][j][1] = (r < M && c0 + 1 < N) ? cp[1] : 0.0;
+        }
+      }
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    mbar_wait(&S.full[s], (it >> 1) & 1);
+    const double* sa = S.a[s];
+    const double* sb = S.b[s];
+    const int kmax = (K + 3) & ~3;
+#pragma unroll 4
+    for (int k4 = 0; k4 < kmax; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SP_K + k4 + fr) * 8 + fc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SP_K + k4 + fr) * 8 + fc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    // epilogue: C -= acc, max|C|
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + fc;
+      if (r >= M) continue;
+      double* crow = C + (int64_t)r * ldc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c0 = n0 + wn + j * 8 + 2 * fr;
+        const double v0 = sub_rn(cv[i][j][0], acc[i][j][0]);
+        const double v1 = sub_rn(cv[i][j][1], acc[i][j][1]);
+        if (vec_ok && c0 + 1 < N) {
+          *reinterpret_cast<double2*>(crow + c0) = make_double2(v0, v1);
+          mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+        } else {
+          if (c0 < N) { crow[c0] = v0; mx = fmax(mx, fabs(v0)); }
+          if (c0 + 1 < N) { crow[c0 + 1] = v1; mx = fmax(mx, fabs(v1)); }
+        }
+      }
+    }
+    __syncthreads();   // stage s is refilled by the issue at the top of tile it+1... (it+2)
+  }
+  mx = block_max(mx, S.red);
+  if (t == 0) atomic_max_abs(&st->inter_max, mx);
+}
+
 // Generic-shape fallback with the identical rounding recipe (odd K or
 // unaligned operands): one thread per C element, fma chain from zero.
 __global__ void __launch_bounds__(256) schur_simt_kernel(const double* L, int64_t ldl, const double* B, int64_t ldb,
