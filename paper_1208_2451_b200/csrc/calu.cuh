@@ -252,3 +252,11 @@ __global__ void calu_tail_gather_kernel(const double* A, int64_t lda, int64_t n,
     if (c == 0) ptmp[r] = porig[pos2row[n + r]];
   }
 }
+
+// leaf_lo[i] = first logical row of leaf i (contiguous blocks, first `extra`
+// blocks one row larger: tournament.py:64-73) -- written on the device so the
+// panel loop never waits for a pageable host copy
+__global__ void calu_leaf_lo_kernel(int64_t* leaf_lo, int64_t p_eff, int64_t base, int64_t extra) {
+  const int64_t i = threadIdx.x;
+  for (int64_t j = i; j < p_eff; j += blockDim.x) leaf_lo[j] = j * base + min(j, extra);
+}

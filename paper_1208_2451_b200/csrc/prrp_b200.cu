@@ -932,6 +932,10 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
   if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
   caps();
+  // PRRP_TRACE: record the timing spans (and write the trace file) for CALU too
+  Timer timer;
+  tl_timer = getenv("PRRP_TRACE") ? &timer : nullptr;
+  struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
   const int npanels = (int)((n + b - 1) / b);
   const int maxnodes = 2 * P;
   Arena ar(s);
@@ -1051,7 +1055,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
             start += cnt[i];
           }
         }
-        CU_TRY(cudaMemcpyAsync(leaf_lo_dev, lo.data(), sizeof(int64_t) * p_eff, cudaMemcpyHostToDevice, s));
+        calu_leaf_lo_kernel<<<1, 64, 0, s>>>(leaf_lo_dev, p_eff, rows / p_eff, rows % p_eff);
         int64_t chg3 = 0;
         int slot = 0;
         run_level(lo, cnt, true, col0, bj, panel, 0, slot);
@@ -1088,11 +1092,15 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         }
         charges[panel] = chg3;
         // new logical order [pivots, rest ascending]; move the pivot rows to slots col0..
+        tbegin(PRRP_K_OTHER, s);
         calu_reorder_kernel<<<1, 1024, 0, s>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
                                                st);
+        tend(s);
       }
+      tbegin(PRRP_K_PERMUTE, s);
       permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
           A, lda, col0, n, B.moved, perm, st, panel);
+      tend(s);
       CU_TRY(cudaGetLastError());
       if (p_eff > 1) {
         // unpivoted QR of the permuted panel transpose -> multiplier_block (tournament.py:271-272)
@@ -1115,6 +1123,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         qa.ovpad = gq.ovpad;
         qa.st = st;
         qa.panel_id = panel;
+        tbegin(PRRP_K_FINALIZE, s);
         iota32_kernel<<<1, 128, 0, s>>>(perm_small, bj);
         launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, s, qa);
         calu_copy_r11_kernel<<<1, 256, 0, s>>>(Rsmall, bj, B.Rbuf, rows);
@@ -1127,6 +1136,8 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
           default: calu_apply_refl_kernel<4><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
         }
         CU_TRY(cudaGetLastError());
+        tend(s);
+        tbegin(PRRP_K_TRSM, s);
         const int64_t ncol = rows - bj;
         const int nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
         const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
@@ -1142,15 +1153,20 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         }
         calu_stats_kernel<<<1, 256, 0, s>>>(B.cand, nblk, node_swaps + (size_t)panel * maxnodes, maxnodes,
                                             swaps_dev, panel, st);
+        tend(s);
         CU_TRY(cudaGetLastError());
       }
       // L21 (logical order) -> physical slots for the Schur update and the compose
       calu_scatter_l21_kernel<<<sms * 4, 256, 0, s>>>(Llog, ldl, log2phys, rows - bj, bj, bj, Lphys, ldl);
       if (width > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lphys, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
-                     width, bj, st, s);
+                     width, bj, st, s, sms);
+      tbegin(PRRP_K_GEPP, s);
       launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
+      tend(s);
+      tbegin(PRRP_K_COMPOSE, s);
       launch_compose_w(Lphys, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
+      tend(s);
     } else {
       // last square block: bring the rows into logical order, then GEPP
       calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, ident, 1, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
@@ -1160,7 +1176,9 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
       launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
     }
     CU_TRY(cudaGetLastError());
+    tbegin(PRRP_K_BLOCKROW, s);
     launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+    tend(s);
     CU_TRY(cudaGetLastError());
   }
   if (m > n) {
@@ -1190,6 +1208,13 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   if (stats) {
     stats->total_swaps = 0;
     for (int v : sw) stats->total_swaps += v;
+  }
+  if (tl_timer) {
+    prrp_timing tm;
+    timer.collect(&tm);
+    fprintf(stderr, "[prrp calu timing] total %.3f ms:", tm.total_ms);
+    for (int c = 0; c < PRRP_K_COUNT; ++c) fprintf(stderr, " %d:%.3f", c, tm.ms[c]);
+    fprintf(stderr, "\n");
   }
   return state_to_err(hs, err);
 }
