@@ -52,9 +52,11 @@ __global__ void calu_select_kernel(const int32_t* const* perms, const int32_t* l
 __global__ void __launch_bounds__(1024) calu_reorder_kernel(const int32_t* pivots, const int32_t* perm_full,
                                                             int order_mode, int b, int64_t rows, int64_t col0,
                                                             int64_t* pos2row, int64_t* scratch /* 3*rows */,
-                                                            int32_t* moved, int32_t* log2phys, DevState* st) {
+                                                            int32_t* moved, int32_t* moved_cnt, int32_t* log2phys,
+                                                            DevState* st) {
   __shared__ int s_cnt[33];
-  __shared__ int s_nv;
+  __shared__ int64_t pv_slot[PRRP_MAXH], vsl[PRRP_MAXH];
+  __shared__ int dsl[PRRP_MAXH], s_np, s_nd;
   if (prrp_failed(st)) return;
   const int t = threadIdx.x, T = blockDim.x;
   int64_t* oldp = scratch;                 // old pos2row (relative slots)
@@ -70,44 +72,56 @@ __global__ void __launch_bounds__(1024) calu_reorder_kernel(const int32_t* pivot
   for (int q = t; q < b; q += T) {
     const int32_t lp = order_mode == 0 ? pivots[q] : perm_full[q];
     flag[lp] = q + 1;
+    pv_slot[q] = oldp[lp];
     slot_pivot[oldp[lp]] = 1;
   }
   __syncthreads();
-  // displaced rows: slots < b not holding a pivot; vacated slots: pivot slots >= b.
-  // pair them in increasing slot order (deterministic)
+  // displaced rows: slots < b not holding a pivot (increasing); vacated slots:
+  // pivot rows' slots >= b (increasing); paired in that order (deterministic).
+  // Ranks by counting (b <= 128 threads, O(b) each).
+  if (t < b) {
+    const int64_t sv = pv_slot[t];
+    if (sv >= b) {
+      int rk = 0;
+      for (int q = 0; q < b; ++q) rk += pv_slot[q] >= b && pv_slot[q] < sv;
+      vsl[rk] = sv;
+    }
+    if (!slot_pivot[t]) {
+      int rk = 0;
+      for (int q = 0; q < t; ++q) rk += !slot_pivot[q];
+      dsl[rk] = t;
+    }
+  }
+  // pivot moves (slot q <- src) in q order: compaction by counting
+  if (t < b) {
+    const bool mv = pv_slot[t] != t;
+    if (mv) {
+      int rk = 0;
+      for (int q = 0; q < t; ++q) rk += pv_slot[q] != q;
+      moved[2 * rk] = t;
+      moved[2 * rk + 1] = (int32_t)pv_slot[t];
+    }
+  }
   if (t == 0) {
-    int nd = 0, nv = 0;
-    int64_t dsl[PRRP_MAXH], vsl[PRRP_MAXH];
-    for (int s = 0; s < b; ++s)
-      if (!slot_pivot[s]) dsl[nd++] = s;
-    // vacated slots in increasing order: scan pivot rows' slots >= b
-    // (at most b of them; simple selection in slot order)
-    int64_t last = -1;
-    for (int q = 0; q < nd; ++q) {
-      int64_t best = INT64_MAX;
-      for (int r = 0; r < b; ++r) {
-        const int32_t lp = order_mode == 0 ? pivots[r] : perm_full[r];
-        const int64_t s = oldp[lp];
-        if (s >= b && s > last && s < best) best = s;
-      }
-      vsl[nv++] = best;
-      last = best;
+    int np = 0, nd = 0;
+    for (int q = 0; q < b; ++q) np += pv_slot[q] != q;
+    for (int q = 0; q < b; ++q) nd += !slot_pivot[q];     // = number of vacated slots
+    s_np = np;
+    s_nd = nd;
+  }
+  __syncthreads();
+  {
+    const int nd = s_nd;
+    if (t < nd) {
+      moved[2 * (s_np + t)] = (int32_t)vsl[t];
+      moved[2 * (s_np + t) + 1] = dsl[t];
+      // the row that was in slot dsl[t] now lives in vsl[t]
+      slot_pivot[dsl[t]] = -(vsl[t] + 2);
     }
-    int cnt = 0;
-    for (int q = 0; q < b; ++q) {
-      const int32_t lp = order_mode == 0 ? pivots[q] : perm_full[q];
-      const int64_t src = oldp[lp];
-      if (src != q) { moved[2 * cnt] = q; moved[2 * cnt + 1] = (int32_t)src; ++cnt; }
+    if (t == 0) {
+      st->moved = s_np + nd;
+      if (moved_cnt) *moved_cnt = s_np + nd;
     }
-    for (int i = 0; i < nd; ++i) {
-      moved[2 * cnt] = (int32_t)vsl[i];
-      moved[2 * cnt + 1] = (int32_t)dsl[i];
-      ++cnt;
-      // remember the displacement: the row that was in slot dsl[i] now lives in vsl[i]
-      slot_pivot[dsl[i]] = -(vsl[i] + 2);   // encoded new slot
-    }
-    st->moved = cnt;
-    s_nv = nv;
   }
   __syncthreads();
   // new logical order

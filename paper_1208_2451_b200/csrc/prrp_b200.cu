@@ -1003,11 +1003,11 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   std::vector<std::vector<std::pair<int64_t, int>>> node_members(npanels);   // (members, node slot)
 
   auto run_level = [&](const std::vector<int64_t>& lo, const std::vector<int64_t>& cnt, bool leaves,
-                       int64_t col0, int bj, int panel, int level, int slot0) {
+                       int64_t col0, int bj, int panel, int level, int slot0, cudaStream_t qs) {
     // fork
     cudaEvent_t fk;
     CU_TRY(cudaEventCreateWithFlags(&fk, cudaEventDisableTiming));
-    CU_TRY(cudaEventRecord(fk, s));
+    CU_TRY(cudaEventRecord(fk, qs));
     const int nn = (int)lo.size();
     for (int i = 0; i < nn; ++i) {
       cudaStream_t ns = node_stream(i);
@@ -1023,26 +1023,78 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
       cudaEvent_t jn;
       CU_TRY(cudaEventCreateWithFlags(&jn, cudaEventDisableTiming));
       CU_TRY(cudaEventRecord(jn, node_stream(i)));
-      CU_TRY(cudaStreamWaitEvent(s, jn, 0));
+      CU_TRY(cudaStreamWaitEvent(qs, jn, 0));
       CU_TRY(cudaEventDestroy(jn));
     }
     CU_TRY(cudaEventDestroy(fk));
   };
 
+  // ---- look-ahead over three streams, as in LU_PRRP (see luprrp_impl):
+  //   main: [side(k-2), fin(k-2)] tournament(k) (nodes on the pool) -> reorder
+  //         -> [W1(k-1)] row moves of [col0, col0+2b) -> final QR of the pivot
+  //         block + logged reflectors on the other rows -> L21 -> narrow Schur
+  //   fin:  [row moves(k)] row moves of [0, col0) + row order -> GEPP -> compose
+  //   side: [narrow(k)] row moves of [col0+2b, n) -> W1(k) -> W2(k) -> [fin(k)]
+  //         blockrow(k)
+  // Moved rows are physical slots >= col0 and blockrow(k-1) writes slots < col0.
+  Streams& ss = streams();
+  cudaStream_t sm = ss.main, sd = ss.side, sf = ss.fin;
+  {
+    cudaEvent_t e0 = ss.ev(0);
+    CU_TRY(cudaEventRecord(e0, s));
+    CU_TRY(cudaStreamWaitEvent(sm, e0, 0));
+    CU_TRY(cudaStreamWaitEvent(sd, e0, 0));
+    CU_TRY(cudaStreamWaitEvent(sf, e0, 0));
+  }
+  int32_t* movedb[2] = {B.moved, ar.get<int32_t>(2 * m)};
+  int32_t* mcntb = ar.get<int32_t>(2);
+  double* Llogb[2] = {Llog, ar.get<double>((size_t)b * ldl)};
+  double* Lphysb[2] = {Lphys, ar.get<double>((size_t)b * ldl)};
+  double* Db[2] = {D, ar.get<double>((size_t)b * b)};
+  int32_t* pivb[2] = {piv, ar.get<int32_t>(b)};
+  int32_t* gpermb[2] = {gperm, ar.get<int32_t>(b)};
+  std::vector<cudaEvent_t> side_ev(npanels, nullptr), fin_ev(npanels, nullptr);
+  cudaEvent_t w1_prev = nullptr, side_done = nullptr;
+  int evi = 1;
+  auto permute_cols = [&](int64_t c_lo, int64_t c_hi, int64_t row0, const int32_t* mv, const int32_t* mc,
+                          int64_t* pp, int pnl, cudaStream_t q) {
+    if (c_hi <= c_lo && !pp) return;
+    const int64_t nc = std::max<int64_t>(c_hi - c_lo, 1);
+    const unsigned grid = (unsigned)std::min<int64_t>((nc + 31) / 32, 2 * sms);
+    permute_cols_kernel<<<grid, 256, 0, q>>>(A, lda, row0, c_lo, std::max(c_lo, c_hi), mv, mc, pp, st, pnl);
+    CU_TRY(cudaGetLastError());
+  };
   int panel = 0;
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
     const int64_t rows = m - col0;
     const int64_t width = n - col0 - bj;
+    const int par = panel & 1;
     double* blk = A + col0 * lda + col0;
+    double* Lg = Llogb[par];
+    double* Lp = Lphysb[par];
+    double* Dk = Db[par];
+    int32_t* pivk = pivb[par];
+    int32_t* gpk = gpermb[par];
+    int32_t* mv = movedb[par];
+    int32_t* mc = mcntb + par;
+    PanelBuffers Bk = B;
+    Bk.moved = mv;
+    Bk.moved_cnt = mc;
     if (rows > bj) {
+      if (panel >= 2) {
+        CU_TRY(cudaStreamWaitEvent(sm, side_ev[panel - 2], 0));
+        CU_TRY(cudaStreamWaitEvent(sm, fin_ev[panel - 2], 0));
+      }
       const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
       if (p_eff == 1) {
         // single node: the selector's own full order and l_block (tournament.py:168-177)
-        strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Llog, ldl, B, st, swaps_dev, nullptr, nullptr,
-                          nullptr, false, s, pos2row + col0);
-        calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, B.perm, 1, bj, rows, col0, pos2row, scratch, B.moved,
-                                               log2phys, st);
+        strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Lg, ldl, Bk, st, swaps_dev, nullptr, nullptr,
+                          nullptr, false, sm, pos2row + col0);
+        tbegin(PRRP_K_OTHER, sm);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(nullptr, Bk.perm, 1, bj, rows, col0, pos2row, scratch, mv, mc,
+                                                log2phys, st);
+        tend(sm);
       } else {
         // leaves: contiguous logical blocks, first blocks larger (tournament.py:64-88)
         std::vector<int64_t> lo(p_eff), cnt(p_eff);
@@ -1055,10 +1107,10 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
             start += cnt[i];
           }
         }
-        calu_leaf_lo_kernel<<<1, 64, 0, s>>>(leaf_lo_dev, p_eff, rows / p_eff, rows % p_eff);
+        calu_leaf_lo_kernel<<<1, 64, 0, sm>>>(leaf_lo_dev, p_eff, rows / p_eff, rows % p_eff);
         int64_t chg3 = 0;
         int slot = 0;
-        run_level(lo, cnt, true, col0, bj, panel, 0, slot);
+        run_level(lo, cnt, true, col0, bj, panel, 0, slot, sm);
         for (int64_t i = 0; i < p_eff; ++i) {
           chg3 += qr_charge3(cnt[i], bj);
           node_members[panel].push_back({cnt[i], slot + (int)i});
@@ -1066,42 +1118,44 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         slot += (int)p_eff;
         int32_t* cur = cands;
         int32_t* nxt = cands + (size_t)maxnodes * b;
-        calu_select_kernel<<<(unsigned)p_eff, 128, 0, s>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
+        calu_select_kernel<<<(unsigned)p_eff, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
         int64_t ncur = p_eff;
         int level = 1;
         while (ncur > 1) {
           const int64_t nmerge = ncur / 2;
           // node i of this level reads lpos_all/rowidx_all[i*2b .. i*2b + 2b) (stride 2b even when bj < b)
-          calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, s>>>(cur, bj, (int)(2 * nmerge), lpos_all, rowidx_all,
-                                                                     pos2row, col0, 2 * b);
+          calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(cur, bj, (int)(2 * nmerge), lpos_all,
+                                                                      rowidx_all, pos2row, col0, 2 * b);
           CU_TRY(cudaGetLastError());
           std::vector<int64_t> mlo(nmerge, 0), mcnt(nmerge, 2 * bj);
-          run_level(mlo, mcnt, false, col0, bj, panel, level, slot);
+          run_level(mlo, mcnt, false, col0, bj, panel, level, slot, sm);
           for (int64_t i = 0; i < nmerge; ++i) {
             chg3 += qr_charge3(2 * bj, bj);
             node_members[panel].push_back({2 * bj, slot + (int)i});
           }
           slot += (int)nmerge;
-          calu_select_kernel<<<(unsigned)nmerge, 128, 0, s>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
+          calu_select_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
           if (ncur % 2)   // odd node promoted unmerged (tournament.py:197-198)
             CU_TRY(cudaMemcpyAsync(nxt + nmerge * bj, cur + (ncur - 1) * bj, sizeof(int32_t) * bj,
-                                   cudaMemcpyDeviceToDevice, s));
+                                   cudaMemcpyDeviceToDevice, sm));
           ncur = nmerge + (ncur % 2);
           std::swap(cur, nxt);
           ++level;
         }
         charges[panel] = chg3;
         // new logical order [pivots, rest ascending]; move the pivot rows to slots col0..
-        tbegin(PRRP_K_OTHER, s);
-        calu_reorder_kernel<<<1, 1024, 0, s>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
-                                               st);
-        tend(s);
+        tbegin(PRRP_K_OTHER, sm);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
+                                                st);
+        tend(sm);
       }
-      tbegin(PRRP_K_PERMUTE, s);
-      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
-          A, lda, col0, n, B.moved, perm, st, panel);
-      tend(s);
-      CU_TRY(cudaGetLastError());
+      if (w1_prev) CU_TRY(cudaStreamWaitEvent(sm, w1_prev, 0));
+      const int64_t wn = std::min<int64_t>(width, b);
+      tbegin(PRRP_K_PERMUTE, sm);
+      permute_cols(col0, col0 + bj + wn, col0, mv, mc, nullptr, panel, sm);
+      tend(sm);
+      cudaEvent_t ev_perm = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_perm, sm));
       if (p_eff > 1) {
         // unpivoted QR of the permuted panel transpose -> multiplier_block (tournament.py:271-272)
         PanelArgs qa{};
@@ -1123,63 +1177,119 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         qa.ovpad = gq.ovpad;
         qa.st = st;
         qa.panel_id = panel;
-        tbegin(PRRP_K_FINALIZE, s);
-        iota32_kernel<<<1, 128, 0, s>>>(perm_small, bj);
-        launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, s, qa);
-        calu_copy_r11_kernel<<<1, 256, 0, s>>>(Rsmall, bj, B.Rbuf, rows);
+        tbegin(PRRP_K_FINALIZE, sm);
+        iota32_kernel<<<1, 128, 0, sm>>>(perm_small, bj);
+        if (bj == P1_H && ((uintptr_t)blk % 16 == 0) && (lda % 2 == 0) && !force_generic_panel()) {
+          // the register engine in fixed-order mode, one CTA (p = b columns)
+          PanelCfg g1 = gq;
+          g1.C = 1;
+          g1.T = P1_T;
+          PanelArgs a1 = qa;
+          a1.per = bj;
+          a1.ovf = B.ovf;
+          a1.fro = nodes[0].B.fro;
+          launch_cluster(panel_qrcp1_kernel, g1, 0, sm, a1);
+        } else {
+          launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
+        }
+        calu_copy_r11_kernel<<<1, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
         const size_t dyn = (size_t)bj * (bj + 1) * 8;
         const unsigned grid = (unsigned)std::min<int64_t>(sms * 4, (rows - bj + 7) / 8);
         switch ((bj + 31) / 32) {
-          case 1: calu_apply_refl_kernel<1><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
-          case 2: calu_apply_refl_kernel<2><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
-          case 3: calu_apply_refl_kernel<3><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
-          default: calu_apply_refl_kernel<4><<<grid, 256, dyn, s>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          case 1: calu_apply_refl_kernel<1><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          case 2: calu_apply_refl_kernel<2><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          case 3: calu_apply_refl_kernel<3><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+          default: calu_apply_refl_kernel<4><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
         }
         CU_TRY(cudaGetLastError());
-        tend(s);
-        tbegin(PRRP_K_TRSM, s);
+        tend(sm);
+        tbegin(PRRP_K_TRSM, sm);
         const int64_t ncol = rows - bj;
-        const int nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
-        const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
-        const double* one = nullptr;
-        (void)one;
         double* fro_inf = nodes[0].B.fro;   // rank check of the final QR: the reference has none (fro = 0)
-        CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), s));
-        switch ((bj + 31) / 32) {
-          case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
-          case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
-          case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
-          default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, s>>>(B.Rbuf, rows, bj, Llog, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+        CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), sm));
+        int nblk;
+        if (bj <= 64) {
+          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TV_COLS - 1) / TV_COLS);
+          trsm_v_kernel<<<nblk, TV_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
+        } else {
+          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
+          const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
+          switch ((bj + 31) / 32) {
+            case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+            default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+          }
         }
-        calu_stats_kernel<<<1, 256, 0, s>>>(B.cand, nblk, node_swaps + (size_t)panel * maxnodes, maxnodes,
-                                            swaps_dev, panel, st);
-        tend(s);
+        calu_stats_kernel<<<1, 256, 0, sm>>>(B.cand, nblk, node_swaps + (size_t)panel * maxnodes, maxnodes,
+                                             swaps_dev, panel, st);
+        tend(sm);
         CU_TRY(cudaGetLastError());
       }
       // L21 (logical order) -> physical slots for the Schur update and the compose
-      calu_scatter_l21_kernel<<<sms * 4, 256, 0, s>>>(Llog, ldl, log2phys, rows - bj, bj, bj, Lphys, ldl);
-      if (width > 0)
-        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lphys, ldl, A + col0 * lda + col0 + bj, lda, rows - bj,
-                     width, bj, st, s, sms);
-      tbegin(PRRP_K_GEPP, s);
-      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
-      tend(s);
-      tbegin(PRRP_K_COMPOSE, s);
-      launch_compose_w(Lphys, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, s);
-      tend(s);
+      calu_scatter_l21_kernel<<<sms * 4, 256, 0, sm>>>(Lg, ldl, log2phys, rows - bj, bj, bj, Lp, ldl);
+      if (wn > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lp, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
+                     bj, st, sm, sms);
+      cudaEvent_t ev_narrow = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_narrow, sm));
+      // fin: L-part row moves + row order, GEPP, compose
+      CU_TRY(cudaStreamWaitEvent(sf, ev_narrow, 0));
+      tbegin(PRRP_K_PERMUTE, sf);
+      permute_cols(0, col0, col0, mv, mc, perm, panel, sf);
+      tend(sf);
+      tbegin(PRRP_K_GEPP, sf);
+      launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sf);
+      tend(sf);
+      tbegin(PRRP_K_COMPOSE, sf);
+      launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf);
+      tend(sf);
+      fin_ev[panel] = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(fin_ev[panel], sf));
+      // side: trailing row moves, trailing update (next narrow region first)
+      CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
+      const int64_t cw0 = col0 + bj + wn;
+      tbegin(PRRP_K_PERMUTE, sd);
+      permute_cols(cw0, n, col0, mv, mc, nullptr, panel, sd);
+      tend(sd);
+      // the tournament needs many SMs at once: one-tile CTAs for the trailing update
+      static const int wide_ctas = getenv("PRRP_SCHUR_WIDE_CTAS") ? atoi(getenv("PRRP_SCHUR_WIDE_CTAS")) : 0;
+      const int64_t w1 = std::min<int64_t>(n - cw0, b);
+      if (w1 > 0)
+        schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd,
+                     wide_ctas);
+      w1_prev = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(w1_prev, sd));
+      if (n - cw0 > w1)
+        schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
+                     n - cw0 - w1, bj, st, sd, wide_ctas);
+      CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
     } else {
-      // last square block: bring the rows into logical order, then GEPP
-      calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, ident, 1, bj, rows, col0, pos2row, scratch, B.moved, log2phys,
-                                             st);
-      permute_kernel<<<(unsigned)((n + PERM_CW - 1) / PERM_CW), 256, PERM_MAXROWS * PERM_CW * 8, s>>>(
-          A, lda, col0, n, B.moved, perm, st, panel);
-      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
+      // last square block: logical order (all columns, on the side stream, which
+      // has seen every earlier update and row move), then GEPP
+      tbegin(PRRP_K_OTHER, sd);
+      calu_reorder_kernel<<<1, 1024, 0, sd>>>(nullptr, ident, 1, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
+                                              st);
+      tend(sd);
+      tbegin(PRRP_K_PERMUTE, sd);
+      permute_cols(0, n, col0, mv, mc, perm, panel, sd);
+      tend(sd);
+      tbegin(PRRP_K_GEPP, sd);
+      launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sd);
+      tend(sd);
     }
     CU_TRY(cudaGetLastError());
-    tbegin(PRRP_K_BLOCKROW, s);
-    launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
-    tend(s);
+    tbegin(PRRP_K_BLOCKROW, sd);
+    launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sd);
+    tend(sd);
     CU_TRY(cudaGetLastError());
+    side_done = ss.ev(evi++);
+    CU_TRY(cudaEventRecord(side_done, sd));
+    side_ev[panel] = side_done;
+  }
+  CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
+  {
+    cudaEvent_t e1 = ss.ev(evi++);
+    CU_TRY(cudaEventRecord(e1, sm));
+    CU_TRY(cudaStreamWaitEvent(s, e1, 0));
   }
   if (m > n) {
     // unfinished tail rows n..m-1 into logical order
