@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
     const int L = 7 - KB;
     const P1Smem xsm{xs0 + (uint32_t)(8 * KB) * (P1_T * 8)};
     const uint32_t bar = buf ? bar1 : bar0;
-    if (t == 0) p1_bar_expect(bar, (uint32_t)(C * (int)sizeof(P1Rec)));
+    if (t == 0 && C > 1) p1_bar_expect(bar, (uint32_t)(C * (int)sizeof(P1Rec)));
     P1_MARK(3)
     P1_TL(0)
     P1_TLW(0)
@@ -538,37 +538,49 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
     P1_TLW(3)
     P1_MARK(0)
     P1_TL(1)
-    // ---- CTA argmax; warp 0 pushes the CTA candidate into every CTA
-    if (warp == 0) {
+    // ---- CTA argmax; warp 0 pushes the CTA candidate into every CTA.  A
+    // one-CTA cluster skips the exchange: every warp takes the CTA winner.
+    const P1Rec* Wp;
+    int rc;
+    if (C == 1) {
       const bool ok = lane < P1_NW && S.wrec[buf][lane].jl >= 0;
       const unsigned long long u = ok ? p1_ukey(S.wrec[buf][lane].key, true) : 0ull;
-      const unsigned pos = ok ? (unsigned)S.wrec[buf][lane].pos : 0xffffffffu;
-      int w = p1_best_lane(u, pos);
-      if (w < 0) w = 0;   // no live column in this CTA: push warp 0's empty record
-      if (lane < C) {
-        const P1Rec& b = S.wrec[buf][w];
-        const uint32_t rbar = p1_mapa(bar, lane);
-        const uint32_t dst = p1_mapa((uint32_t)__cvta_generic_to_shared(&S.rec[buf][c]), lane);
-        p1_push16(dst, b.key, __longlong_as_double(b.pos), rbar);
-        p1_push16(dst + 16, __longlong_as_double((long long)(unsigned)b.jl | ((long long)b.skip << 32)),
-                  b.alpha, rbar);
-        p1_push16(dst + 32, b.beta, S.fro, rbar);
+      int w = p1_best_lane(u, ok ? (unsigned)S.wrec[buf][lane].pos : 0xffffffffu);
+      if (w < 0) w = 0;
+      Wp = &S.wrec[buf][w];
+      rc = 0;
+      if (k == 0 && mode == 0 && warp == 0 && lane == 0) *a.fro = sqrt(S.fro);
+    } else {
+      if (warp == 0) {
+        const bool ok = lane < P1_NW && S.wrec[buf][lane].jl >= 0;
+        const unsigned long long u = ok ? p1_ukey(S.wrec[buf][lane].key, true) : 0ull;
+        const unsigned pos = ok ? (unsigned)S.wrec[buf][lane].pos : 0xffffffffu;
+        int w = p1_best_lane(u, pos);
+        if (w < 0) w = 0;   // no live column in this CTA: push warp 0's empty record
+        if (lane < C) {
+          const P1Rec& b = S.wrec[buf][w];
+          const uint32_t rbar = p1_mapa(bar, lane);
+          const uint32_t dst = p1_mapa((uint32_t)__cvta_generic_to_shared(&S.rec[buf][c]), lane);
+          p1_push16(dst, b.key, __longlong_as_double(b.pos), rbar);
+          p1_push16(dst + 16, __longlong_as_double((long long)(unsigned)b.jl | ((long long)b.skip << 32)),
+                    b.alpha, rbar);
+          p1_push16(dst + 32, b.beta, S.fro, rbar);
+        }
       }
+      P1_TL(2)
+      p1_bar_wait(bar, (uint32_t)((k >> 1) & 1));
+      P1_MARK(1)
+      P1_TL(3)
+      // ---- the cluster winner (every warp redundantly); its v pulled once per CTA
+      {
+        const bool ok = lane < C && S.rec[buf][lane].jl >= 0;
+        const unsigned long long u = ok ? p1_ukey(S.rec[buf][lane].key, true) : 0ull;
+        rc = p1_best_lane(u, ok ? (unsigned)S.rec[buf][lane].pos : 0xffffffffu);
+        if (rc < 0) rc = 0;
+      }
+      Wp = &S.rec[buf][rc];
     }
-    P1_TL(2)
-    p1_bar_wait(bar, (uint32_t)((k >> 1) & 1));
-    P1_MARK(1)
-    P1_TL(3)
-
-    // ---- the cluster winner (every warp redundantly); its v pulled once per CTA
-    int rc;
-    {
-      const bool ok = lane < C && S.rec[buf][lane].jl >= 0;
-      const unsigned long long u = ok ? p1_ukey(S.rec[buf][lane].key, true) : 0ull;
-      rc = p1_best_lane(u, ok ? (unsigned)S.rec[buf][lane].pos : 0xffffffffu);
-      if (rc < 0) rc = 0;
-    }
-    const P1Rec& W = S.rec[buf][rc];
+    const P1Rec& W = *Wp;
     const long long wpos = W.pos;
     const int skip = W.skip;
     const double beta = W.beta, alpha = W.alpha;
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
       __syncthreads();
     }
     P1_TL(4)
-    if (k == 0 && mode == 0 && c == 0 && warp == 0) {
+    if (C > 1 && k == 0 && mode == 0 && c == 0 && warp == 0) {
       double f = lane < C ? S.rec[buf][lane].fro : 0.0;
       for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
       if (lane == 0) *a.fro = sqrt(f);
