@@ -64,6 +64,33 @@ __device__ int r11_checks(const double* r11, int bsel, double fro, DevState* st,
   return 0;
 }
 
+// r11_checks by one warp (ballots over the diagonal; same codes and indices):
+// the first k with |r_kk| < eps*fro, else the last i with r_ii == 0.
+template <typename Diag>
+__device__ int r11_checks_warp(Diag diag, int bsel, double fro, DevState* st, int panel, bool report, int tl = -1,
+                               int ti = -1) {
+  const int lane = threadIdx.x & 31;
+  const double thr = PRRP_EPS * fro;
+  int first_rank = -1, last_zero = -1;
+  for (int k0 = 0; k0 < bsel; k0 += 32) {
+    const int k = k0 + lane;
+    const double d = k < bsel ? diag(k) : 1.0;
+    const unsigned br = __ballot_sync(0xffffffffu, k < bsel && fabs(d) < thr);
+    const unsigned bz = __ballot_sync(0xffffffffu, k < bsel && d == 0.0);
+    if (br && first_rank < 0) first_rank = k0 + __ffs(br) - 1;
+    if (bz) last_zero = k0 + 31 - __clz(bz);
+  }
+  if (first_rank >= 0) {
+    if (report && lane == 0) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, first_rank, -1, 0.0, tl, ti);
+    return 1;
+  }
+  if (last_zero >= 0) {
+    if (report && lane == 0) prrp_set_error(st, PRRP_ERR_SINGULAR_FACTOR, panel, last_zero, -1, 0.0, tl, ti);
+    return 1;
+  }
+  return 0;
+}
+
 // Solve R11 x = R12[:, pos] for the positions [q0, q0 + blockDim.x) and write
 // L21 (column-major, row pos - bsel).  Tracks the worst |x| with its
 // row-major flat index in lt = R11^-1 R12 (bsel x (p - bsel)).

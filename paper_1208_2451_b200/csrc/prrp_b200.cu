@@ -432,8 +432,8 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       return;
     }
     if (bsel <= 64) {
-      const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + TV_COLS - 1) / TV_COLS);
-      trsm_v_kernel<<<nbv, TV_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
+      const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
+      trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nbv, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
@@ -1209,8 +1209,8 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), sm));
         int nblk;
         if (bj <= 64) {
-          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TV_COLS - 1) / TV_COLS);
-          trsm_v_kernel<<<nblk, TV_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
+          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
+          trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
         } else {
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
           const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;

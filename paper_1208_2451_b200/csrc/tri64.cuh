@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
   for (int i = threadIdx.x; i < bsel; i += blockDim.x) rcp[i] = __drcp_rn(r11[upk(i, i)]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, *fro, st, panel, true, tl, ti);
+  if (blockIdx.x == 0 && threadIdx.x < 32)
+    r11_checks_warp([&](int k) { return r11[upk(k, k)]; }, bsel, *fro, st, panel, true, tl, ti);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t ncol = p - bsel;
   double worst = -1.0;
@@ -102,66 +103,143 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
   if (threadIdx.x == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
 }
 
-// trsm, four columns per warp (8 lanes per column; lane j of a group holds
-// rows j, j+8, ..., j+56 in registers).  Per step i (descending): the owner
-// lane's value is broadcast within the group, every lane divides it
-// (div_fast = true division), and each lane updates its rows l < i with the
-// reference's product-then-subtract (matcore.py:78-94).  ~10 instructions per
-// column-step instead of ~80 for a warp per column.  Requires bsel <= 64.
-#define TV_WARPS 8
-#define TV_T (TV_WARPS * 32)
-#define TV_COLS (TV_WARPS * 4)
-__global__ void __launch_bounds__(TV_T) trsm_v_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
+// trsm in 8-row chunks, four columns per warp (8 lanes per column, lane j
+// holds rows j + 8q in registers).  Chunk k (rows 8k..8k+7, descending) is one register
+// x[k] per lane: its 8x8 triangle is solved with a shuffle per step, which
+// leaves the 8 solved values in registers of every lane of the group; rows of
+// the chunks q < k then take their 8 product-then-subtract updates in step
+// order with one 16-byte shared load per two multipliers.  Per element the
+// operation sequence is exactly matcore.trsm_upper's (matcore.py:78-94):
+// x_l -= u_li x_i for i = b-1 .. l+1, then x_l /= u_ll.  The divisions use the
+// reciprocal form and are range-checked once per column group; a group that
+// saw an out-of-range quotient is redone with IEEE divisions.
+// R11 is padded to 8-row chunks with an identity tail (x = 0 rows): the padded
+// updates are x_l - 0*0, which leave every x_l (including -0 and NaN) unchanged.
+#define TC_WARPS 8
+#define TC_T (TC_WARPS * 32)
+#define TC_COLS (TC_WARPS * 4)
+#define TC_UP 66   // padded R11 row pitch: 8 consecutive rows hit 8 distinct 16-byte bank groups
+
+#ifndef TC_STAMP
+#define TC_STAMP(k)
+#endif
+
+template <bool EXACT>
+__device__ __forceinline__ bool trsm_c_column(double (&x)[8], const double* __restrict__ us, const double* __restrict__ dg,
+                                              const double* __restrict__ rc, int nk, int lane) {
+  const int j = lane & 7;
+  bool bad = false;
+#pragma unroll 1
+  for (int k = nk - 1; k >= 0; --k) {
+    double v = x[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q == k) v = x[q];
+    const double2* ur = reinterpret_cast<const double2*>(us + (8 * k + j) * TC_UP + 8 * k);
+    const double2* dr = reinterpret_cast<const double2*>(dg + 8 * k);
+    const double2* rr = reinterpret_cast<const double2*>(rc + 8 * k);
+    double ut[8], dk[8], rk[8], xs[8];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double2 a = ur[s], d = dr[s], r = rr[s];
+      ut[2 * s] = a.x; ut[2 * s + 1] = a.y;
+      dk[2 * s] = d.x; dk[2 * s + 1] = d.y;
+      rk[2 * s] = r.x; rk[2 * s + 1] = r.y;
+    }
+#pragma unroll
+    for (int s = 7; s >= 0; --s) {
+      const double a = __shfl_sync(0xffffffffu, v, (lane & ~7) | s);
+      double xi;
+      if (EXACT) {
+        xi = __ddiv_rn(a, dk[s]);
+      } else {
+        const double q0 = __dmul_rn(a, rk[s]);
+        xi = fma(fma(-dk[s], q0, a), rk[s], q0);
+        const double aq = fabs(xi);
+        bad |= !(aq < 1e300 && (aq > 1e-290 || a == 0.0));
+      }
+      xs[s] = xi;
+      if (j < s) v = sub_rn(v, mul_rn(ut[s], xi));
+      else if (j == s) v = xi;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == k) x[q] = v;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      if (q < k) {
+        const double2* uq = reinterpret_cast<const double2*>(us + (8 * q + j) * TC_UP + 8 * k);
+        double u[8];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const double2 a = uq[s];
+          u[2 * s] = a.x; u[2 * s + 1] = a.y;
+        }
+#pragma unroll
+        for (int s = 7; s >= 0; --s) x[q] = sub_rn(x[q], mul_rn(u[s], xs[s]));
+      }
+    }
+  }
+  return bad;
+}
+
+__global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                       double* L21, int64_t ldl, double* cand, long long* cand_flat,
                                                       DevState* st, int panel, const double* fro, int tl, int ti) {
-  __shared__ double r11[64 * 65 / 2];
-  __shared__ double rcp[64], dg[64];
+  __shared__ __align__(16) double us[64 * TC_UP];
+  __shared__ __align__(16) double dg[64], rc[64];
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
   if (prrp_failed(st)) return;
-  load_r11(Rbuf, p, bsel, r11);
-  __syncthreads();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int i = t; i < bsel; i += blockDim.x) {
-    dg[i] = r11[upk(i, i)];
-    rcp[i] = __drcp_rn(dg[i]);
+  const int nk = (bsel + 7) >> 3, bp = nk * 8;
+  TC_STAMP(0);
+  const double frov = (blockIdx.x == 0 && t < 32) ? *fro : 0.0;   // issued before the staging loads
+  // padded R11: upper triangle of the first bsel rows, identity on [bsel, bp)
+  for (int base = t; base < bp * 64; base += 8 * TC_T) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * TC_T, l = e >> 6, i = e & 63;
+      v[u] = (e < bp * 64 && l < bsel && i >= l && i < bsel) ? Rbuf[(int64_t)l * p + i] : (l == i ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * TC_T, l = e >> 6, i = e & 63;
+      if (e < bp * 64) us[l * TC_UP + i] = v[u];
+    }
   }
-  if (blockIdx.x == 0 && t == 0) r11_checks(r11, bsel, *fro, st, panel, true, tl, ti);
   __syncthreads();
+  TC_STAMP(4);
+  for (int i = t; i < bp; i += TC_T) {
+    dg[i] = us[i * TC_UP + i];
+    rc[i] = __drcp_rn(dg[i]);
+  }
+  if (blockIdx.x == 0 && t < 32)
+    r11_checks_warp([&](int k) { return us[k * TC_UP + k]; }, bsel, frov, st, panel, true, tl, ti);
+  TC_STAMP(5);
+  __syncthreads();
+  TC_STAMP(1);
   const int64_t ncol = p - bsel;
   const int g = lane >> 3, j = lane & 7;
-  const unsigned gmask = 0xffu << (8 * g);
   double worst = -1.0;
   long long wflat = LLONG_MAX;
-  for (int64_t cb = ((int64_t)blockIdx.x * TV_WARPS + warp) * 4; cb < ncol; cb += (int64_t)gridDim.x * TV_COLS) {
+  for (int64_t cb = ((int64_t)blockIdx.x * TC_WARPS + warp) * 4; cb < ncol; cb += (int64_t)gridDim.x * TC_COLS) {
     const int64_t c = cb + g;
     const bool on = c < ncol;
     double x[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int row = j + 8 * q;
-      x[q] = (on && row < bsel) ? Rbuf[(int64_t)row * p + bsel + c] : 0.0;
-    }
-#pragma unroll 1
-    for (int i = bsel - 1; i >= 0; --i) {
-      // x[i >> 3] by a select tree (a dynamic index would put x in local memory)
-      const int qi = i >> 3;
-      const bool b0 = qi & 1, b1 = qi & 2, b2 = qi & 4;
-      const double s01 = b0 ? x[1] : x[0], s23 = b0 ? x[3] : x[2];
-      const double s45 = b0 ? x[5] : x[4], s67 = b0 ? x[7] : x[6];
-      const double s03 = b1 ? s23 : s01, s47 = b1 ? s67 : s45;
-      const double xo = b2 ? s47 : s03;
-      double xi = __shfl_sync(0xffffffffu, xo, (lane & ~7) | (i & 7));
-      xi = div_fast(xi, dg[i], rcp[i]);
-      const double* u = r11 + i * (i + 1) / 2;   // column i of R11, rows 0..i-1
+    auto load = [&] {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int row = j + 8 * q;
-        if (row < i) x[q] = sub_rn(x[q], mul_rn(u[row], xi));
-        else if (row == i) x[q] = xi;
+        x[q] = (on && row < bsel) ? Rbuf[(int64_t)row * p + bsel + c] : 0.0;
       }
+    };
+    load();
+    if (__any_sync(0xffffffffu, trsm_c_column<false>(x, us, dg, rc, nk, lane))) {
+      load();
+      trsm_c_column<true>(x, us, dg, rc, nk, lane);
     }
-    (void)gmask;
     if (on) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -175,8 +253,10 @@ __global__ void __launch_bounds__(TV_T) trsm_v_kernel(const double* __restrict__
       }
     }
   }
+  TC_STAMP(2);
   reduce_worst(worst, wflat, red_d, red_l);
   if (t == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
+  TC_STAMP(3);
 }
 
 // out[r][j] = sum_{k >= j} L21[r][gperm[k]] * L11[k][j]

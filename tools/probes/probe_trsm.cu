@@ -2,9 +2,12 @@
 #include <cstdio>
 #include <vector>
 #include <cstring>
+#include <cstdint>
+__device__ unsigned long long g_stamp[8];
+#define TC_STAMP(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long _t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t)); g_stamp[k] = _t; } } while (0)
 #include "../../paper_1208_2451_b200/csrc/tri64.cuh"
-int main() {
-  const int64_t p = 8192;
+int main(int argc, char** argv) {
+  const int64_t p = argc > 1 ? atoll(argv[1]) : 8192;
   const int b = 64;
   std::vector<double> R((size_t)b * p);
   srand(3);
@@ -30,12 +33,14 @@ int main() {
   };
   const size_t dynw = (((size_t)b * (b + 1) / 2 + 1) / 2 * 2 + (size_t)b * TTCP) * 8;
   timeit("trsm_w<2>", [&] { trsm_w_kernel<2><<<(int)std::min<int64_t>(2048, (ncol + TTC - 1) / TTC), TW_WARPS * 32, dynw>>>(Rd, p, b, L1, ldl, cand, cf, st, 0, fro, -1, -1); });
-  timeit("trsm_v", [&] { trsm_v_kernel<<<(int)std::min<int64_t>(2048, (ncol + TV_COLS - 1) / TV_COLS), TV_T, 0>>>(Rd, p, b, L2, ldl, cand, cf, st, 0, fro, -1, -1); });
-  std::vector<double> h1((size_t)b * ldl), h2((size_t)b * ldl);
-  cudaMemcpy(h1.data(), L1, h1.size() * 8, cudaMemcpyDeviceToHost);
-  cudaMemcpy(h2.data(), L2, h2.size() * 8, cudaMemcpyDeviceToHost);
-  size_t diff = 0;
-  for (int i = 0; i < b; ++i) for (int64_t c = 0; c < ncol; ++c) diff += memcmp(&h1[i * ldl + c], &h2[i * ldl + c], 8) != 0;
-  printf("bitwise differences: %zu\n", diff);
+  timeit("trsm_c", [&] { trsm_c_kernel<<<(int)std::min<int64_t>(2048, (ncol + TC_COLS - 1) / TC_COLS), TC_T, 0>>>(Rd, p, b, L2, ldl, cand, cf, st, 0, fro, -1, -1); });
+  { std::vector<double> h1((size_t)b * ldl), h2((size_t)b * ldl);
+    cudaMemcpy(h1.data(), L1, h1.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h2.data(), L2, h2.size() * 8, cudaMemcpyDeviceToHost);
+    size_t diff = 0;
+    for (int i = 0; i < b; ++i) for (int64_t c = 0; c < ncol; ++c) diff += memcmp(&h1[i * ldl + c], &h2[i * ldl + c], 8) != 0;
+    printf("trsm_c bitwise differences: %zu\n", diff); }
+  { unsigned long long h[8]; cudaMemcpyFromSymbol(h, g_stamp, sizeof(h));
+    printf("stamps (ns from start): load %llu check-done %llu stage %llu  loop %llu  reduce %llu\n", h[4]-h[0], h[5]-h[0], h[1]-h[0], h[2]-h[1], h[3]-h[2]); }
   return 0;
 }
