@@ -9,6 +9,9 @@
 //   schur_dmma_kernel      all SMs: A22 -= L21 A12 (TMA + DMMA), growth max
 //   compose_kernel         all SMs: L21 <- L21[:, perm] L11 into the L part
 //   blockrow_kernel        all SMs: GEPP finish of the block row, finish max
+#include <functional>
+#include <chrono>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <cmath>
@@ -22,6 +25,7 @@
 #include "verify.cuh"
 #include "panel64.cuh"
 #include "panel1.cuh"
+#include "panel2.cuh"
 #include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
@@ -69,8 +73,13 @@ int report(prrp_err* err, const Fail& f) {
 }
 
 // ---------------------------------------------------------------- device probe
+// claim-counter slots of the dynamically scheduled Schur kernel; a slot is
+// reused kSchedSlots launches later (long after its launch has finished)
+constexpr unsigned kSchedSlots = 1024;
 struct DeviceCaps {
   bool init = false;
+  int* sched = nullptr;        // kSchedSlots pairs of tile-claim counters (schur_ws_kernel), self-resetting
+  unsigned sched_next = 0;
   int sms = 0;
   int max_cluster = 8;
 };
@@ -90,7 +99,8 @@ DeviceCaps& caps() {
     CU_TRY(cudaGetDevice(&dev));
     CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
-                           (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel}) {
+                           (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel,
+                           (const void*)panel_qrcp2_kernel}) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       set_max_dyn((const void*)fn);
     }
@@ -109,6 +119,7 @@ DeviceCaps& caps() {
       set_max_dyn((const void*)fn);
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurPSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurWSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
@@ -129,6 +140,8 @@ DeviceCaps& caps() {
       }
       cudaGetLastError();
     }
+    CU_TRY(cudaMalloc(&c.sched, kSchedSlots * 2 * sizeof(int)));
+    CU_TRY(cudaMemset(c.sched, 0, kSchedSlots * 2 * sizeof(int)));
     c.init = true;
   }
   return c;
@@ -166,15 +179,24 @@ CUtensorMap make_map(const double* base, uint64_t inner, uint64_t outer, uint64_
 }
 
 // ---------------------------------------------------------------- workspace
+// keep != nullptr: persistent buffers (cudaMalloc, recorded in *keep and
+// owned by a cached graph plan; usable while a stream is being captured)
 struct Arena {
   cudaStream_t s;
   std::vector<void*> ptrs;
-  explicit Arena(cudaStream_t st) : s(st) {}
+  std::vector<void*>* keep;
+  explicit Arena(cudaStream_t st, std::vector<void*>* kp = nullptr) : s(st), keep(kp) {}
   template <typename T>
   T* get(size_t count) {
     void* p = nullptr;
-    CU_TRY(cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), s));
-    ptrs.push_back(p);
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (keep) {
+      CU_TRY(cudaMalloc(&p, bytes));
+      keep->push_back(p);
+    } else {
+      CU_TRY(cudaMallocAsync(&p, bytes, s));
+      ptrs.push_back(p);
+    }
     return static_cast<T*>(p);
   }
   ~Arena() {
@@ -409,6 +431,14 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
     a1.per = (p + c1 - 1) / c1;
     const size_t dyn = a1.per > P1_T ? (size_t)P1_H * P1_T * 8 : 0;
     launch_cluster(panel_qrcp1_kernel, g1, dyn, s, a1);
+  } else if (h == P2_H && p <= (int64_t)P2_T * maxc && aligned && !force_generic_panel()) {
+    // thread-per-column split-column engine (h = 128): register window + shared rows
+    PanelCfg g2 = g;
+    g2.C = (int)std::max<int64_t>((p + P2_T - 1) / P2_T, std::min<int64_t>(maxc, (p + cpc - 1) / cpc));
+    g2.T = P2_T;
+    PanelArgs a2 = a;
+    a2.per = (p + g2.C - 1) / g2.C;
+    launch_cluster(panel_qrcp2_kernel, g2, (size_t)(P2_H - P2_W) * P2_T * 8, s, a2);
   } else {
     launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, a);
   }
@@ -482,17 +512,42 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
   }
 }
 
+// claim counters of a graph plan being captured (its launches own their slots)
+thread_local int* tl_sched = nullptr;
+thread_local unsigned tl_sched_next = 0, tl_sched_slots = 1;
+
+// PRRP_SCHUR_W2_STREAM=1: the bulk trailing update (W2) streams C with evict-first hints
+const bool w2_stream = getenv("PRRP_SCHUR_W2_STREAM") && atoi(getenv("PRRP_SCHUR_W2_STREAM")) != 0;
+
 // max_ctas > 0 selects the persistent kernel with at most that many CTAs
 // (K <= 64); 0 the classic one-tile-per-CTA kernel, whose short CTAs let a
 // concurrent high-priority stream claim SMs quickly
 void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const double* Bm, int64_t ldb, int64_t M,
-                  int64_t N, int K, DevState* st, cudaStream_t s, int max_ctas = 0) {
+                  int64_t N, int K, DevState* st, cudaStream_t s, int max_ctas = 0, int quantum = 0,
+                  bool stream_c = false) {
   if (M <= 0 || N <= 0) return;
   tl_schur_flops += 2.0 * (double)M * (double)N * (double)K;
   tbegin(PRRP_K_SCHUR, s);
   const bool tma_ok = ((uintptr_t)L % 16 == 0) && ((uintptr_t)Bm % 16 == 0) && (ldl % 2 == 0) && (ldb % 2 == 0) &&
                       K <= 4 * SCH_KC && M < (1ll << 31) && N < (1ll << 31);
-  if (tma_ok && max_ctas > 0 && K <= SP_K) {
+  static const int schur_old = getenv("PRRP_SCHUR_OLD") ? atoi(getenv("PRRP_SCHUR_OLD")) : 0;
+  // K <= 64 with a CTA budget: the whole-K-stage persistent kernel (measured
+  // steadier than the warp-specialised one inside the b = 64 LU_PRRP
+  // schedule); K > 64 (b = 128): the warp-specialised kernel (70-74% of the
+  // DMMA peak on the big updates vs 58-63% for the classic kernel)
+  const bool use_ws = !schur_old && (max_ctas > 0 || quantum > 0) && (K > SP_K || quantum > 0);
+  if (tma_ok && use_ws) {
+    const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl, SW_KC);
+    const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, SW_KC);
+    const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
+    const int64_t tiles = ((M + SCH_BM - 1) / SCH_BM) * ((N + SCH_BN - 1) / SCH_BN);
+    const unsigned grid = (unsigned)(quantum > 0 ? (tiles + quantum - 1) / quantum : std::min<int64_t>(tiles, max_ctas));
+    int* ctr = tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
+                        : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);
+    schur_ws_kernel<<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st,
+                                                                 ctr, quantum > 0 ? quantum : INT_MAX,
+                                                                 stream_c ? 1 : 0);
+  } else if (tma_ok && max_ctas > 0 && K <= SP_K) {
     const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl, SP_K);
     const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, SP_K);
     const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
@@ -687,6 +742,7 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
   if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
   caps();
+  const auto host_t0 = std::chrono::steady_clock::now();
   const int npanels = (int)((n + b - 1) / b);
   Arena ar(s);
   DevState* st = new_state(ar, s);
@@ -835,7 +891,7 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
       CU_TRY(cudaEventRecord(w1_prev, sd));
       if (n - cw0 > w1)
         schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, L, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
-                     n - cw0 - w1, bj, st, sd, wide_ctas);
+                     n - cw0 - w1, bj, st, sd, wide_ctas, 0, w2_stream);
       CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
     } else {
       // last block (rows == bj): all its updates and row moves came through main
@@ -865,8 +921,13 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     CU_TRY(cudaEventRecord(e1, sm));
     CU_TRY(cudaStreamWaitEvent(s, e1, 0));
   }
+  const auto host_t1 = std::chrono::steady_clock::now();
   DevState hs;
   read_state(st, hs, s);
+  if (getenv("PRRP_HOSTTIME"))
+    fprintf(stderr, "[prrp lu host] enqueue %.3f ms, then wait %.3f ms\n",
+            std::chrono::duration<double, std::milli>(host_t1 - host_t0).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t1).count());
   if (tl_prof) {
     long long pr[8];
     CU_TRY(cudaMemcpy(pr, tl_prof, sizeof(pr), cudaMemcpyDeviceToHost));
@@ -909,6 +970,11 @@ struct NodeBufs {
   int64_t* rowidx;    // merge nodes: 2b physical rows
 };
 
+struct PtrPack { const int32_t* p[32]; };
+__global__ void store_ptrs_kernel(PtrPack pk, int cnt, const int32_t** out) {
+  if ((int)threadIdx.x < cnt) out[threadIdx.x] = pk.p[threadIdx.x];
+}
+
 thread_local std::vector<cudaStream_t> tl_node_streams;
 cudaStream_t node_stream(int i) {
   while ((int)tl_node_streams.size() <= i) {
@@ -923,22 +989,32 @@ cudaStream_t node_stream(int i) {
 
 int64_t qr_charge3(int64_t r, int64_t b) { return 6 * r * b * b - 2 * b * b * b; }   // 3 * _charge_qr
 
-int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
-                  int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
-  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
-  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
-  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
-  if (P < 1) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1");
-  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
-  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
-  caps();
-  // PRRP_TRACE: record the timing spans (and write the trace file) for CALU too
-  Timer timer;
-  tl_timer = getenv("PRRP_TRACE") ? &timer : nullptr;
-  struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
+// What the host needs after a CALU_PRRP enqueue (device result slots and the
+// tournament bookkeeping for the flop charges); kept by a cached graph plan.
+struct CaluOut {
+  DevState* st = nullptr;
+  int32_t* swaps_dev = nullptr;
+  int32_t* node_swaps = nullptr;
+  std::vector<int64_t> charges;
+  std::vector<std::vector<std::pair<int64_t, int>>> node_members;   // (members, node slot)
+  int npanels = 0, maxnodes = 0, b = 0;
+};
+
+// Enqueue one CALU_PRRP factorization on stream s (capturable: no host
+// synchronisation, no pageable copies); buffers from `ar`.
+void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
+                      cudaStream_t s, Arena& ar, CaluOut& out) {
   const int npanels = (int)((n + b - 1) / b);
   const int maxnodes = 2 * P;
-  Arena ar(s);
+  // Schur launches: the tournament needs whole SMs (16-CTA clusters) at once,
+  // so by default the updates run as short CTAs (classic kernel, quantum 0)
+  // that hand SMs back quickly.  PRRP_CALU_NARROW: CTAs of a persistent
+  // narrow update (0 = classic); PRRP_CALU_WIDE_Q: tiles per CTA of the
+  // warp-specialised trailing update (0 = classic)
+  static const int calu_narrow_ctas = getenv("PRRP_CALU_NARROW") ? atoi(getenv("PRRP_CALU_NARROW")) : 0;
+  static const int calu_wide_q = getenv("PRRP_CALU_WIDE_Q") ? atoi(getenv("PRRP_CALU_WIDE_Q")) : 0;
+  static const int calu_wide_ctas = getenv("PRRP_CALU_WIDE_CTAS") ? atoi(getenv("PRRP_CALU_WIDE_CTAS"))
+                                                                  : std::max(1, caps().sms - 24);
   DevState* st = new_state(ar, s);
   const int64_t ldl = ((m + 7) / 8) * 8;
   double* Lphys = ar.get<double>((size_t)b * ldl);
@@ -988,10 +1064,11 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   int32_t* gperm = ar.get<int32_t>(b);
   int32_t* swaps_dev = ar.get<int32_t>(npanels);
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
-  {
-    std::vector<const int32_t*> hp(maxnodes);
-    for (int i = 0; i < maxnodes; ++i) hp[i] = nodes[i].B.perm;
-    CU_TRY(cudaMemcpyAsync(perms_dev, hp.data(), sizeof(void*) * maxnodes, cudaMemcpyHostToDevice, s));
+  for (int i0 = 0; i0 < maxnodes; i0 += 32) {   // node perm pointers (by value: capturable)
+    PtrPack pk{};
+    const int cnt = std::min(32, maxnodes - i0);
+    for (int i = 0; i < cnt; ++i) pk.p[i] = nodes[i0 + i].B.perm;
+    store_ptrs_kernel<<<1, 32, 0, s>>>(pk, cnt, perms_dev + i0);
   }
   const int sms = caps().sms;
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
@@ -1064,6 +1141,26 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     permute_cols_kernel<<<grid, 256, 0, q>>>(A, lda, row0, c_lo, std::max(c_lo, c_hi), mv, mc, pp, st, pnl);
     CU_TRY(cudaGetLastError());
   };
+  // The tournament's multi-CTA leaf clusters need whole SMs of one GPC at
+  // once, which a running trailing update never hands back; so the bulk of
+  // panel k's trailing update (W2) and its block row are enqueued only after
+  // panel k+1's leaves (side waits for them), and run as a persistent kernel
+  // on all but 24 SMs, beside the rest of the tournament chain
+  // (PRRP_CALU_DEFER=0: enqueue at once).
+  static const int calu_defer = getenv("PRRP_CALU_DEFER") ? atoi(getenv("PRRP_CALU_DEFER")) : 1;
+  std::function<void()> pending_side;
+  auto flush_side = [&](cudaEvent_t after) {
+    if (!pending_side) return;
+    if (after) CU_TRY(cudaStreamWaitEvent(sd, after, 0));
+    pending_side();
+    pending_side = nullptr;
+  };
+  auto flush_after_main = [&]() {
+    if (!pending_side) return;
+    cudaEvent_t e = ss.ev(evi++);
+    CU_TRY(cudaEventRecord(e, sm));
+    flush_side(e);
+  };
   int panel = 0;
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
@@ -1091,6 +1188,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         // single node: the selector's own full order and l_block (tournament.py:168-177)
         strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Lg, ldl, Bk, st, swaps_dev, nullptr, nullptr,
                           nullptr, false, sm, pos2row + col0);
+        flush_after_main();
         tbegin(PRRP_K_OTHER, sm);
         calu_reorder_kernel<<<1, 1024, 0, sm>>>(nullptr, Bk.perm, 1, bj, rows, col0, pos2row, scratch, mv, mc,
                                                 log2phys, st);
@@ -1111,6 +1209,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
         int64_t chg3 = 0;
         int slot = 0;
         run_level(lo, cnt, true, col0, bj, panel, 0, slot, sm);
+        flush_after_main();
         for (int64_t i = 0; i < p_eff; ++i) {
           chg3 += qr_charge3(cnt[i], bj);
           node_members[panel].push_back({cnt[i], slot + (int)i});
@@ -1189,6 +1288,15 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
           a1.ovf = B.ovf;
           a1.fro = nodes[0].B.fro;
           launch_cluster(panel_qrcp1_kernel, g1, 0, sm, a1);
+        } else if (bj == P2_H && ((uintptr_t)blk % 16 == 0) && (lda % 2 == 0) && !force_generic_panel()) {
+          PanelCfg g2 = gq;
+          g2.C = 1;
+          g2.T = P2_T;
+          PanelArgs a2 = qa;
+          a2.per = bj;
+          a2.ovf = B.ovf;
+          a2.fro = nodes[0].B.fro;
+          launch_cluster(panel_qrcp2_kernel, g2, (size_t)(P2_H - P2_W) * P2_T * 8, sm, a2);
         } else {
           launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
         }
@@ -1228,7 +1336,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
       calu_scatter_l21_kernel<<<sms * 4, 256, 0, sm>>>(Lg, ldl, log2phys, rows - bj, bj, bj, Lp, ldl);
       if (wn > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lp, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
-                     bj, st, sm, sms);
+                     bj, st, sm, calu_narrow_ctas, calu_wide_q);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
       // fin: L-part row moves + row order, GEPP, compose
@@ -1250,19 +1358,31 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
       tbegin(PRRP_K_PERMUTE, sd);
       permute_cols(cw0, n, col0, mv, mc, nullptr, panel, sd);
       tend(sd);
-      // the tournament needs many SMs at once: one-tile CTAs for the trailing update
-      static const int wide_ctas = getenv("PRRP_SCHUR_WIDE_CTAS") ? atoi(getenv("PRRP_SCHUR_WIDE_CTAS")) : 0;
       const int64_t w1 = std::min<int64_t>(n - cw0, b);
       if (w1 > 0)
         schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd,
-                     wide_ctas);
+                     calu_wide_ctas, calu_wide_q);
       w1_prev = ss.ev(evi++);
       CU_TRY(cudaEventRecord(w1_prev, sd));
-      if (n - cw0 > w1)
-        schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
-                     n - cw0 - w1, bj, st, sd, wide_ctas);
-      CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
+      // the rest of the trailing update (W2) and the block row: deferred until
+      // the next panel's tournament leaves have run (see pending_side)
+      pending_side = [=, &ss, &evi, &side_done, &side_ev, &fin_ev]() {
+        if (n - cw0 > w1)
+          schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
+                       n - cw0 - w1, bj, st, sd, calu_wide_ctas, calu_wide_q, w2_stream);
+        CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
+        tbegin(PRRP_K_BLOCKROW, sd);
+        launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sd);
+        tend(sd);
+        CU_TRY(cudaGetLastError());
+        side_done = ss.ev(evi++);
+        CU_TRY(cudaEventRecord(side_done, sd));
+        side_ev[panel] = side_done;
+      };
+      if (!calu_defer) flush_side(nullptr);
+      continue;
     } else {
+      flush_side(nullptr);
       // last square block: logical order (all columns, on the side stream, which
       // has seen every earlier update and row move), then GEPP
       tbegin(PRRP_K_OTHER, sd);
@@ -1285,6 +1405,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     CU_TRY(cudaEventRecord(side_done, sd));
     side_ev[panel] = side_done;
   }
+  flush_side(nullptr);
   CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
   {
     cudaEvent_t e1 = ss.ev(evi++);
@@ -1299,8 +1420,129 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     CU_TRY(cudaMemcpy2DAsync(A + n * lda, lda * 8, tmp, n * 8, n * 8, m - n, cudaMemcpyDeviceToDevice, s));
     CU_TRY(cudaMemcpyAsync(perm + n, ptmp, sizeof(int64_t) * (m - n), cudaMemcpyDeviceToDevice, s));
   }
+  out.st = st;
+  out.swaps_dev = swaps_dev;
+  out.node_swaps = node_swaps;
+  out.charges = std::move(charges);
+  out.node_members = std::move(node_members);
+  out.npanels = npanels;
+  out.maxnodes = maxnodes;
+  out.b = b;
+}
+
+// A captured CALU_PRRP factorization for one (matrix, shape, parameters) key:
+// replayed by one graph launch (the host enqueue of the ~10^4 launches of a
+// large factorization costs more than the GPU work at n = 16384).
+struct CaluPlan {
+  double* A; int64_t lda, m, n; int b; double tau; int P; int64_t* perm; int dev;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> bufs;
+  CaluOut out;
+  uint64_t used = 0;
+  ~CaluPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+std::vector<std::unique_ptr<CaluPlan>>& calu_plans() {
+  static std::vector<std::unique_ptr<CaluPlan>> v;
+  return v;
+}
+constexpr size_t kMaxPlans = 4;
+uint64_t g_plan_clock = 0;
+
+int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,
+                    prrp_err* err, std::chrono::steady_clock::time_point host_t0, Timer* timer);
+
+int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
+                  int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+  if (P < 1) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1");
+  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  caps();
+  const auto host_t0 = std::chrono::steady_clock::now();
+  // PRRP_TRACE: record the timing spans (and write the trace file) for CALU too
+  if (getenv("PRRP_TRACE") || (getenv("PRRP_GRAPH") && atoi(getenv("PRRP_GRAPH")) == 0)) {
+    Timer timer;
+    tl_timer = getenv("PRRP_TRACE") ? &timer : nullptr;
+    struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
+    Arena ar(s);
+    CaluOut out;
+    caluprrp_enqueue(A, lda, m, n, b, tau, P, perm, s, ar, out);
+    return caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, tl_timer);
+  }
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  auto& plans = calu_plans();
+  CaluPlan* pl = nullptr;
+  for (auto& q : plans)
+    if (q->A == A && q->lda == lda && q->m == m && q->n == n && q->b == b && q->tau == tau && q->P == P &&
+        q->perm == perm && q->dev == dev)
+      pl = q.get();
+  if (!pl) {
+    if (plans.size() >= kMaxPlans) {
+      auto lru = std::min_element(plans.begin(), plans.end(),
+                                  [](const std::unique_ptr<CaluPlan>& x, const std::unique_ptr<CaluPlan>& y) {
+                                    return x->used < y->used;
+                                  });
+      CU_TRY(cudaStreamSynchronize(s));
+      plans.erase(lru);
+    }
+    std::unique_ptr<CaluPlan> np(new CaluPlan{A, lda, m, n, b, tau, P, perm, dev});
+    // capture on a private stream (the caller's may be the legacy stream)
+    static thread_local cudaStream_t cs = nullptr;
+    if (!cs) CU_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const int npan = (int)((n + b - 1) / b);
+    tl_sched_slots = (unsigned)(4 * npan + 64);
+    int* sched = nullptr;
+    CU_TRY(cudaMalloc(&sched, sizeof(int) * 2 * tl_sched_slots));
+    np->bufs.push_back(sched);
+    CU_TRY(cudaMemset(sched, 0, sizeof(int) * 2 * tl_sched_slots));
+    tl_sched = sched;
+    tl_sched_next = 0;
+    cudaGraph_t g = nullptr;
+    CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    try {
+      Arena ar(cs, &np->bufs);
+      caluprrp_enqueue(A, lda, m, n, b, tau, P, perm, cs, ar, np->out);
+    } catch (...) {
+      tl_sched = nullptr;
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    tl_sched = nullptr;
+    CU_TRY(cudaStreamEndCapture(cs, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) fail(PRRP_ERR_CUDA, "cudaGraphInstantiate failed");
+    plans.push_back(std::move(np));
+    pl = plans.back().get();
+  }
+  pl->used = ++g_plan_clock;
+  CU_TRY(cudaGraphLaunch(pl->exec, s));
+  return caluprrp_finish(pl->out, s, swap_counts, tchg3, stats, err, host_t0, nullptr);
+}
+
+int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,
+                    prrp_err* err, std::chrono::steady_clock::time_point host_t0, Timer* timer) {
+  const int npanels = out.npanels, maxnodes = out.maxnodes, b = out.b;
+  const auto& charges = out.charges;
+  const auto& node_members = out.node_members;
+  const auto host_t1 = std::chrono::steady_clock::now();
   DevState hs;
-  read_state(st, hs, s);
+  read_state(out.st, hs, s);
+  if (getenv("PRRP_HOSTTIME")) {
+    const auto host_t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[prrp calu host] enqueue %.3f ms, then wait %.3f ms\n",
+            std::chrono::duration<double, std::milli>(host_t1 - host_t0).count(),
+            std::chrono::duration<double, std::milli>(host_t2 - host_t1).count());
+  }
+  int32_t* swaps_dev = out.swaps_dev;
+  int32_t* node_swaps = out.node_swaps;
   std::vector<int32_t> sw(npanels);
   CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
   std::vector<int32_t> nsw((size_t)npanels * maxnodes);
@@ -1319,9 +1561,12 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     stats->total_swaps = 0;
     for (int v : sw) stats->total_swaps += v;
   }
-  if (tl_timer) {
+  if (getenv("PRRP_HOSTTIME"))
+    fprintf(stderr, "[prrp calu host] stats done at %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count());
+  if (timer) {
     prrp_timing tm;
-    timer.collect(&tm);
+    timer->collect(&tm);
     fprintf(stderr, "[prrp calu timing] total %.3f ms:", tm.total_ms);
     for (int c = 0; c < PRRP_K_COUNT; ++c) fprintf(stderr, " %d:%.3f", c, tm.ms[c]);
     fprintf(stderr, "\n");

@@ -294,3 +294,158 @@ __global__ void __launch_bounds__(256) schur_simt_kernel(const double* L, int64_
   mx = block_max(mx, red);
   if (threadIdx.x == 0) atomic_max_abs(&st->inter_max, mx);
 }
+
+// Warp-specialised persistent variant for any K: one producer warp claims
+// 128 x 64 tiles from a global counter (dynamic scheduling: a CTA that
+// starts late because a concurrent stream holds its SM simply claims fewer
+// tiles) and streams their K chunks through a SW_ST-deep mbarrier ring
+// (continuous across tiles, so the next tile's operands are in flight while
+// the current one finishes); the claimed tile id rides in the ring slot of
+// its first chunk.  Eight consumer warps own a 32 x 32 sub-tile each,
+// prefetch their C elements into registers at the start of a tile (the HBM
+// read overlaps the MMA loop) and release each stage with one arrive per
+// warp.  At most `quantum` tiles per CTA.  stream_c: C is read and written
+// with evict-first hints (an update whose result is not read again soon).  Same fragments, same k order
+// (increasing, from a zero accumulator) and the same epilogue rounding as
+// schur_dmma_kernel: bit-identical results.  ctr[0] (claims) and ctr[1]
+// (finished CTAs) are reset by the last CTA.
+#define SW_KC 32
+#define SW_ST 4
+#define SW_CONS 8
+#define SW_THREADS ((SW_CONS + 1) * 32)
+struct SchurWSmem {
+  double a[SW_ST][SCH_BM * SW_KC];
+  double b[SW_ST][SCH_BN * SW_KC];
+  unsigned long long full[SW_ST];
+  unsigned long long empty[SW_ST];
+  int tile[SW_ST];
+  double red[40];
+};
+
+__global__ void __launch_bounds__(SW_THREADS, 1)
+schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
+                double* C, int64_t ldc, int M, int N, int K, int vec_ok, DevState* st, int* ctr, int quantum,
+                int stream_c) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  SchurWSmem& S = *reinterpret_cast<SchurWSmem*>(sbuf);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ntN = (N + SCH_BN - 1) / SCH_BN, ntM = (M + SCH_BM - 1) / SCH_BM;
+  const int ntiles = prrp_failed(st) ? 0 : ntM * ntN;   // a failed factorization claims nothing
+  const int nk = (K + SW_KC - 1) / SW_KC;
+  constexpr uint32_t kStageBytes = (SCH_BM + SCH_BN) * SW_KC * 8;
+  if (t == 0) {
+    for (int s = 0; s < SW_ST; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], SW_CONS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapL) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapB) : "memory");
+  }
+  __syncthreads();
+  double mx = 0.0;
+  if (warp == SW_CONS) {
+    // ---- producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int claimed = 0;; ++claimed) {
+        int tile = claimed < quantum ? atomicAdd(&ctr[0], 1) : ntiles;
+        if (tile >= ntiles) tile = -1;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % SW_ST;
+          if (it >= SW_ST) mbar_wait(&S.empty[s], ((it / SW_ST) & 1) ^ 1);
+          if (kc == 0) {
+            *reinterpret_cast<volatile int*>(&S.tile[s]) = tile;
+            if (tile < 0) { mbar_arrive(&S.full[s]); break; }
+          }
+          const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+          mbar_expect_tx(&S.full[s], kStageBytes);
+#pragma unroll 1
+          for (int g = 0; g < SCH_BM / 8; ++g)
+            tma_load_2d(&S.a[s][g * SW_KC * 8], &mapL, &S.full[s], m0 + 8 * g, kc * SW_KC);
+#pragma unroll 1
+          for (int g = 0; g < SCH_BN / 8; ++g)
+            tma_load_2d(&S.b[s][g * SW_KC * 8], &mapB, &S.full[s], n0 + 8 * g, kc * SW_KC);
+        }
+        if (tile < 0) break;
+      }
+    }
+  } else {
+    // ---- consumers
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int fr = lane & 3, fc = lane >> 2;
+    uint32_t it = 0;
+    for (;;) {
+      mbar_wait(&S.full[it % SW_ST], (it / SW_ST) & 1);
+      const int tile = *reinterpret_cast<volatile int*>(&S.tile[it % SW_ST]);
+      if (tile < 0) break;
+      const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+      double cv[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm + i * 8 + fc;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c0 = n0 + wn + j * 8 + 2 * fr;
+          const double* cp = C + (int64_t)r * ldc + c0;
+          if (r < M && vec_ok && c0 + 1 < N) {
+            const double2 v = stream_c ? __ldcs(reinterpret_cast<const double2*>(cp))
+                                       : *reinterpret_cast<const double2*>(cp);
+            cv[i][j][0] = v.x;
+            cv[i][j][1] = v.y;
+          } else {
+            cv[i][j][0] = (r < M && c0 < N) ? cp[0] : 0.0;
+            cv[i][j][1] = (r < M && c0 + 1 < N) ? cp[1] : 0.0;
+          }
+        }
+      }
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = it % SW_ST;
+        if (kc > 0) mbar_wait(&S.full[s], (it / SW_ST) & 1);
+        const double* sa = S.a[s];
+        const double* sb = S.b[s];
+#pragma unroll
+        for (int k4 = 0; k4 < SW_KC; k4 += 4) {
+          double af[4], bf[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SW_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm + i * 8 + fc;
+        if (r >= M) continue;
+        double* crow = C + (int64_t)r * ldc;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c0 = n0 + wn + j * 8 + 2 * fr;
+          const double v0 = sub_rn(cv[i][j][0], acc[i][j][0]);
+          const double v1 = sub_rn(cv[i][j][1], acc[i][j][1]);
+          if (vec_ok && c0 + 1 < N) {
+            if (stream_c) __stcs(reinterpret_cast<double2*>(crow + c0), make_double2(v0, v1));
+            else *reinterpret_cast<double2*>(crow + c0) = make_double2(v0, v1);
+            mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+          } else {
+            if (c0 < N) { crow[c0] = v0; mx = fmax(mx, fabs(v0)); }
+            if (c0 + 1 < N) { crow[c0 + 1] = v1; mx = fmax(mx, fabs(v1)); }
+          }
+        }
+      }
+    }
+  }
+  mx = block_max(mx, S.red);
+  if (t == 0) {
+    if (mx > 0.0) atomic_max_abs(&st->inter_max, mx);
+    if (atomicAdd(&ctr[1], 1) == (int)gridDim.x - 1) { ctr[0] = 0; ctr[1] = 0; }
+  }
+}

@@ -37,8 +37,11 @@ def main():
         rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, 2.0, args.P,
                                ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
                                _lib.stream_handle())
+        t1 = time.perf_counter()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if os.environ.get("PRRP_HOSTTIME"):
+            print(f"call returned after {(t1 - t0) * 1e3:.1f} ms, synchronized after {dt * 1e3:.1f} ms", flush=True)
         _lib.raise_for(rc, err, "caluprrp")
         gf = 2 * n ** 3 / 3 / dt / 1e9
         print(f"rep {r}: n={n} b={b} P={args.P}: {dt * 1e3:.1f} ms, {gf:.0f} GFLOP/s, swaps {sum(sw)}, "
