@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--secondary-b", type=int, default=128, help="also report this panel width (0 = off)")
     ap.add_argument("--calu-n", type=int, default=16384,
                     help="also time CALU_PRRP (BASELINE config 4: randn(n), b=64, binary tree P=8); 0 = off")
+    ap.add_argument("--calu5-n", type=int, default=32768,
+                    help="also time CALU_PRRP (BASELINE config 5 on 1 GPU: U(-1,1), b=128, P=8); 0 = off")
     return ap.parse_args()
 
 
@@ -277,20 +279,20 @@ def run_device(args):
         extra["secondary"] = {"b": args.secondary_b, "ms_per_step": ms2,
                               "value": ws * lu_flops(n) / (ms2 * 1e-3) / 1e9, "unit": UNIT}
 
-    # BASELINE config 4: CALU_PRRP, randn(16384, seed 42), b = 64, binary tournament tree over P = 8
-    if args.calu_n and rank == 0:
+    def calu_line(cn, cb, gen, label, reps=2):
+        """CALU_PRRP (binary tree, P = 8) on a device-resident matrix; the first two
+        calls capture and upload the factorization's CUDA graph (untimed)."""
         import ctypes
-        cn = args.calu_n
-        ca = matgen.gen_randn(cn, args.seed, order="C")
+        ca = (matgen.gen_urand if gen == "urand" else matgen.gen_randn)(cn, args.seed, order="C")
         cld = cn + (cn & 1)
         cprist = torch.empty((cn, cld), dtype=torch.float64, device="cuda")
         cprist[:, :cn].copy_(torch.from_numpy(ca))
         del ca
         cwork = torch.empty_like(cprist)
         cperm = torch.empty(cn, dtype=torch.int64, device="cuda")
-        npc = (cn + 63) // 64
+        npc = (cn + cb - 1) // cb
         ct = []
-        for i in range(3):
+        for i in range(2 + reps):
             cwork.copy_(cprist)
             sw = (ctypes.c_int32 * npc)()
             chg = (ctypes.c_int64 * npc)()
@@ -298,20 +300,31 @@ def run_device(args):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rc = lib.prrp_caluprrp(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, 64, float(tau), 8,
+            rc = lib.prrp_caluprrp(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, float(tau), 8,
                                    ctypes.c_void_p(cperm.data_ptr()), sw, chg, ctypes.byref(cst), ctypes.byref(cerr),
                                    _lib.stream_handle())
             e1.record()
             e1.synchronize()
             _lib.raise_for(rc, cerr, "prrp_caluprrp")
-            if i > 0:
+            if i >= 2:
                 ct.append(e0.elapsed_time(e1))
         cms = statistics.mean(ct)
-        extra["calu_config4"] = {"workload": f"CALU_PRRP randn({cn}, seed {args.seed}), b=64, tau={tau}, binary tree P=8",
-                                 "ms_per_step": cms, "value": lu_flops(cn) / (cms * 1e-3) / 1e9, "unit": UNIT,
-                                 "swaps": int(sum(sw)), "growth_factor": cst.intermediate_max / cst.original_max}
         del cprist, cwork, cperm
         torch.cuda.empty_cache()
+        v = lu_flops(cn) / (cms * 1e-3) / 1e9
+        return {"workload": f"CALU_PRRP {label}({cn}, seed {args.seed}), b={cb}, tau={tau}, binary tree P=8, 1 GPU",
+                "ms_per_step": cms, "value": v, "unit": UNIT,
+                "fp64_peak_fraction": (v / 1e3) / pk.value if pk.value else None,
+                "swaps": int(sum(sw)), "growth_factor": cst.intermediate_max / cst.original_max,
+                "timing": f"CUDA events around prrp_caluprrp, mean of {reps} steps after 2 untimed "
+                          "(graph capture + upload)"}
+
+    # BASELINE config 4: CALU_PRRP, randn(16384, seed 42), b = 64, binary tournament tree over P = 8
+    if args.calu_n and rank == 0:
+        extra["calu_config4"] = calu_line(args.calu_n, 64, "randn", "randn")
+    # BASELINE config 5 on one GPU: CALU_PRRP, U(-1,1) n = 32768 (8 GiB), b = 128, P = 8
+    if args.calu5_n and rank == 0:
+        extra["calu_config5"] = calu_line(args.calu5_n, 128, "urand", "urand")
 
     # end to end through the public API: host input in pinned memory -> device -> factors on host
     e2e = None
