@@ -274,3 +274,22 @@ __global__ void calu_leaf_lo_kernel(int64_t* leaf_lo, int64_t p_eff, int64_t bas
   const int64_t i = threadIdx.x;
   for (int64_t j = i; j < p_eff; j += blockDim.x) leaf_lo[j] = j * base + min(j, extra);
 }
+
+// A21 of the permuted panel, transposed: out[k * ldo + t] = A[rowof[t], col0 + k]
+// for t < ncol, k < b (32 rows per block through a padded shared tile)
+__global__ void __launch_bounds__(256) calu_gather_t_kernel(const double* A, int64_t lda, int64_t col0, int b,
+                                                           int64_t ncol, const int64_t* rowof, double* out,
+                                                           int64_t ldo) {
+  extern __shared__ double tile[];   // b x 33
+  const int64_t t0 = (int64_t)blockIdx.x * 32;
+  const int nt = (int)min((int64_t)32, ncol - t0);
+  for (int e = threadIdx.x; e < 32 * b; e += blockDim.x) {
+    const int tl = e / b, k = e % b;
+    if (tl < nt) tile[k * 33 + tl] = A[rowof[t0 + tl] * lda + col0 + k];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * b; e += blockDim.x) {
+    const int k = e / 32, tl = e % 32;
+    if (tl < nt) out[(int64_t)k * ldo + t0 + tl] = tile[k * 33 + tl];
+  }
+}

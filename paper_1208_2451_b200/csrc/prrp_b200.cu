@@ -72,6 +72,8 @@ int report(prrp_err* err, const Fail& f) {
   return f.code;
 }
 
+__global__ void form_q_kernel(const double* refl, int h, int steps, double* Q, int neg_t = 0);
+
 // ---------------------------------------------------------------- device probe
 // claim-counter slots of the dynamically scheduled Schur kernel; a slot is
 // reused kSchedSlots launches later (long after its launch has finished)
@@ -105,6 +107,7 @@ DeviceCaps& caps() {
       set_max_dyn((const void*)fn);
     }
     set_max_dyn((const void*)trsm_kernel);
+    set_max_dyn((const void*)form_q_kernel);
     set_max_dyn((const void*)permute_kernel);
     set_max_dyn((const void*)blockrow_kernel);
     set_max_dyn((const void*)compose_kernel);
@@ -604,7 +607,15 @@ void fill_stats(const DevState& hs, prrp_stats* stats) {
 }
 
 // Q = H_0 H_1 ... assembled like pivoted_qr._reflect (q[:, k:] -= outer(beta*qv, v)).
-__global__ void form_q_kernel(const double* refl, int h, int steps, double* Q /* col-major h x h */) {
+// Q = H_0 H_1 ... H_{steps-1} from a reflector log.  neg_t = 0: Q column-major;
+// neg_t = 1: -Q^T column-major (the Schur kernel's L operand for R12 = Q^T A21^T)
+__global__ void zero2d_kernel(double* C, int64_t ldc, int rows, int64_t cols) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x)
+    C[(e / cols) * ldc + e % cols] = 0.0;
+}
+
+__global__ void form_q_kernel(const double* refl, int h, int steps, double* Q, int neg_t) {
   extern __shared__ __align__(16) double q[];   // row-major h x h
   __shared__ double qv[PRRP_MAXH];
   const int t = threadIdx.x;
@@ -628,7 +639,8 @@ __global__ void form_q_kernel(const double* refl, int h, int steps, double* Q /*
   }
   for (int e = t; e < h * h; e += blockDim.x) {
     const int i = e / h, j = e % h;
-    Q[i + (int64_t)j * h] = q[e];
+    if (neg_t) Q[e] = -q[e];
+    else Q[i + (int64_t)j * h] = q[e];
   }
 }
 
@@ -1030,6 +1042,14 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   double* Rsmall = ar.get<double>((size_t)b * b);
   double* refl = ar.get<double>((size_t)b * (b + 1));
   int32_t* perm_small = ar.get<int32_t>(b);
+  // R12 of the final panel QR as a DMMA product (PRRP_CALU_R12_GEMM=1) instead
+  // of the logged reflectors applied row by row (default: measured faster in
+  // the three-stream schedule, 1745 vs 1794 ms at n = 32768, b = 128)
+  static const bool calu_r12_gemm = getenv("PRRP_CALU_R12_GEMM") && atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
+  double* Qneg = ar.get<double>((size_t)b * b);
+  const int64_t ld21t = ((m + 7) / 8) * 8;
+  double* A21t = ar.get<double>((size_t)b * ld21t);
+  DevState* st_r12 = new_state(ar, s);   // the product's |C| must not enter the growth statistics
   // tree nodes
   std::vector<NodeBufs> nodes(maxnodes);
   const int64_t leafmax = m / std::max<int64_t>(1, std::min<int64_t>(P, std::max<int64_t>(1, m / (b + 1)))) + 1;
@@ -1301,6 +1321,21 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
         }
         calu_copy_r11_kernel<<<1, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
+        if (calu_r12_gemm && (bj % 2 == 0)) {
+          // R12 = Q^T A21^T on the DMMA pipe: Q from the reflector log, A21's
+          // rows gathered transposed, C = 0 - (-Q^T) A21^T (the reflectors'
+          // sequential application and this product agree to a few ulps; the
+          // reference's own dgemv order is not reproducible either)
+          const int64_t ncol = rows - bj;
+          form_q_kernel<<<1, 256, (size_t)bj * bj * 8, sm>>>(refl, bj, bj, Qneg, 1);
+          calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, sm>>>(
+              A, lda, col0, bj, ncol, pos2row + col0 + bj, A21t, ld21t);
+          zero2d_kernel<<<(unsigned)std::min<int64_t>(4 * sms, (ncol * bj + 255) / 256), 256, 0, sm>>>(
+              B.Rbuf + bj, rows, bj, ncol);
+          tend(sm);
+          schur_update(B.Rbuf + bj, rows, Qneg, bj, A21t, ld21t, bj, ncol, bj, st_r12, sm, 0, 0);
+          tbegin(PRRP_K_FINALIZE, sm);
+        } else {
         const size_t dyn = (size_t)bj * (bj + 1) * 8;
         const unsigned grid = (unsigned)std::min<int64_t>(sms * 4, (rows - bj + 7) / 8);
         switch ((bj + 31) / 32) {
@@ -1308,6 +1343,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           case 2: calu_apply_refl_kernel<2><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
           case 3: calu_apply_refl_kernel<3><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
           default: calu_apply_refl_kernel<4><<<grid, 256, dyn, sm>>>(A, lda, col0, bj, rows, pos2row, refl, B.Rbuf, st); break;
+        }
         }
         CU_TRY(cudaGetLastError());
         tend(sm);
