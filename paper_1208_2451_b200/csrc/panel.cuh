@@ -64,6 +64,12 @@ struct PanelArgs {
   int swap_slot;            // index into swaps_dev for this node's swap count
   int tree_level, tree_index;   // CALU tournament node (error payload), -1 otherwise
   double* fro;              // out (mode 0): ||panel||_F of this node
+  // panel2 multi-cluster mode (mode 0 only): ngroups clusters exchange their
+  // winners through global memory each step
+  int ngroups;              // 0/1: one cluster
+  double* xg;               // 2 x ngroups x P2_XS doubles (step-parity slots)
+  unsigned long long* xflag;   // ngroups flags: epoch + k + 1 once group g published step k
+  unsigned long long epoch;
 };
 
 struct Rec {

@@ -14,7 +14,12 @@
 // boundary the finished rows go to the global row-save area and 8 rows move
 // from shared memory into the window.  From step 64 on, the column is
 // entirely in registers.  One column per thread, <= 256 per CTA, <= 4096 per
-// 16-CTA cluster.
+// 16-CTA cluster.  Taller panels (LU_PRRP b = 128, p <= 8192) run as
+// `ngroups` co-resident clusters: each cluster's winner CTA publishes its
+// record and reflector to a global step-parity slot and releases a flag
+// (epoch + k + 1); every CTA acquires the other groups' flags, takes the
+// lexicographic best (largest key, then lowest global position) and, if it
+// lies in another cluster, loads that reflector from L2.
 #pragma once
 #include "panel1.cuh"
 
@@ -23,6 +28,7 @@
 #define P2_T 256
 #define P2_NW (P2_T / 32)
 #define P2_RS (P2_T * 8)         // shared row stride (bytes)
+#define P2_XS 136                // global exchange slot: 8 record doubles + 128 v
 
 struct P2Shared {
   double wpub[2][P2_NW][P2_H];
@@ -35,6 +41,8 @@ struct P2Shared {
   int slog[P2_H];
   double fro;
   int failed;
+  int gwin;                 // multi-cluster: group of the global winner
+  double grec[8];           // its record (key, pos, alpha, beta, fro, jl|skip)
 };
 
 // element i (relative to row 8*KB) of a split column: i < 64 in registers,
@@ -233,7 +241,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
   cl.sync();
   if (*cl.map_shared_rank(&S.failed, 0)) { cl.sync(); return; }
   const int mode = a.mode;
-  const int64_t j0 = (int64_t)c * a.per;
+  const int G = a.ngroups > 1 ? a.ngroups : 1;
+  const int grp = (int)(blockIdx.x / (unsigned)C);
+  const int64_t j0 = ((int64_t)grp * C + c) * a.per;
   const int nl = (int)max((int64_t)0, min(a.per, a.p - j0));
   const bool on = t < nl;
   double* rsave = a.ovf;             // finished rows: rsave[row * p + j0 + t]
@@ -359,15 +369,99 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       Wp = &S.rec[buf][rc];
     }
     const P1Rec& W = *Wp;
-    const long long wpos = W.pos;
-    const int skip = W.skip;
-    const double beta = W.beta, alpha = W.alpha;
-    const int wjl = W.jl;
-    const bool mine = rc == c;
+    long long wpos = W.pos;
+    int skip = W.skip;
+    double beta = W.beta, alpha = W.alpha;
+    int wjl = W.jl;
+    bool mine = rc == c;
+    int ww = wjl >> 5;
+    bool remote = false;             // the global winner is in another cluster
+    if (G > 1) {
+      // ---- cross-cluster exchange through global memory
+      const unsigned long long tag = a.epoch + (unsigned long long)k + 1ull;
+      if (mine && warp == 0) {
+        double* slot = a.xg + ((int64_t)buf * G + grp) * P2_XS;
+        if (lane == 0) {
+          double cf = 0.0;
+          if (k == 0 && mode == 0)
+            for (int q = 0; q < C; ++q) cf += S.rec[buf][q].fro;
+          slot[0] = W.key;
+          slot[1] = __longlong_as_double(W.pos);
+          slot[2] = W.alpha;
+          slot[3] = W.beta;
+          slot[4] = cf;
+          slot[5] = __longlong_as_double((long long)(unsigned)W.jl | ((long long)W.skip << 32));
+        }
+        if (!W.skip)
+          for (int i = lane; i < 8 * (L + 1); i += 32) slot[8 + i] = S.wpub[buf][ww][i];
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(a.xflag + grp), "l"(tag) : "memory");
+      }
+      if (warp == 0) {
+        double key = -INFINITY;
+        long long gp = LLONG_MAX;
+        bool ok = false;
+        if (lane < G) {
+          if (lane == grp) {
+            ok = W.jl >= 0;
+            key = W.key;
+            gp = W.pos;
+          } else {
+            unsigned long long f;
+            do {
+              asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.xflag + lane) : "memory");
+            } while (f != tag);
+            const double* slot = a.xg + ((int64_t)buf * G + lane) * P2_XS;
+            key = __ldcg(slot);
+            gp = __double_as_longlong(__ldcg(slot + 1));
+            ok = (int)(unsigned)__double_as_longlong(__ldcg(slot + 5)) >= 0;
+          }
+        }
+        const unsigned long long u = ok ? p1_ukey(key, true) : 0ull;
+        int g = p1_best_lane(u, ok ? (unsigned)gp : 0xffffffffu);
+        if (g < 0) g = grp;
+        if (lane == 0) S.gwin = g;
+        if (g != grp) {
+          const double* slot = a.xg + ((int64_t)buf * G + g) * P2_XS;
+          if (lane < 8) S.grec[lane] = __ldcg(slot + lane);
+          const long long bits = __double_as_longlong(__ldcg(slot + 5));
+          if ((bits >> 32) == 0)
+            for (int i = lane; i < 8 * (L + 1); i += 32) S.vs[i] = __ldcg(slot + 8 + i);
+        }
+        if (k == 0 && mode == 0 && grp == 0 && c == 0) {
+          // ||panel||_F over the groups, in group order
+          double f = 0.0;
+          for (int q = 0; q < G; ++q) {
+            double cf;
+            if (q == grp) {
+              cf = 0.0;
+              for (int r2 = 0; r2 < C; ++r2) cf += S.rec[buf][r2].fro;
+            } else {
+              cf = __ldcg(a.xg + ((int64_t)buf * G + q) * P2_XS + 4);
+            }
+            f += cf;
+          }
+          if (lane == 0) *a.fro = sqrt(f);
+        }
+      }
+      __syncthreads();
+      if (S.gwin != grp) {
+        remote = true;
+        mine = false;
+        wpos = __double_as_longlong(S.grec[1]);
+        alpha = S.grec[2];
+        beta = S.grec[3];
+        const long long bits = __double_as_longlong(S.grec[5]);
+        wjl = (int)(unsigned)bits;
+        skip = (int)(bits >> 32);
+        ww = wjl >> 5;
+      }
+    }
     if (t == 0) { S.alog[k] = alpha; S.slog[k] = skip; }
-    const int ww = wjl >> 5;
     const double* vs = mine ? S.wpub[buf][ww] : S.vs;
-    if (!mine) {
+    if (!mine && !remote) {
       if (warp == 0 && !skip) {
         for (int q = lane; q < 4 * (L + 1); q += 32) {       // 16-byte chunks of the live rows
           const uint32_t src = p1_mapa((uint32_t)__cvta_generic_to_shared(&S.wpub[buf][ww][2 * q]), rc);
@@ -379,7 +473,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       }
       __syncthreads();
     }
-    if (C > 1 && k == 0 && mode == 0 && c == 0 && warp == 0) {
+    if (G == 1 && C > 1 && k == 0 && mode == 0 && c == 0 && warp == 0) {
       double f = lane < C ? S.rec[buf][lane].fro : 0.0;
       for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
       if (lane == 0) *a.fro = sqrt(f);

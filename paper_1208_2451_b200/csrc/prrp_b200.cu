@@ -316,10 +316,11 @@ size_t ovf_elems(int h, int64_t p, int bsel) {
                    (size_t)h * p});
 }
 
+// `groups` clusters of g.C CTAs each (groups > 1: the multi-cluster panel engine)
 template <typename K, typename... Args>
-void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Args... args) {
+void launch_clusters(K kernel, const PanelCfg& g, int groups, size_t dyn, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.C);
+  cfg.gridDim = dim3(g.C * groups);
   cfg.blockDim = dim3(g.T);
   cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
@@ -331,6 +332,11 @@ void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Arg
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CU_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
+template <typename K, typename... Args>
+void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Args... args) {
+  launch_clusters(kernel, g, 1, dyn, s, args...);
 }
 
 // GEPP of a b x b block (register kernel for b <= 64, shared-memory kernel above)
@@ -372,7 +378,17 @@ struct PanelBuffers {
   int32_t* moved;
   double* refl;
   int32_t* moved_cnt = nullptr;
+  double* xg = nullptr;                   // multi-cluster panel exchange slots (panel2.cuh)
+  unsigned long long* xflag = nullptr;
 };
+
+constexpr int kP2MaxGroups = 4;
+unsigned long long g_xepoch = 0;        // per-launch flag epoch of the multi-cluster engine
+void alloc_exchange(Arena& ar, cudaStream_t s, PanelBuffers& B) {
+  B.xg = ar.get<double>((size_t)2 * kP2MaxGroups * P2_XS);
+  B.xflag = ar.get<unsigned long long>(kP2MaxGroups);
+  CU_TRY(cudaMemsetAsync(B.xflag, 0, sizeof(unsigned long long) * kP2MaxGroups, s));
+}
 
 constexpr int kMaxCand = 2048;   // trsm blocks per panel (candidate slots)
 
@@ -434,6 +450,21 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
     a1.per = (p + c1 - 1) / c1;
     const size_t dyn = a1.per > P1_T ? (size_t)P1_H * P1_T * 8 : 0;
     launch_cluster(panel_qrcp1_kernel, g1, dyn, s, a1);
+  } else if (h == P2_H && p > (int64_t)P2_T * maxc && p <= (int64_t)P2_T * maxc * kP2MaxGroups && maxc == 16 &&
+             aligned && B.xg && !force_generic_panel() && !getenv("PRRP_P2_NOGROUPS")) {
+    // taller than one cluster: co-resident clusters exchanging winners through L2
+    PanelCfg g2 = g;
+    g2.C = maxc;
+    g2.T = P2_T;
+    const int groups = (int)((p + (int64_t)P2_T * maxc - 1) / ((int64_t)P2_T * maxc));
+    PanelArgs a2 = a;
+    a2.per = (p + (int64_t)groups * maxc - 1) / ((int64_t)groups * maxc);
+    a2.ngroups = groups;
+    a2.xg = B.xg;
+    a2.xflag = B.xflag;
+    g_xepoch += 1024;
+    a2.epoch = g_xepoch;
+    launch_clusters(panel_qrcp2_kernel, g2, groups, (size_t)(P2_H - P2_W) * P2_T * 8, s, a2);
   } else if (h == P2_H && p <= (int64_t)P2_T * maxc && aligned && !force_generic_panel()) {
     // thread-per-column split-column engine (h = 128): register window + shared rows
     PanelCfg g2 = g;
@@ -768,6 +799,7 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   B.cand = ar.get<double>(kMaxCand);
   B.cand_flat = ar.get<long long>(kMaxCand);
   B.moved = ar.get<int32_t>(2 * m);
+  alloc_exchange(ar, s, B);
   B.refl = nullptr;
   // per-panel-parity buffers (the three streams overlap consecutive panels)
   int32_t* movedb[2] = {B.moved, ar.get<int32_t>(2 * m)};
@@ -894,8 +926,9 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
       // persistent trailing update on all but 24 SMs: the high-priority stream
       // keeps room for the panel cluster (16 SMs of one GPC) and its kernels
       // (PRRP_SCHUR_WIDE_CTAS overrides; 0 = one tile per CTA)
-      static const int wide_ctas = getenv("PRRP_SCHUR_WIDE_CTAS") ? atoi(getenv("PRRP_SCHUR_WIDE_CTAS"))
-                                                                  : std::max(1, sms - 24);
+      // (b = 128 panels taller than 4096 rows take two 16-CTA clusters: 40 SMs kept free)
+      static const int wide_env = getenv("PRRP_SCHUR_WIDE_CTAS") ? atoi(getenv("PRRP_SCHUR_WIDE_CTAS")) : 0;
+      const int wide_ctas = wide_env > 0 ? wide_env : std::max(1, sms - (b > 64 && m > 4096 ? 40 : 24));
       if (w1 > 0)
         schur_update(A + (col0 + bj) * lda + cw0, lda, L, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd,
                      wide_ctas);
@@ -1038,6 +1071,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   B.cand = ar.get<double>(kMaxCand);
   B.cand_flat = ar.get<long long>(kMaxCand);
   B.moved = ar.get<int32_t>(2 * m);
+  alloc_exchange(ar, s, B);
   double* Llog = ar.get<double>((size_t)b * ldl);
   double* Rsmall = ar.get<double>((size_t)b * b);
   double* refl = ar.get<double>((size_t)b * (b + 1));
@@ -1714,6 +1748,7 @@ int prrp_strong_rrqr(const double* a, int64_t lda, int32_t h, int64_t p, int32_t
     B.cand = ar.get<double>(kMaxCand);
     B.cand_flat = ar.get<long long>(kMaxCand);
     B.moved = ar.get<int32_t>(2 * p);
+    alloc_exchange(ar, s, B);
     const int steps = (int)std::min<int64_t>(h, p);
     B.refl = ar.get<double>((size_t)steps * (h + 1));
     const int64_t ldl = std::max<int64_t>(1, p - bsel);
