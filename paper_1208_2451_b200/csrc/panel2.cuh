@@ -43,6 +43,7 @@ struct P2Shared {
   int failed;
   int gwin;                 // multi-cluster: group of the global winner
   double grec[8];           // its record (key, pos, alpha, beta, fro, jl|skip)
+  double gx[4][P2_XS];      // staged remote records + reflectors (<= 4 groups)
 };
 
 // element i (relative to row 8*KB) of a split column: i < 64 in registers,
@@ -286,6 +287,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
     S.fro = f;
   }
   const bool log_refl = a.refl != nullptr && c == 0;
+  // PRRP_PANEL_PROF=1 PRRP_PANEL_TL=<panel>: clock64 marks of thread 0 of CTA 0
+  long long* tl = (a.prof && grp == 0 && c == 0 && t == 0 && a.panel_id == a.prof[6]) ? a.prof + 8 : nullptr;
+#define P2_TL(m) if (tl) tl[k * 8 + (m)] = clock64();
 
   int KB = 0;
   for (int k = 0; k < a.steps; ++k) {
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       ++KB;
     }
     const int L = 15 - KB;
+    P2_TL(0)
     const P2Col x{rr, s0 + (uint32_t)(8 * KB) * P2_RS};
     const uint32_t bar = buf ? bar1 : bar0;
     if (t == 0 && C > 1) p1_bar_expect(bar, (uint32_t)(C * (int)sizeof(P1Rec)));
@@ -330,7 +335,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       }
       __syncwarp();
     }
+    P2_TL(1)
     __syncthreads();
+    P2_TL(2)
     // ---- CTA argmax; warp 0 pushes the CTA candidate into every CTA
     const P1Rec* Wp;
     int rc;
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
         }
       }
       p1_bar_wait(bar, (uint32_t)((k >> 1) & 1));
+      P2_TL(3)
       {
         const bool ok = lane < C && S.rec[buf][lane].jl >= 0;
         const unsigned long long u = ok ? p1_ukey(S.rec[buf][lane].key, true) : 0ull;
@@ -394,12 +402,29 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
         }
         if (!W.skip)
           for (int i = lane; i < 8 * (L + 1); i += 32) slot[8 + i] = S.wpub[buf][ww][i];
-        __threadfence();
+        // the warp barrier orders the lanes' stores before lane 0's gpu-scope
+        // release (cumulative), which publishes them with the flag
         __syncwarp();
         if (lane == 0)
           asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(a.xflag + grp), "l"(tag) : "memory");
       }
       if (warp == 0) {
+        // wait for the other groups' step-k records, then fetch every remote
+        // record and reflector in one L2 round trip
+        if (lane < G && lane != grp) {
+          unsigned long long f;
+          do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.xflag + lane) : "memory");
+          } while (f != tag);
+        }
+        __syncwarp();
+        const int nx = 8 + 8 * (L + 1);
+        for (int q = 0; q < G; ++q) {
+          if (q == grp) continue;
+          const double* slot = a.xg + ((int64_t)buf * G + q) * P2_XS;
+          for (int i = lane; i < nx; i += 32) S.gx[q][i] = __ldcg(slot + i);
+        }
+        __syncwarp();
         double key = -INFINITY;
         long long gp = LLONG_MAX;
         bool ok = false;
@@ -409,14 +434,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
             key = W.key;
             gp = W.pos;
           } else {
-            unsigned long long f;
-            do {
-              asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.xflag + lane) : "memory");
-            } while (f != tag);
-            const double* slot = a.xg + ((int64_t)buf * G + lane) * P2_XS;
-            key = __ldcg(slot);
-            gp = __double_as_longlong(__ldcg(slot + 1));
-            ok = (int)(unsigned)__double_as_longlong(__ldcg(slot + 5)) >= 0;
+            key = S.gx[lane][0];
+            gp = __double_as_longlong(S.gx[lane][1]);
+            ok = (int)(unsigned)__double_as_longlong(S.gx[lane][5]) >= 0;
           }
         }
         const unsigned long long u = ok ? p1_ukey(key, true) : 0ull;
@@ -424,11 +444,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
         if (g < 0) g = grp;
         if (lane == 0) S.gwin = g;
         if (g != grp) {
-          const double* slot = a.xg + ((int64_t)buf * G + g) * P2_XS;
-          if (lane < 8) S.grec[lane] = __ldcg(slot + lane);
-          const long long bits = __double_as_longlong(__ldcg(slot + 5));
-          if ((bits >> 32) == 0)
-            for (int i = lane; i < 8 * (L + 1); i += 32) S.vs[i] = __ldcg(slot + 8 + i);
+          if (lane < 8) S.grec[lane] = S.gx[g][lane];
+          if ((__double_as_longlong(S.gx[g][5]) >> 32) == 0)
+            for (int i = lane; i < 8 * (L + 1); i += 32) S.vs[i] = S.gx[g][8 + i];
         }
         if (k == 0 && mode == 0 && grp == 0 && c == 0) {
           // ||panel||_F over the groups, in group order
@@ -439,7 +457,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
               cf = 0.0;
               for (int r2 = 0; r2 < C; ++r2) cf += S.rec[buf][r2].fro;
             } else {
-              cf = __ldcg(a.xg + ((int64_t)buf * G + q) * P2_XS + 4);
+              cf = S.gx[q][4];
             }
             f += cf;
           }
@@ -473,6 +491,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       }
       __syncthreads();
     }
+    P2_TL(4)
     if (G == 1 && C > 1 && k == 0 && mode == 0 && c == 0 && warp == 0) {
       double f = lane < C ? S.rec[buf][lane].fro : 0.0;
       for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
@@ -498,7 +517,9 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
         key = (live && pos == k + 1) ? 1.0 : -1.0;
       }
     }
+    P2_TL(5)
   }
+#undef P2_TL
   cl.sync();
   // ---- R by position, column order; rows >= q of the pivot column of step
   // q are (alpha_q, 0, ..., 0) unless step q was skipped

@@ -468,7 +468,8 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   } else if (h == P2_H && p <= (int64_t)P2_T * maxc && aligned && !force_generic_panel()) {
     // thread-per-column split-column engine (h = 128): register window + shared rows
     PanelCfg g2 = g;
-    g2.C = (int)std::max<int64_t>((p + P2_T - 1) / P2_T, std::min<int64_t>(maxc, (p + cpc - 1) / cpc));
+    static const int64_t cpc2 = getenv("PRRP_P2_COLS") ? atoll(getenv("PRRP_P2_COLS")) : 256;
+    g2.C = (int)std::max<int64_t>((p + P2_T - 1) / P2_T, std::min<int64_t>(maxc, (p + cpc2 - 1) / cpc2));
     g2.T = P2_T;
     PanelArgs a2 = a;
     a2.per = (p + g2.C - 1) / g2.C;

@@ -219,18 +219,42 @@ def _to_host(dev, out):
     return out
 
 
-def split_packed_device(packed, m, n):
+class _Prefault:
+    """Result arrays allocated up front and first-touched by a background
+    thread (torch's multi-threaded fill, GIL released) while the device
+    factorizes: the page faults of ~1 GB of fresh host memory no longer sit
+    between the last kernel and the return."""
+
+    def __init__(self, shapes):
+        import threading
+        self.arrays = [np.empty(sh) for sh in shapes]
+        self.thread = threading.Thread(target=self._touch, daemon=True)
+        self.thread.start()
+
+    def _touch(self):
+        import torch
+        for a in self.arrays:
+            torch.from_numpy(a.reshape(-1)).zero_()
+
+    def get(self):
+        self.thread.join()
+        return self.arrays
+
+
+def split_packed_device(packed, m, n, out=None):
     """split_packed on the device: unit-lower L and upper U built with torch
     and transposed there, so the host receives Fortran-ordered arrays (the
-    reference's layout, luprrp.py:130-132) without a host-side transpose."""
+    reference's layout, luprrp.py:130-132) without a host-side transpose.
+    out: optional pre-allocated host arrays (n x m, n x n)."""
     import torch
     lt = torch.tril(packed, -1)
     lt.diagonal().fill_(1.0)
     lt_t = lt.t().contiguous()
     del lt
     u_t = torch.triu(packed[:n, :]).t().contiguous()
-    l_h = _to_host(lt_t, np.empty((n, m)))
-    u_h = _to_host(u_t, np.empty((n, n)))
+    l_out, u_out = out if out is not None else (np.empty((n, m)), np.empty((n, n)))
+    l_h = _to_host(lt_t, l_out)
+    u_h = _to_host(u_t, u_out)
     return l_h.T, u_h.T
 
 
@@ -251,9 +275,10 @@ def luprrp_factor(a, b, tau=2.0):
     _validate(a, b, tau)
     m, n = a.shape
     _lib.device_lib()
+    pre = _Prefault([(n, m), (n, n)]) if m * n >= (1 << 22) else None
     buf, lda = upload(a)
     perm, st, swaps = run_device("prrp_luprrp", buf, lda, m, n, b, tau)
-    l, u = split_packed_device(buf[:, :n], m, n)
+    l, u = split_packed_device(buf[:, :n], m, n, out=pre.get() if pre else None)
     return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b,
                           stats=_stats(st, swaps, m, n, b))
 

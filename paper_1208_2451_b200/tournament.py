@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .errors import DimensionMismatch
 from .luprrp import (BlockLUFactors, ElimStats, _validate, as_matrix, flop_counters,
-                     split_packed_device, upload)
+                     split_packed_device, upload, _Prefault)
 
 
 @dataclass(frozen=True)
@@ -208,6 +208,7 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
     m, n = a.shape
     lib = _lib.device_lib()
     import torch
+    pre = _Prefault([(n, m), (n, n)]) if m * n >= (1 << 22) else None
     buf, lda = upload(a)
     perm = torch.empty(m, dtype=torch.int64, device="cuda")
     npan = (n + b - 1) // b
@@ -225,5 +226,5 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
                       finish_max=st.finish_max, swap_counts=list(map(int, swaps)),
                       flops_charged=charged, flops_executed=executed,
                       panel_multiplier_max=st.panel_multiplier_max)
-    l, u = split_packed_device(buf[:, :n], m, n)
+    l, u = split_packed_device(buf[:, :n], m, n, out=pre.get() if pre else None)
     return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b, stats=stats)
