@@ -108,6 +108,7 @@ DeviceCaps& caps() {
     }
     set_max_dyn((const void*)trsm_kernel);
     set_max_dyn((const void*)form_q_kernel);
+    CU_TRY(cudaFuncSetAttribute(trsm_c2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmC2Smem));
     set_max_dyn((const void*)permute_kernel);
     set_max_dyn((const void*)blockrow_kernel);
     set_max_dyn((const void*)compose_kernel);
@@ -346,6 +347,13 @@ void launch_gepp(const double* src, int64_t ld, const int32_t* rowmap, int b, do
   else gepp_diag_kernel<<<1, 128, (size_t)b * (b + 1) * 8, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
 }
 
+// b in (64, 128]: 8-lane chunked trsm (trsm_c2_kernel); PRRP_TRSM_W=1 selects
+// the warp-per-column kernel instead
+bool use_trsm_c2() {
+  static const bool v = !(getenv("PRRP_TRSM_W") && atoi(getenv("PRRP_TRSM_W")) != 0);
+  return v;
+}
+
 // PRRP_GENERIC_PANEL=1 forces the generic shared-memory engine (A/B testing)
 bool force_generic_panel() {
   static int v = -1;
@@ -496,9 +504,13 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
       return;
     }
-    if (bsel <= 64) {
+    if (bsel <= 64 || use_trsm_c2()) {
       const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
-      trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
+      if (bsel <= 64)
+        trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
+      else
+        trsm_c2_kernel<<<nbv, TC_T, kTrsmC2Smem, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro,
+                                                       tl, ti);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nbv, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
@@ -1387,9 +1399,13 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         double* fro_inf = nodes[0].B.fro;   // rank check of the final QR: the reference has none (fro = 0)
         CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), sm));
         int nblk;
-        if (bj <= 64) {
+        if (bj <= 64 || use_trsm_c2()) {
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
-          trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
+          if (bj <= 64)
+            trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
+          else
+            trsm_c2_kernel<<<nblk, TC_T, kTrsmC2Smem, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel,
+                                                            fro_inf, -1, -1);
         } else {
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
           const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
@@ -1949,9 +1965,11 @@ int prrp_multiplier_block(const double* R, int64_t ldr, int32_t b, int64_t p, do
       long long* candf = ar.get<long long>(kMaxCand);
       CU_TRY(cudaMemsetAsync(fro0, 0, sizeof(double), s));
       r_in_kernel<<<caps().sms, 256, 0, s>>>(R, ldr, b, p, Rbuf);
-      const int nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
+      const bool c2 = b > 64 && use_trsm_c2();
+      const int nblk = (int)std::min<int64_t>(kMaxCand, c2 ? (ncol + TC_COLS - 1) / TC_COLS : (ncol + TTC - 1) / TTC);
       const size_t tdyn = (((size_t)b * (b + 1) / 2 + 1) / 2 * 2 + (size_t)b * TTCP) * 8;
-      switch ((b + 31) / 32) {
+      if (c2) trsm_c2_kernel<<<nblk, TC_T, kTrsmC2Smem, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1);
+      else switch ((b + 31) / 32) {
         case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
         case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
         case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;

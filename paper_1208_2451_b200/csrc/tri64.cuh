@@ -124,18 +124,20 @@ __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __r
 #define TC_STAMP(k)
 #endif
 
-template <bool EXACT>
-__device__ __forceinline__ bool trsm_c_column(double (&x)[8], const double* __restrict__ us, const double* __restrict__ dg,
-                                              const double* __restrict__ rc, int nk, int lane) {
+// NQ = 8-row chunks per column (8: b <= 64, 16: b <= 128), UP = padded R11 pitch
+template <bool EXACT, int NQ, int UP>
+__device__ __forceinline__ bool trsm_c_column(double (&x)[NQ], const double* __restrict__ us,
+                                              const double* __restrict__ dg, const double* __restrict__ rc, int nk,
+                                              int lane) {
   const int j = lane & 7;
   bool bad = false;
 #pragma unroll 1
   for (int k = nk - 1; k >= 0; --k) {
     double v = x[0];
 #pragma unroll
-    for (int q = 1; q < 8; ++q)
+    for (int q = 1; q < NQ; ++q)
       if (q == k) v = x[q];
-    const double2* ur = reinterpret_cast<const double2*>(us + (8 * k + j) * TC_UP + 8 * k);
+    const double2* ur = reinterpret_cast<const double2*>(us + (8 * k + j) * UP + 8 * k);
     const double2* dr = reinterpret_cast<const double2*>(dg + 8 * k);
     const double2* rr = reinterpret_cast<const double2*>(rc + 8 * k);
     double ut[8], dk[8], rk[8], xs[8];
@@ -163,12 +165,12 @@ __device__ __forceinline__ bool trsm_c_column(double (&x)[8], const double* __re
       else if (j == s) v = xi;
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < NQ; ++q)
       if (q == k) x[q] = v;
 #pragma unroll
-    for (int q = 0; q < 7; ++q) {
+    for (int q = 0; q < NQ - 1; ++q) {
       if (q < k) {
-        const double2* uq = reinterpret_cast<const double2*>(us + (8 * q + j) * TC_UP + 8 * k);
+        const double2* uq = reinterpret_cast<const double2*>(us + (8 * q + j) * UP + 8 * k);
         double u[8];
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
@@ -183,40 +185,38 @@ __device__ __forceinline__ bool trsm_c_column(double (&x)[8], const double* __re
   return bad;
 }
 
-__global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
-                                                      double* L21, int64_t ldl, double* cand, long long* cand_flat,
-                                                      DevState* st, int panel, const double* fro, int tl, int ti) {
-  __shared__ __align__(16) double us[64 * TC_UP];
-  __shared__ __align__(16) double dg[64], rc[64];
-  __shared__ double red_d[33];
-  __shared__ long long red_l[33];
-  if (prrp_failed(st)) return;
+template <int NQ, int UP>
+__device__ __forceinline__ void trsm_c_body(double* us, double* dg, double* rc, double* red_d, long long* red_l,
+                                            const double* __restrict__ Rbuf, int64_t p, int bsel, double* L21,
+                                            int64_t ldl, double* cand, long long* cand_flat, DevState* st, int panel,
+                                            const double* fro, int tl, int ti) {
+  constexpr int BW = 8 * NQ;   // padded R11 width
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int nk = (bsel + 7) >> 3, bp = nk * 8;
   TC_STAMP(0);
   const double frov = (blockIdx.x == 0 && t < 32) ? *fro : 0.0;   // issued before the staging loads
   // padded R11: upper triangle of the first bsel rows, identity on [bsel, bp)
-  for (int base = t; base < bp * 64; base += 8 * TC_T) {
+  for (int base = t; base < bp * BW; base += 8 * TC_T) {
     double v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = base + u * TC_T, l = e >> 6, i = e & 63;
-      v[u] = (e < bp * 64 && l < bsel && i >= l && i < bsel) ? Rbuf[(int64_t)l * p + i] : (l == i ? 1.0 : 0.0);
+      const int e = base + u * TC_T, l = e / BW, i = e % BW;
+      v[u] = (e < bp * BW && l < bsel && i >= l && i < bsel) ? Rbuf[(int64_t)l * p + i] : (l == i ? 1.0 : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = base + u * TC_T, l = e >> 6, i = e & 63;
-      if (e < bp * 64) us[l * TC_UP + i] = v[u];
+      const int e = base + u * TC_T, l = e / BW, i = e % BW;
+      if (e < bp * BW) us[l * UP + i] = v[u];
     }
   }
   __syncthreads();
   TC_STAMP(4);
   for (int i = t; i < bp; i += TC_T) {
-    dg[i] = us[i * TC_UP + i];
+    dg[i] = us[i * UP + i];
     rc[i] = __drcp_rn(dg[i]);
   }
   if (blockIdx.x == 0 && t < 32)
-    r11_checks_warp([&](int k) { return us[k * TC_UP + k]; }, bsel, frov, st, panel, true, tl, ti);
+    r11_checks_warp([&](int k) { return us[k * UP + k]; }, bsel, frov, st, panel, true, tl, ti);
   TC_STAMP(5);
   __syncthreads();
   TC_STAMP(1);
@@ -227,22 +227,22 @@ __global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__
   for (int64_t cb = ((int64_t)blockIdx.x * TC_WARPS + warp) * 4; cb < ncol; cb += (int64_t)gridDim.x * TC_COLS) {
     const int64_t c = cb + g;
     const bool on = c < ncol;
-    double x[8];
+    double x[NQ];
     auto load = [&] {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const int row = j + 8 * q;
         x[q] = (on && row < bsel) ? Rbuf[(int64_t)row * p + bsel + c] : 0.0;
       }
     };
     load();
-    if (__any_sync(0xffffffffu, trsm_c_column<false>(x, us, dg, rc, nk, lane))) {
+    if (__any_sync(0xffffffffu, trsm_c_column<false, NQ, UP>(x, us, dg, rc, nk, lane))) {
       load();
-      trsm_c_column<true>(x, us, dg, rc, nk, lane);
+      trsm_c_column<true, NQ, UP>(x, us, dg, rc, nk, lane);
     }
     if (on) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const int row = j + 8 * q;
         if (row < bsel) {
           L21[(int64_t)row * ldl + c] = x[q];
@@ -257,6 +257,31 @@ __global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__
   reduce_worst(worst, wflat, red_d, red_l);
   if (t == 0) { cand[blockIdx.x] = worst; cand_flat[blockIdx.x] = wflat; }
   TC_STAMP(3);
+}
+
+__global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
+                                                      double* L21, int64_t ldl, double* cand, long long* cand_flat,
+                                                      DevState* st, int panel, const double* fro, int tl, int ti) {
+  __shared__ __align__(16) double us[64 * TC_UP];
+  __shared__ __align__(16) double dg[64], rc[64];
+  __shared__ double red_d[33];
+  __shared__ long long red_l[33];
+  if (prrp_failed(st)) return;
+  trsm_c_body<8, TC_UP>(us, dg, rc, red_d, red_l, Rbuf, p, bsel, L21, ldl, cand, cand_flat, st, panel, fro, tl, ti);
+}
+
+// b in (64, 128]: 16 chunks per column, R11 (128 x TC_UP2) in dynamic shared memory
+#define TC_UP2 130
+constexpr size_t kTrsmC2Smem = (size_t)(128 * TC_UP2 + 2 * 128) * 8;
+__global__ void __launch_bounds__(TC_T) trsm_c2_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
+                                                       double* L21, int64_t ldl, double* cand, long long* cand_flat,
+                                                       DevState* st, int panel, const double* fro, int tl, int ti) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double red_d[33];
+  __shared__ long long red_l[33];
+  if (prrp_failed(st)) return;
+  trsm_c_body<16, TC_UP2>(dsm, dsm + 128 * TC_UP2, dsm + 128 * TC_UP2 + 128, red_d, red_l, Rbuf, p, bsel, L21, ldl,
+                          cand, cand_flat, st, panel, fro, tl, ti);
 }
 
 // out[r][j] = sum_{k >= j} L21[r][gperm[k]] * L11[k][j]
