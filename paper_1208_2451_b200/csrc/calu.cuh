@@ -293,3 +293,45 @@ __global__ void __launch_bounds__(256) calu_gather_t_kernel(const double* A, int
     if (tl < nt) out[(int64_t)k * ldo + t0 + tl] = tile[k * 33 + tl];
   }
 }
+
+// L = -Q^T (column-major b x b) of a logged unpivoted QR, Q^T = H_{b-1} ... H_0:
+// the identity's columns are transformed by the reflectors in log order, two
+// threads per column (rows [0, 64) and [64, 128) in registers, partial dots
+// combined with one shuffle).  Reflector log: refl[k*(b+1) + i] = v_i
+// (zero for i < k), refl[k*(b+1) + b] = beta (0: step skipped).
+__global__ void __launch_bounds__(256) calu_form_negqt_kernel(const double* refl, int b, double* L) {
+  extern __shared__ __align__(16) double rf[];   // b x (b + 1)
+  for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) rf[e] = refl[e];
+  __syncthreads();
+  const int j = threadIdx.x >> 1, hh = threadIdx.x & 1;
+  const bool on = j < b;
+  double m[64];
+#pragma unroll
+  for (int u = 0; u < 64; ++u) m[u] = (on && hh * 64 + u == j) ? 1.0 : 0.0;
+  for (int k = 0; k < b; ++k) {
+    const double* v = rf + k * (b + 1);
+    const double beta = v[b];
+    if (beta == 0.0) continue;
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 64; ++u) {
+      const int i = hh * 64 + u;
+      if (i < b) d[u & 3] = fma(v[i], m[u], d[u & 3]);
+    }
+    double dot = (d[0] + d[1]) + (d[2] + d[3]);
+    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    const double w = beta * dot;
+#pragma unroll
+    for (int u = 0; u < 64; ++u) {
+      const int i = hh * 64 + u;
+      if (i < b) m[u] = fma(-v[i], w, m[u]);
+    }
+  }
+  if (on) {
+#pragma unroll
+    for (int u = 0; u < 64; ++u) {
+      const int i = hh * 64 + u;
+      if (i < b) L[i + (int64_t)j * b] = -m[u];
+    }
+  }
+}

@@ -108,6 +108,7 @@ DeviceCaps& caps() {
     }
     set_max_dyn((const void*)trsm_kernel);
     set_max_dyn((const void*)form_q_kernel);
+    set_max_dyn((const void*)calu_form_negqt_kernel);
     CU_TRY(cudaFuncSetAttribute(trsm_c2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmC2Smem));
     set_max_dyn((const void*)permute_kernel);
     set_max_dyn((const void*)blockrow_kernel);
@@ -505,7 +506,9 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       return;
     }
     if (bsel <= 64 || use_trsm_c2()) {
-      const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
+      // b > 64: 4 column groups per CTA amortise the 133 KB R11 staging
+      const int64_t cpb = bsel <= 64 ? TC_COLS : 4 * TC_COLS;
+      const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
       if (bsel <= 64)
         trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
       else
@@ -1089,10 +1092,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   double* Rsmall = ar.get<double>((size_t)b * b);
   double* refl = ar.get<double>((size_t)b * (b + 1));
   int32_t* perm_small = ar.get<int32_t>(b);
-  // R12 of the final panel QR as a DMMA product (PRRP_CALU_R12_GEMM=1) instead
-  // of the logged reflectors applied row by row (default: measured faster in
-  // the three-stream schedule, 1745 vs 1794 ms at n = 32768, b = 128)
-  static const bool calu_r12_gemm = getenv("PRRP_CALU_R12_GEMM") && atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
+  // R12 of the final panel QR as a DMMA product (default; PRRP_CALU_R12_GEMM=0:
+  // the logged reflectors applied row by row, one warp per row, which holds
+  // the critical stream ~4 ms per panel at n = 32768 while the trailing
+  // update occupies most SMs)
+  static const bool calu_r12_gemm = !getenv("PRRP_CALU_R12_GEMM") || atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
   double* Qneg = ar.get<double>((size_t)b * b);
   const int64_t ld21t = ((m + 7) / 8) * 8;
   double* A21t = ar.get<double>((size_t)b * ld21t);
@@ -1193,6 +1197,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   int32_t* movedb[2] = {B.moved, ar.get<int32_t>(2 * m)};
   int32_t* mcntb = ar.get<int32_t>(2);
   double* Llogb[2] = {Llog, ar.get<double>((size_t)b * ldl)};
+  const int64_t lda12 = std::max<int64_t>(2, ((n + 1) / 2) * 2);           // pivot-row copies, per parity
+  double* a12cb[2] = {ar.get<double>((size_t)b * lda12), ar.get<double>((size_t)b * lda12)};
   double* Lphysb[2] = {Lphys, ar.get<double>((size_t)b * ldl)};
   double* Db[2] = {D, ar.get<double>((size_t)b * b)};
   int32_t* pivb[2] = {piv, ar.get<int32_t>(b)};
@@ -1374,7 +1380,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           // sequential application and this product agree to a few ulps; the
           // reference's own dgemv order is not reproducible either)
           const int64_t ncol = rows - bj;
-          form_q_kernel<<<1, 256, (size_t)bj * bj * 8, sm>>>(refl, bj, bj, Qneg, 1);
+          tend(sm);
+          tbegin(PRRP_K_OTHER, sm);
+          calu_form_negqt_kernel<<<1, 256, (size_t)bj * (bj + 1) * 8, sm>>>(refl, bj, Qneg);
+          tend(sm);
+          tbegin(PRRP_K_PERMUTE, sm);
           calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, sm>>>(
               A, lda, col0, bj, ncol, pos2row + col0 + bj, A21t, ld21t);
           zero2d_kernel<<<(unsigned)std::min<int64_t>(4 * sms, (ncol * bj + 255) / 256), 256, 0, sm>>>(
@@ -1400,7 +1410,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), sm));
         int nblk;
         if (bj <= 64 || use_trsm_c2()) {
-          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TC_COLS - 1) / TC_COLS);
+          const int64_t cpb = bj <= 64 ? TC_COLS : 4 * TC_COLS;
+          nblk = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
           if (bj <= 64)
             trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
           else
@@ -1421,8 +1432,15 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       }
       // L21 (logical order) -> physical slots for the Schur update and the compose
       calu_scatter_l21_kernel<<<sms * 4, 256, 0, sm>>>(Lg, ldl, log2phys, rows - bj, bj, bj, Lp, ldl);
+      // the updates read the pivot rows (A12 before the GEPP finish) from a
+      // copy, so the block row can be finished on the fin stream while the
+      // trailing update is still running
+      double* a12 = a12cb[par];
       if (wn > 0)
-        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lp, ldl, A + col0 * lda + col0 + bj, lda, rows - bj, wn,
+        CU_TRY(cudaMemcpy2DAsync(a12, (size_t)lda12 * 8, A + col0 * lda + col0 + bj, (size_t)lda * 8, (size_t)wn * 8,
+                                 (size_t)bj, cudaMemcpyDeviceToDevice, sm));
+      if (wn > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lp, ldl, a12, lda12, rows - bj, wn,
                      bj, st, sm, calu_narrow_ctas, calu_wide_q);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
@@ -1437,31 +1455,39 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       tbegin(PRRP_K_COMPOSE, sf);
       launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf);
       tend(sf);
-      fin_ev[panel] = ss.ev(evi++);
-      CU_TRY(cudaEventRecord(fin_ev[panel], sf));
-      // side: trailing row moves, trailing update (next narrow region first)
+      // side: trailing row moves + copy of their pivot-row part, trailing
+      // update (next narrow region first)
       CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
       const int64_t cw0 = col0 + bj + wn;
       tbegin(PRRP_K_PERMUTE, sd);
       permute_cols(cw0, n, col0, mv, mc, nullptr, panel, sd);
+      if (n > cw0)
+        CU_TRY(cudaMemcpy2DAsync(a12 + wn, (size_t)lda12 * 8, A + col0 * lda + cw0, (size_t)lda * 8,
+                                 (size_t)(n - cw0) * 8, (size_t)bj, cudaMemcpyDeviceToDevice, sd));
       tend(sd);
+      cudaEvent_t ev_copy = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(ev_copy, sd));
+      // fin: the block row (after every row move of this panel and the copy;
+      // side's permute also orders it after the previous trailing update)
+      CU_TRY(cudaStreamWaitEvent(sf, ev_copy, 0));
+      tbegin(PRRP_K_BLOCKROW, sf);
+      launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sf);
+      tend(sf);
+      CU_TRY(cudaGetLastError());
+      fin_ev[panel] = ss.ev(evi++);
+      CU_TRY(cudaEventRecord(fin_ev[panel], sf));
       const int64_t w1 = std::min<int64_t>(n - cw0, b);
       if (w1 > 0)
-        schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, A + col0 * lda + cw0, lda, rows - bj, w1, bj, st, sd,
+        schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, a12 + wn, lda12, rows - bj, w1, bj, st, sd,
                      calu_wide_ctas, calu_wide_q);
       w1_prev = ss.ev(evi++);
       CU_TRY(cudaEventRecord(w1_prev, sd));
-      // the rest of the trailing update (W2) and the block row: deferred until
-      // the next panel's tournament leaves have run (see pending_side)
-      pending_side = [=, &ss, &evi, &side_done, &side_ev, &fin_ev]() {
+      // the rest of the trailing update (W2): deferred until the next panel's
+      // tournament leaves have run (see pending_side)
+      pending_side = [=, &ss, &evi, &side_done, &side_ev]() {
         if (n - cw0 > w1)
-          schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, A + col0 * lda + cw0 + w1, lda, rows - bj,
+          schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, a12 + wn + w1, lda12, rows - bj,
                        n - cw0 - w1, bj, st, sd, calu_wide_ctas, calu_wide_q, w2_stream);
-        CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel], 0));
-        tbegin(PRRP_K_BLOCKROW, sd);
-        launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sd);
-        tend(sd);
-        CU_TRY(cudaGetLastError());
         side_done = ss.ev(evi++);
         CU_TRY(cudaEventRecord(side_done, sd));
         side_ev[panel] = side_done;
@@ -1470,6 +1496,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       continue;
     } else {
       flush_side(nullptr);
+      if (panel >= 1 && fin_ev[panel - 1]) CU_TRY(cudaStreamWaitEvent(sd, fin_ev[panel - 1], 0));
       // last square block: logical order (all columns, on the side stream, which
       // has seen every earlier update and row move), then GEPP
       tbegin(PRRP_K_OTHER, sd);
@@ -1494,6 +1521,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   }
   flush_side(nullptr);
   CU_TRY(cudaStreamWaitEvent(sm, side_done, 0));
+  for (int k = npanels - 1; k >= 0; --k)      // join the fin stream (its last block row)
+    if (fin_ev[k]) { CU_TRY(cudaStreamWaitEvent(sm, fin_ev[k], 0)); break; }
   {
     cudaEvent_t e1 = ss.ev(evi++);
     CU_TRY(cudaEventRecord(e1, sm));
