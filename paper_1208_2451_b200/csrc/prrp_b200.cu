@@ -1075,7 +1075,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   static const int calu_narrow_ctas = getenv("PRRP_CALU_NARROW") ? atoi(getenv("PRRP_CALU_NARROW")) : 0;
   static const int calu_wide_q = getenv("PRRP_CALU_WIDE_Q") ? atoi(getenv("PRRP_CALU_WIDE_Q")) : 0;
   static const int calu_wide_ctas = getenv("PRRP_CALU_WIDE_CTAS") ? atoi(getenv("PRRP_CALU_WIDE_CTAS"))
-                                                                  : std::max(1, caps().sms - 24);
+                                                                  : std::max(1, caps().sms - 8);
   DevState* st = new_state(ar, s);
   const int64_t ldl = ((m + 7) / 8) * 8;
   double* Lphys = ar.get<double>((size_t)b * ldl);
@@ -1092,10 +1092,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   double* Rsmall = ar.get<double>((size_t)b * b);
   double* refl = ar.get<double>((size_t)b * (b + 1));
   int32_t* perm_small = ar.get<int32_t>(b);
-  // R12 of the final panel QR as a DMMA product (default; PRRP_CALU_R12_GEMM=0:
-  // the logged reflectors applied row by row, one warp per row, which holds
-  // the critical stream ~4 ms per panel at n = 32768 while the trailing
-  // update occupies most SMs)
+  // R12 of the final panel QR as a DMMA product for b > 64 (default;
+  // PRRP_CALU_R12_GEMM=0: the logged reflectors applied row by row, one warp
+  // per row, which holds the critical stream ~4 ms per panel at n = 32768,
+  // b = 128, while the trailing update occupies most SMs; at b = 64 the row
+  // by row form is the faster one, 289 vs 303 ms at n = 16384)
   static const bool calu_r12_gemm = !getenv("PRRP_CALU_R12_GEMM") || atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
   double* Qneg = ar.get<double>((size_t)b * b);
   const int64_t ld21t = ((m + 7) / 8) * 8;
@@ -1218,7 +1219,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   // once, which a running trailing update never hands back; so the bulk of
   // panel k's trailing update (W2) and its block row are enqueued only after
   // panel k+1's leaves (side waits for them), and run as a persistent kernel
-  // on all but 24 SMs, beside the rest of the tournament chain
+  // on all but 8 SMs, beside the rest of the tournament chain
   // (PRRP_CALU_DEFER=0: enqueue at once).
   static const int calu_defer = getenv("PRRP_CALU_DEFER") ? atoi(getenv("PRRP_CALU_DEFER")) : 1;
   std::function<void()> pending_side;
@@ -1374,7 +1375,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
         }
         calu_copy_r11_kernel<<<1, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
-        if (calu_r12_gemm && (bj % 2 == 0)) {
+        if (calu_r12_gemm && bj > 64 && (bj % 2 == 0)) {
           // R12 = Q^T A21^T on the DMMA pipe: Q from the reflector log, A21's
           // rows gathered transposed, C = 0 - (-Q^T) A21^T (the reflectors'
           // sequential application and this product agree to a few ulps; the
