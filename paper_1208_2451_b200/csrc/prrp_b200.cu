@@ -124,7 +124,10 @@ DeviceCaps& caps() {
       set_max_dyn((const void*)fn);
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurPSmem)));
-    CU_TRY(cudaFuncSetAttribute(schur_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurWSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SchurWSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SchurWSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
@@ -594,7 +597,17 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     const unsigned grid = (unsigned)(quantum > 0 ? (tiles + quantum - 1) / quantum : std::min<int64_t>(tiles, max_ctas));
     int* ctr = tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
                         : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);
-    schur_ws_kernel<<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st,
+    // C read in the epilogue (default): the MMA loop then has the registers to
+    // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
+    // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
+    static const bool late_c = !getenv("PRRP_SCHUR_LATE_C") || atoi(getenv("PRRP_SCHUR_LATE_C")) != 0;
+    if (late_c)
+      schur_ws_kernel<false><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K,
+                                                                           vec_ok, st, ctr,
+                                                                           quantum > 0 ? quantum : INT_MAX,
+                                                                           stream_c ? 1 : 0);
+    else
+    schur_ws_kernel<true><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st,
                                                                  ctr, quantum > 0 ? quantum : INT_MAX,
                                                                  stream_c ? 1 : 0);
   } else if (tma_ok && max_ctas > 0 && K <= SP_K) {
@@ -1618,7 +1631,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     CU_TRY(cudaMalloc(&sched, sizeof(int) * 2 * tl_sched_slots));
     np->bufs.push_back(sched);
     CU_TRY(cudaMemset(sched, 0, sizeof(int) * 2 * tl_sched_slots));
-    tl_sched = sched;
+    tl_sched = getenv("PRRP_GRAPH_GLOBAL_SCHED") ? nullptr : sched;
     tl_sched_next = 0;
     cudaGraph_t g = nullptr;
     CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));

@@ -322,6 +322,7 @@ struct SchurWSmem {
   double red[40];
 };
 
+template <bool PC>
 __global__ void __launch_bounds__(SW_THREADS, 1)
 schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
                 double* C, int64_t ldc, int M, int N, int K, int vec_ok, DevState* st, int* ctr, int quantum,
@@ -378,24 +379,27 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
       if (tile < 0) break;
       const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
       double cv[4][4][2];
+      auto load_c = [&]() {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = m0 + wm + i * 8 + fc;
+        for (int i = 0; i < 4; ++i) {
+          const int r = m0 + wm + i * 8 + fc;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c0 = n0 + wn + j * 8 + 2 * fr;
-          const double* cp = C + (int64_t)r * ldc + c0;
-          if (r < M && vec_ok && c0 + 1 < N) {
-            const double2 v = stream_c ? __ldcs(reinterpret_cast<const double2*>(cp))
-                                       : *reinterpret_cast<const double2*>(cp);
-            cv[i][j][0] = v.x;
-            cv[i][j][1] = v.y;
-          } else {
-            cv[i][j][0] = (r < M && c0 < N) ? cp[0] : 0.0;
-            cv[i][j][1] = (r < M && c0 + 1 < N) ? cp[1] : 0.0;
+          for (int j = 0; j < 4; ++j) {
+            const int c0 = n0 + wn + j * 8 + 2 * fr;
+            const double* cp = C + (int64_t)r * ldc + c0;
+            if (r < M && vec_ok && c0 + 1 < N) {
+              const double2 v = stream_c ? __ldcs(reinterpret_cast<const double2*>(cp))
+                                         : *reinterpret_cast<const double2*>(cp);
+              cv[i][j][0] = v.x;
+              cv[i][j][1] = v.y;
+            } else {
+              cv[i][j][0] = (r < M && c0 < N) ? cp[0] : 0.0;
+              cv[i][j][1] = (r < M && c0 + 1 < N) ? cp[1] : 0.0;
+            }
           }
         }
-      }
+      };
+      if (PC) load_c();
       double acc[4][4][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -421,6 +425,7 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
       }
+      if (!PC) load_c();
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = m0 + wm + i * 8 + fc;
@@ -449,3 +454,4 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
     if (atomicAdd(&ctr[1], 1) == (int)gridDim.x - 1) { ctr[0] = 0; ctr[1] = 0; }
   }
 }
+

@@ -240,6 +240,41 @@ def test_caluprrp_single_leaf_equals_luprrp(dev):
     assert np.array_equal(f1.l, f2.l) and np.array_equal(f1.u, f2.u)
 
 
+@pytest.mark.parametrize("n,b", [(4096, 64), (4096, 128)])
+def test_caluprrp_graph_replay_bit_identical(dev, n, b):
+    """The first call captures the factorization into a CUDA graph, later calls
+    replay it (three streams + the node-stream pool, deferred trailing
+    updates): every replay must give the capture's bits, and the factors must
+    reproduce A (schedule races would show up as differing bits)."""
+    import ctypes
+    import torch
+    from paper_1208_2451_b200 import _lib
+    lib = _lib.device_lib()
+    a = orc.randn_matrix(n, 11)
+    lda = n
+    buf = torch.empty((n, lda), dtype=torch.float64, device="cuda")
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    outs = []
+    for _ in range(3):
+        buf.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        npan = (n + b - 1) // b
+        sw = (ctypes.c_int32 * npan)()
+        chg = (ctypes.c_int64 * npan)()
+        st, err = _lib.PrrpStats(), _lib.PrrpErr()
+        rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, 2.0, 8,
+                               ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                               _lib.stream_handle())
+        assert rc == 0, err.msg
+        outs.append((buf.cpu().numpy().copy(), perm.cpu().numpy().copy()))
+    for lu, p in outs[1:]:
+        assert np.array_equal(lu, outs[0][0]) and np.array_equal(p, outs[0][1])
+    lu, p = outs[0]
+    l = np.tril(lu, -1) + np.eye(n)
+    u = np.triu(lu)
+    res = np.linalg.norm(a[p] - l @ u) / np.linalg.norm(a)
+    assert res < n * 2.0 ** -52, res
+
+
 def test_dist_calu_device_ops_single_rank(dev):
     """The distributed orchestration with the device ops (world size 1) agrees
     with the single-call device CALU_PRRP and with the reference algorithm."""
