@@ -588,7 +588,8 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
   // steadier than the warp-specialised one inside the b = 64 LU_PRRP
   // schedule); K > 64 (b = 128): the warp-specialised kernel (70-74% of the
   // DMMA peak on the big updates vs 58-63% for the classic kernel)
-  const bool use_ws = !schur_old && (max_ctas > 0 || quantum > 0) && (K > SP_K || quantum > 0);
+  static const bool ws64 = getenv("PRRP_SCHUR_WS64") && atoi(getenv("PRRP_SCHUR_WS64")) != 0;   // diagnostics
+  const bool use_ws = !schur_old && (max_ctas > 0 || quantum > 0) && (K > SP_K || quantum > 0 || ws64);
   if (tma_ok && use_ws) {
     const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl, SW_KC);
     const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, SW_KC);

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--b", type=int, default=128)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--urand", action="store_true")
+    ap.add_argument("--lu", action="store_true", help="LU_PRRP (prrp_luprrp) instead of CALU_PRRP")
     args = ap.parse_args()
     import torch
     from paper_1208_2451_b200 import _lib, matgen
@@ -32,8 +33,13 @@ def main():
         sw = (ctypes.c_int32 * npan)()
         chg = (ctypes.c_int64 * npan)()
         st, err = _lib.PrrpStats(), _lib.PrrpErr()
-        rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, 2.0, 8, ctypes.c_void_p(perm.data_ptr()),
-                               sw, chg, ctypes.byref(st), ctypes.byref(err), _lib.stream_handle())
+        if args.lu:
+            rc = lib.prrp_luprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, 2.0, ctypes.c_void_p(perm.data_ptr()),
+                                 sw, ctypes.byref(st), ctypes.byref(err), _lib.stream_handle())
+        else:
+            rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, 2.0, 8,
+                                   ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                                   _lib.stream_handle())
         torch.cuda.synchronize()
         _lib.raise_for(rc, err, "caluprrp")
         h = hashlib.sha1(buf[:, :n].contiguous().cpu().numpy().tobytes()).hexdigest()[:12]
