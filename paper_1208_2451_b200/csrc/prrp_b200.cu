@@ -413,7 +413,8 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
 void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel, double tau, int panel,
                        double* L21, int64_t ldl, const PanelBuffers& B, DevState* st, int32_t* swaps_dev,
                        double* D, int32_t* piv, int32_t* gperm, bool do_gepp, cudaStream_t s,
-                       const int64_t* rowidx = nullptr, int swap_slot = -1, int tl = -1, int ti = -1) {
+                       const int64_t* rowidx = nullptr, int swap_slot = -1, int tl = -1, int ti = -1,
+                       cudaEvent_t after_qrcp = nullptr) {
   const PanelCfg g = panel_config(h, p, bsel);
   PanelArgs a{};
   a.src = src;
@@ -492,6 +493,7 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   tend(s);
   CU_TRY(cudaGetLastError());
 
+  if (after_qrcp) CU_TRY(cudaEventRecord(after_qrcp, s));
   const int64_t ncol = p - bsel;
   const int nblk = ncol > 0 ? (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC) : 0;
   if (nblk > 0) {
@@ -596,8 +598,10 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
     const int64_t tiles = ((M + SCH_BM - 1) / SCH_BM) * ((N + SCH_BN - 1) / SCH_BN);
     const unsigned grid = (unsigned)(quantum > 0 ? (tiles + quantum - 1) / quantum : std::min<int64_t>(tiles, max_ctas));
-    int* ctr = tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
-                        : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);
+    static const bool static_claims = getenv("PRRP_SCHUR_STATIC") && atoi(getenv("PRRP_SCHUR_STATIC")) != 0;
+    int* ctr = static_claims ? nullptr
+               : tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
+                          : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);
     // C read in the epilogue (default): the MMA loop then has the registers to
     // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
@@ -1165,6 +1169,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   std::vector<int64_t> charges(npanels, -1);
   std::vector<std::vector<std::pair<int64_t, int>>> node_members(npanels);   // (members, node slot)
 
+  static const int early_w2 = getenv("PRRP_CALU_EARLY_W2") ? atoi(getenv("PRRP_CALU_EARLY_W2")) : 0;   // diagnostics
+  std::vector<cudaEvent_t> leaf_qrcp_ev;
   auto run_level = [&](const std::vector<int64_t>& lo, const std::vector<int64_t>& cnt, bool leaves,
                        int64_t col0, int bj, int panel, int level, int slot0, cudaStream_t qs) {
     // fork
@@ -1177,9 +1183,14 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       CU_TRY(cudaStreamWaitEvent(ns, fk, 0));
       const int64_t* ridx = leaves ? pos2row + col0 + lo[i] : nodes[i].rowidx;
       if (cnt[i] <= bj) continue;                       // node passes its rows through
+      cudaEvent_t qe = nullptr;
+      if (leaves && early_w2) {
+        CU_TRY(cudaEventCreateWithFlags(&qe, cudaEventDisableTiming));
+        leaf_qrcp_ev.push_back(qe);
+      }
       strong_rrqr_panel(A + col0, lda, bj, cnt[i], bj, tau, panel, nodes[i].L21, nodes[i].ldl, nodes[i].B, st,
                         node_swaps + (size_t)panel * maxnodes, nullptr, nullptr, nullptr, false, ns, ridx,
-                        slot0 + i, level, i);
+                        slot0 + i, level, i, qe);
     }
     // join
     for (int i = 0; i < nn; ++i) {
@@ -1296,8 +1307,15 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         calu_leaf_lo_kernel<<<1, 64, 0, sm>>>(leaf_lo_dev, p_eff, rows / p_eff, rows % p_eff);
         int64_t chg3 = 0;
         int slot = 0;
+        leaf_qrcp_ev.clear();
         run_level(lo, cnt, true, col0, bj, panel, 0, slot, sm);
-        flush_after_main();
+        if (early_w2 && pending_side) {
+          for (cudaEvent_t e : leaf_qrcp_ev) CU_TRY(cudaStreamWaitEvent(sd, e, 0));
+          flush_side(nullptr);
+        } else {
+          flush_after_main();
+        }
+        for (cudaEvent_t e : leaf_qrcp_ev) CU_TRY(cudaEventDestroy(e));
         for (int64_t i = 0; i < p_eff; ++i) {
           chg3 += qr_charge3(cnt[i], bj);
           node_members[panel].push_back({cnt[i], slot + (int)i});

@@ -347,7 +347,8 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
     if (lane == 0) {
       uint32_t it = 0;
       for (int claimed = 0;; ++claimed) {
-        int tile = claimed < quantum ? atomicAdd(&ctr[0], 1) : ntiles;
+        int tile = claimed >= quantum ? ntiles
+                   : ctr ? atomicAdd(&ctr[0], 1) : (int)blockIdx.x + claimed * (int)gridDim.x;
         if (tile >= ntiles) tile = -1;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % SW_ST;
@@ -451,7 +452,7 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
   mx = block_max(mx, S.red);
   if (t == 0) {
     if (mx > 0.0) atomic_max_abs(&st->inter_max, mx);
-    if (atomicAdd(&ctr[1], 1) == (int)gridDim.x - 1) { ctr[0] = 0; ctr[1] = 0; }
+    if (ctr && atomicAdd(&ctr[1], 1) == (int)gridDim.x - 1) { ctr[0] = 0; ctr[1] = 0; }
   }
 }
 
