@@ -598,7 +598,10 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
     const int64_t tiles = ((M + SCH_BM - 1) / SCH_BM) * ((N + SCH_BN - 1) / SCH_BN);
     const unsigned grid = (unsigned)(quantum > 0 ? (tiles + quantum - 1) / quantum : std::min<int64_t>(tiles, max_ctas));
-    static const bool static_claims = getenv("PRRP_SCHUR_STATIC") && atoi(getenv("PRRP_SCHUR_STATIC")) != 0;
+    // static tile assignment by default (measured as fast: 1437.6 vs 1437.9 ms
+    // at n = 32768, and it keeps no state across launches); PRRP_SCHUR_DYNAMIC=1
+    // claims tiles from a self-resetting global counter instead
+    static const bool static_claims = !(getenv("PRRP_SCHUR_DYNAMIC") && atoi(getenv("PRRP_SCHUR_DYNAMIC")) != 0);
     int* ctr = static_claims ? nullptr
                : tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
                           : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);

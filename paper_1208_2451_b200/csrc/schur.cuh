@@ -295,10 +295,10 @@ __global__ void __launch_bounds__(256) schur_simt_kernel(const double* L, int64_
   if (threadIdx.x == 0) atomic_max_abs(&st->inter_max, mx);
 }
 
-// Warp-specialised persistent variant for any K: one producer warp claims
-// 128 x 64 tiles from a global counter (dynamic scheduling: a CTA that
-// starts late because a concurrent stream holds its SM simply claims fewer
-// tiles) and streams their K chunks through a SW_ST-deep mbarrier ring
+// Warp-specialised persistent variant for any K: one producer warp walks its
+// 128 x 64 tiles (static: blockIdx.x + i * gridDim.x; or, with ctr != null,
+// claimed from a global counter so that a CTA that starts late because a
+// concurrent stream holds its SM simply claims fewer tiles) and streams their K chunks through a SW_ST-deep mbarrier ring
 // (continuous across tiles, so the next tile's operands are in flight while
 // the current one finishes); the claimed tile id rides in the ring slot of
 // its first chunk.  Eight consumer warps own a 32 x 32 sub-tile each,
