@@ -12,6 +12,8 @@
 #include <functional>
 #include <chrono>
 #include <memory>
+#include <mutex>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <cmath>
@@ -81,7 +83,7 @@ constexpr unsigned kSchedSlots = 1024;
 struct DeviceCaps {
   bool init = false;
   int* sched = nullptr;        // kSchedSlots pairs of tile-claim counters (schur_ws_kernel), self-resetting
-  unsigned sched_next = 0;
+  std::atomic<unsigned> sched_next{0};
   int sms = 0;
   int max_cluster = 8;
 };
@@ -94,8 +96,14 @@ void set_max_dyn(const void* fn) {
                               (int)(kSmemOptin - fa.sharedSizeBytes)));
 }
 
+// Process-wide device setup, done once under a lock (the ABI may be called
+// from several host threads; one device per process, SURVEY 8(b) threading)
+std::mutex g_caps_mu;
 DeviceCaps& caps() {
   static DeviceCaps c;
+  static std::atomic<bool> ready{false};
+  if (ready.load(std::memory_order_acquire)) return c;
+  std::lock_guard<std::mutex> lk(g_caps_mu);
   if (!c.init) {
     int dev = 0;
     CU_TRY(cudaGetDevice(&dev));
@@ -151,6 +159,7 @@ DeviceCaps& caps() {
     CU_TRY(cudaMalloc(&c.sched, kSchedSlots * 2 * sizeof(int)));
     CU_TRY(cudaMemset(c.sched, 0, kSchedSlots * 2 * sizeof(int)));
     c.init = true;
+    ready.store(true, std::memory_order_release);
   }
   return c;
 }
@@ -395,7 +404,7 @@ struct PanelBuffers {
 };
 
 constexpr int kP2MaxGroups = 4;
-unsigned long long g_xepoch = 0;        // per-launch flag epoch of the multi-cluster engine
+std::atomic<unsigned long long> g_xepoch{0};   // per-launch flag epoch of the multi-cluster engine
 void alloc_exchange(Arena& ar, cudaStream_t s, PanelBuffers& B) {
   B.xg = ar.get<double>((size_t)2 * kP2MaxGroups * P2_XS);
   B.xflag = ar.get<unsigned long long>(kP2MaxGroups);
@@ -475,8 +484,7 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
     a2.ngroups = groups;
     a2.xg = B.xg;
     a2.xflag = B.xflag;
-    g_xepoch += 1024;
-    a2.epoch = g_xepoch;
+    a2.epoch = g_xepoch.fetch_add(1024) + 1024;
     launch_clusters(panel_qrcp2_kernel, g2, groups, (size_t)(P2_H - P2_W) * P2_T * 8, s, a2);
   } else if (h == P2_H && p <= (int64_t)P2_T * maxc && aligned && !force_generic_panel()) {
     // thread-per-column split-column engine (h = 128): register window + shared rows
@@ -604,7 +612,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     static const bool static_claims = !(getenv("PRRP_SCHUR_DYNAMIC") && atoi(getenv("PRRP_SCHUR_DYNAMIC")) != 0);
     int* ctr = static_claims ? nullptr
                : tl_sched ? tl_sched + 2 * (tl_sched_next++ % tl_sched_slots)
-                          : caps().sched + 2 * (caps().sched_next++ % kSchedSlots);
+                          : caps().sched + 2 * (caps().sched_next.fetch_add(1) % kSchedSlots);
     // C read in the epilogue (default): the MMA loop then has the registers to
     // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
@@ -1606,6 +1614,8 @@ uint64_t g_plan_clock = 0;
 int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,
                     prrp_err* err, std::chrono::steady_clock::time_point host_t0, Timer* timer);
 
+std::mutex g_plans_mu;   // the plan cache is shared by the host threads of the process
+
 int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
                   int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
   if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
@@ -1628,6 +1638,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   }
   int dev = 0;
   CU_TRY(cudaGetDevice(&dev));
+  std::unique_lock<std::mutex> plans_lock(g_plans_mu);
   auto& plans = calu_plans();
   CaluPlan* pl = nullptr;
   for (auto& q : plans)
@@ -1640,7 +1651,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
                                   [](const std::unique_ptr<CaluPlan>& x, const std::unique_ptr<CaluPlan>& y) {
                                     return x->used < y->used;
                                   });
-      CU_TRY(cudaStreamSynchronize(s));
+      CU_TRY(cudaDeviceSynchronize());   // its graph may be running on another thread's stream
       plans.erase(lru);
     }
     std::unique_ptr<CaluPlan> np(new CaluPlan{A, lda, m, n, b, tau, P, perm, dev});
@@ -1676,7 +1687,9 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   }
   pl->used = ++g_plan_clock;
   CU_TRY(cudaGraphLaunch(pl->exec, s));
-  return caluprrp_finish(pl->out, s, swap_counts, tchg3, stats, err, host_t0, nullptr);
+  const CaluOut out = pl->out;   // a copy: the read-back runs outside the cache lock
+  plans_lock.unlock();
+  return caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, nullptr);
 }
 
 int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,

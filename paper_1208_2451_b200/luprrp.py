@@ -184,7 +184,21 @@ class _Staging:
         return self.bufs, self.stream
 
 
-_staging = _Staging()
+class _ThreadStaging:
+    """One staging pair per host thread (concurrent calls must not share it)."""
+
+    def __init__(self):
+        import threading
+        self.tls = threading.local()
+
+    def get(self):
+        st = getattr(self.tls, "st", None)
+        if st is None:
+            st = self.tls.st = _Staging()
+        return st.get()
+
+
+_staging = _ThreadStaging()
 
 
 def _to_host(dev, out):

@@ -363,3 +363,28 @@ def test_luprrp_solve_and_residual(dev):
     assert 0 < e <= 4 * e_ref + 1e-15 and e_ref <= 4 * e + 1e-15
     with pytest.raises(dev.DimensionMismatch):
         dev.luprrp_solve(f, np.ones(7))
+
+
+def test_concurrent_host_threads(dev):
+    """The ABI is called from several host threads at once (SURVEY 8(b)
+    threading: stream-ordered, reentrant): results equal the serial ones."""
+    import threading
+    mats = [orc.randn_matrix(768, 100 + i) for i in range(4)]
+    serial_lu = [dev.luprrp_factor(a, 64, 2.0) for a in mats[:2]]
+    serial_calu = [dev.caluprrp_factor(a, 64, 2.0) for a in mats[2:]]
+    out = {}
+
+    def work(i):
+        if i < 2:
+            out[i] = dev.luprrp_factor(mats[i], 64, 2.0)
+        else:
+            out[i] = dev.caluprrp_factor(mats[i], 64, 2.0)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i, ref in enumerate(serial_lu + serial_calu):
+        assert np.array_equal(out[i].perm, ref.perm)
+        assert np.array_equal(out[i].l, ref.l) and np.array_equal(out[i].u, ref.u)
