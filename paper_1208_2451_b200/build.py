@@ -22,7 +22,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
     "-Xptxas", "-v",
     "-I" + os.path.join(ROOT, "include"),
-] + (["-DPRRP_P64_PROF"] if os.environ.get("PRRP_P64_PROF") else [])
+] + (["-DPRRP_P64_PROF"] if os.environ.get("PRRP_P64_PROF") else []) + [
+    "-D" + d for d in os.environ.get("PRRP_NVCC_DEFS", "").split(",") if d]
 
 
 def nvcc():

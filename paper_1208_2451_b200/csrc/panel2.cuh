@@ -29,6 +29,10 @@
 #define P2_NW (P2_T / 32)
 #define P2_RS (P2_T * 8)         // shared row stride (bytes)
 #define P2_XS 136                // global exchange slot: 8 record doubles + 128 v
+#ifndef P2_UNR
+#define P2_UNR 1                 // unroll of the shared-memory block loops (ILP across blocks)
+#endif
+constexpr int kP2Unr = P2_UNR;
 
 struct P2Shared {
   double wpub[2][P2_NW][P2_H];
@@ -105,7 +109,7 @@ __device__ __forceinline__ double p2_sumsq(const P2Col& x, int r0, int L) {
       }
     }
   }
-#pragma unroll 1
+#pragma unroll kP2Unr
   for (int B = 8; B <= L; ++B) {
     const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
     double q[8];
@@ -150,7 +154,7 @@ __device__ __forceinline__ void p2_apply(const P2Col& x, const double* vp, doubl
       }
     }
   }
-#pragma unroll 1
+#pragma unroll kP2Unr
   for (int B = 8; B <= L; ++B) {
     const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
 #pragma unroll
@@ -174,7 +178,7 @@ __device__ __forceinline__ void p2_apply(const P2Col& x, const double* vp, doubl
     }
   }
   if (!act) return;
-#pragma unroll 1
+#pragma unroll kP2Unr
   for (int B = 8; B <= L; ++B) {
     const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
 #pragma unroll
@@ -211,7 +215,7 @@ __device__ __forceinline__ void p2_candidate(const P2Col& x, int r, int L, int m
 #pragma unroll
     for (int s = 0; s < 8; s += 2) w2[4 * B + s / 2] = make_double2(x.ld(8 * B + s), x.ld(8 * B + s + 1));
   }
-#pragma unroll 1
+#pragma unroll kP2Unr
   for (int B = 8; B <= L; ++B) {
     const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
 #pragma unroll

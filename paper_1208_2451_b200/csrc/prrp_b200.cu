@@ -519,8 +519,7 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       return;
     }
     if (bsel <= 64 || use_trsm_c2()) {
-      // b > 64: 4 column groups per CTA amortise the 133 KB R11 staging
-      const int64_t cpb = bsel <= 64 ? TC_COLS : 4 * TC_COLS;
+      const int64_t cpb = TC_COLS;
       const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
       if (bsel <= 64)
         trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
@@ -575,6 +574,11 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
   }
 }
 
+thread_local int tl_force_ws = -1;   // diagnostics: per-call kernel choice (PRRP_WS_W1 / PRRP_WS_W2)
+// CALU_PRRP enqueue: the warp-specialised kernel prefetches C (see DESIGN.md 4:
+// with the C read in the epilogue the graph-replayed CALU schedule gave
+// run-to-run different results; with the prefetch it is bit-stable)
+thread_local bool tl_schur_prefetch_c = false;
 // claim counters of a graph plan being captured (its launches own their slots)
 thread_local int* tl_sched = nullptr;
 thread_local unsigned tl_sched_next = 0, tl_sched_slots = 1;
@@ -599,7 +603,8 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
   // schedule); K > 64 (b = 128): the warp-specialised kernel (70-74% of the
   // DMMA peak on the big updates vs 58-63% for the classic kernel)
   static const bool ws64 = getenv("PRRP_SCHUR_WS64") && atoi(getenv("PRRP_SCHUR_WS64")) != 0;   // diagnostics
-  const bool use_ws = !schur_old && (max_ctas > 0 || quantum > 0) && (K > SP_K || quantum > 0 || ws64);
+  bool use_ws = !schur_old && (max_ctas > 0 || quantum > 0) && (K > SP_K || quantum > 0 || ws64);
+  if (tl_force_ws >= 0 && (max_ctas > 0 || quantum > 0)) use_ws = tl_force_ws == 1;   // diagnostics
   if (tma_ok && use_ws) {
     const CUtensorMap mapL = make_map(L, (uint64_t)M, (uint64_t)K, (uint64_t)ldl, SW_KC);
     const CUtensorMap mapB = make_map(Bm, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, SW_KC);
@@ -617,7 +622,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
     static const bool late_c = !getenv("PRRP_SCHUR_LATE_C") || atoi(getenv("PRRP_SCHUR_LATE_C")) != 0;
-    if (late_c)
+    if (late_c && !tl_schur_prefetch_c)
       schur_ws_kernel<false><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K,
                                                                            vec_ok, st, ctr,
                                                                            quantum > 0 ? quantum : INT_MAX,
@@ -1094,6 +1099,9 @@ struct CaluOut {
 // synchronisation, no pageable copies); buffers from `ar`.
 void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
                       cudaStream_t s, Arena& ar, CaluOut& out) {
+  static const bool calu_late_c = getenv("PRRP_CALU_LATE_C") && atoi(getenv("PRRP_CALU_LATE_C")) != 0;
+  tl_schur_prefetch_c = !calu_late_c;
+  struct ResetPf { ~ResetPf() { tl_schur_prefetch_c = false; } } reset_pf;
   const int npanels = (int)((n + b - 1) / b);
   const int maxnodes = 2 * P;
   // Schur launches: the tournament needs whole SMs (16-CTA clusters) at once,
@@ -1454,6 +1462,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaMemsetAsync(fro_inf, 0, sizeof(double), sm));
         int nblk;
         if (bj <= 64 || use_trsm_c2()) {
+          // b > 64, beside the trailing update (few free SMs): 4 column groups
+          // per CTA amortise the 133 KB R11 staging
           const int64_t cpb = bj <= 64 ? TC_COLS : 4 * TC_COLS;
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
           if (bj <= 64)
@@ -1522,16 +1532,26 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       CU_TRY(cudaEventRecord(fin_ev[panel], sf));
       const int64_t w1 = std::min<int64_t>(n - cw0, b);
       if (w1 > 0)
+      {
+        static const int fw1 = getenv("PRRP_WS_W1") ? atoi(getenv("PRRP_WS_W1")) : -1;
+        tl_force_ws = fw1;
         schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, a12 + wn, lda12, rows - bj, w1, bj, st, sd,
                      calu_wide_ctas, calu_wide_q);
+        tl_force_ws = -1;
+      }
       w1_prev = ss.ev(evi++);
       CU_TRY(cudaEventRecord(w1_prev, sd));
       // the rest of the trailing update (W2): deferred until the next panel's
       // tournament leaves have run (see pending_side)
       pending_side = [=, &ss, &evi, &side_done, &side_ev]() {
         if (n - cw0 > w1)
+        {
+          static const int fw2 = getenv("PRRP_WS_W2") ? atoi(getenv("PRRP_WS_W2")) : -1;
+          tl_force_ws = fw2;
           schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, a12 + wn + w1, lda12, rows - bj,
                        n - cw0 - w1, bj, st, sd, calu_wide_ctas, calu_wide_q, w2_stream);
+          tl_force_ws = -1;
+        }
         side_done = ss.ev(evi++);
         CU_TRY(cudaEventRecord(side_done, sd));
         side_ev[panel] = side_done;
@@ -1616,6 +1636,28 @@ int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, in
 
 std::mutex g_plans_mu;   // the plan cache is shared by the host threads of the process
 
+#ifdef PRRP_SCHUR_RACECHECK
+// diagnostics build: the warp-specialised Schur kernel records C elements that
+// changed between the start of their tile and its epilogue
+void racecheck_begin(const double* A, int64_t lda) {
+  static int zeros[2 + 4 * 64] = {0};
+  long long ld = lda;
+  CU_TRY(cudaMemcpyToSymbol(g_racecheck, zeros, sizeof(zeros)));
+  CU_TRY(cudaMemcpyToSymbol(g_race_base, &A, sizeof(A)));
+  CU_TRY(cudaMemcpyToSymbol(g_race_ld, &ld, sizeof(ld)));
+}
+void racecheck_end() {
+  int h[2 + 4 * 64];
+  CU_TRY(cudaMemcpyFromSymbol(h, g_racecheck, sizeof(h)));
+  fprintf(stderr, "[racecheck] %d changed C elements\n", h[0]);
+  for (int i = 0; i < std::min(h[0], 64); ++i)
+    fprintf(stderr, "  row %d col %d (M %d N %d)\n", h[2 + 4 * i], h[3 + 4 * i], h[4 + 4 * i], h[5 + 4 * i]);
+}
+#else
+void racecheck_begin(const double*, int64_t) {}
+void racecheck_end() {}
+#endif
+
 int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
                   int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
   if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
@@ -1625,6 +1667,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
   if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
   caps();
+  racecheck_begin(A, lda);
   const auto host_t0 = std::chrono::steady_clock::now();
   // PRRP_TRACE: record the timing spans (and write the trace file) for CALU too
   if (getenv("PRRP_TRACE") || (getenv("PRRP_GRAPH") && atoi(getenv("PRRP_GRAPH")) == 0)) {
@@ -1679,6 +1722,8 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     }
     tl_sched = nullptr;
     CU_TRY(cudaStreamEndCapture(cs, &g));
+    if (const char* dot = getenv("PRRP_GRAPH_DOT"))   // diagnostics: the captured dependency graph
+      cudaGraphDebugDotPrint(g, dot, cudaGraphDebugDotFlagsVerbose);
     const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) fail(PRRP_ERR_CUDA, "cudaGraphInstantiate failed");
@@ -1708,6 +1753,7 @@ int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, in
   }
   int32_t* swaps_dev = out.swaps_dev;
   int32_t* node_swaps = out.node_swaps;
+  racecheck_end();
   std::vector<int32_t> sw(npanels);
   CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
   std::vector<int32_t> nsw((size_t)npanels * maxnodes);

@@ -309,6 +309,11 @@ __global__ void __launch_bounds__(256) schur_simt_kernel(const double* L, int64_
 // (increasing, from a zero accumulator) and the same epilogue rounding as
 // schur_dmma_kernel: bit-identical results.  ctr[0] (claims) and ctr[1]
 // (finished CTAs) are reset by the last CTA.
+#ifdef PRRP_SCHUR_RACECHECK
+__device__ int g_racecheck[2 + 4 * 64];
+__device__ const double* g_race_base;
+__device__ long long g_race_ld;
+#endif
 #define SW_KC 32
 #define SW_ST 4
 #define SW_CONS 8
@@ -390,17 +395,20 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
             const double* cp = C + (int64_t)r * ldc + c0;
             if (r < M && vec_ok && c0 + 1 < N) {
               const double2 v = stream_c ? __ldcs(reinterpret_cast<const double2*>(cp))
-                                         : *reinterpret_cast<const double2*>(cp);
+                                         : __ldcg(reinterpret_cast<const double2*>(cp));
               cv[i][j][0] = v.x;
               cv[i][j][1] = v.y;
             } else {
-              cv[i][j][0] = (r < M && c0 < N) ? cp[0] : 0.0;
-              cv[i][j][1] = (r < M && c0 + 1 < N) ? cp[1] : 0.0;
+              cv[i][j][0] = (r < M && c0 < N) ? __ldcg(cp) : 0.0;
+              cv[i][j][1] = (r < M && c0 + 1 < N) ? __ldcg(cp + 1) : 0.0;
             }
           }
         }
       };
       if (PC) load_c();
+#ifdef PRRP_SCHUR_RACECHECK
+      if (!PC) load_c();   // early copy, compared with the epilogue's read
+#endif
       double acc[4][4][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -426,7 +434,32 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
       }
-      if (!PC) load_c();
+      if (!PC) {
+#ifdef PRRP_SCHUR_RACECHECK
+        double c0v[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { c0v[i][j][0] = cv[i][j][0]; c0v[i][j][1] = cv[i][j][1]; }
+#endif
+        load_c();
+#ifdef PRRP_SCHUR_RACECHECK
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            for (int h = 0; h < 2; ++h)
+              if (__double_as_longlong(c0v[i][j][h]) != __double_as_longlong(cv[i][j][h])) {
+                const int n_ = atomicAdd(&g_racecheck[0], 1);
+                if (n_ < 64) {
+                  g_racecheck[2 + 4 * n_] = (int)(((C - g_race_base) + 0) / g_race_ld) + m0 + wm + i * 8 + fc;
+                  g_racecheck[3 + 4 * n_] = (int)((C - g_race_base) % g_race_ld) + n0 + wn + j * 8 + 2 * fr + h;
+                  g_racecheck[4 + 4 * n_] = M;
+                  g_racecheck[5 + 4 * n_] = N;
+                }
+              }
+#endif
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = m0 + wm + i * 8 + fc;
