@@ -136,6 +136,8 @@ DeviceCaps& caps() {
                                 (int)sizeof(SchurWSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SchurWCSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
@@ -622,7 +624,12 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
     static const bool late_c = !getenv("PRRP_SCHUR_LATE_C") || atoi(getenv("PRRP_SCHUR_LATE_C")) != 0;
-    if (late_c && !tl_schur_prefetch_c)
+    static const bool wsc = !getenv("PRRP_SCHUR_WSC") || atoi(getenv("PRRP_SCHUR_WSC")) != 0;
+    if (wsc && vec_ok && static_claims && quantum <= 0) {
+      // C staged through shared memory by TMA (read early, registers free)
+      const CUtensorMap mapC = make_map(C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, SCH_BM);
+      schur_wsc_kernel<<<grid, SW_THREADS, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K, st);
+    } else if (late_c && !tl_schur_prefetch_c)
       schur_ws_kernel<false><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K,
                                                                            vec_ok, st, ctr,
                                                                            quantum > 0 ? quantum : INT_MAX,

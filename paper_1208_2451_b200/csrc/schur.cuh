@@ -489,3 +489,144 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
   }
 }
 
+
+// Warp-specialised variant with C staged through shared memory by TMA: at the
+// start of each tile consumer thread 0 (after a consumer-only barrier that
+// retires the previous tile's reads of the buffer) loads the tile's C into a
+// 64 KB buffer ([8-column group][128 rows][8]); the epilogue reads it from
+// shared memory.  C is thus read early (like the register prefetch) while the
+// registers stay free for the MMA loop (like the epilogue read).  Three operand
+// stages (144 KB) + C (64 KB).  Same fragments, k order and epilogue rounding
+// as schur_ws_kernel (bit-identical).
+#define SWC_ST 3
+struct SchurWCSmem {
+  double a[SWC_ST][SCH_BM * SW_KC];
+  double b[SWC_ST][SCH_BN * SW_KC];
+  double c[SCH_BN / 8][SCH_BM * 8];
+  unsigned long long full[SWC_ST];
+  unsigned long long empty[SWC_ST];
+  unsigned long long cfull;
+  int tile[SWC_ST];
+  double red[40];
+};
+
+__device__ __forceinline__ void consumers_sync() {   // named barrier 1 over the 8 consumer warps
+  asm volatile("bar.sync 1, %0;" :: "n"(SW_CONS * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(SW_THREADS, 1)
+schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
+                 const __grid_constant__ CUtensorMap mapC, double* C, int64_t ldc, int M, int N, int K,
+                 DevState* st) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  SchurWCSmem& S = *reinterpret_cast<SchurWCSmem*>(sbuf);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ntN = (N + SCH_BN - 1) / SCH_BN, ntM = (M + SCH_BM - 1) / SCH_BM;
+  const int ntiles = prrp_failed(st) ? 0 : ntM * ntN;
+  const int nk = (K + SW_KC - 1) / SW_KC;
+  constexpr uint32_t kStageBytes = (SCH_BM + SCH_BN) * SW_KC * 8;
+  constexpr uint32_t kCBytes = SCH_BM * SCH_BN * 8;
+  if (t == 0) {
+    for (int s = 0; s < SWC_ST; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], SW_CONS); }
+    mbar_init(&S.cfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapL) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&mapC) : "memory");
+  }
+  __syncthreads();
+  double mx = 0.0;
+  if (warp == SW_CONS) {
+    // ---- producer (static tiles)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int claimed = 0;; ++claimed) {
+        int tile = (int)blockIdx.x + claimed * (int)gridDim.x;
+        if (tile >= ntiles) tile = -1;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % SWC_ST;
+          if (it >= SWC_ST) mbar_wait(&S.empty[s], ((it / SWC_ST) & 1) ^ 1);
+          if (kc == 0) {
+            *reinterpret_cast<volatile int*>(&S.tile[s]) = tile;
+            if (tile < 0) { mbar_arrive(&S.full[s]); break; }
+          }
+          const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+          mbar_expect_tx(&S.full[s], kStageBytes);
+#pragma unroll 1
+          for (int g = 0; g < SCH_BM / 8; ++g)
+            tma_load_2d(&S.a[s][g * SW_KC * 8], &mapL, &S.full[s], m0 + 8 * g, kc * SW_KC);
+#pragma unroll 1
+          for (int g = 0; g < SCH_BN / 8; ++g)
+            tma_load_2d(&S.b[s][g * SW_KC * 8], &mapB, &S.full[s], n0 + 8 * g, kc * SW_KC);
+        }
+        if (tile < 0) break;
+      }
+    }
+  } else {
+    // ---- consumers
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int fr = lane & 3, fc = lane >> 2;
+    uint32_t it = 0, ntile = 0;
+    for (;; ++ntile) {
+      mbar_wait(&S.full[it % SWC_ST], (it / SWC_ST) & 1);
+      const int tile = *reinterpret_cast<volatile int*>(&S.tile[it % SWC_ST]);
+      if (tile < 0) break;
+      const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
+      consumers_sync();          // every consumer finished reading the previous tile's C
+      if (t == 0) {
+        mbar_expect_tx(&S.cfull, kCBytes);
+#pragma unroll 1
+        for (int g = 0; g < SCH_BN / 8; ++g) tma_load_2d(&S.c[g][0], &mapC, &S.cfull, n0 + 8 * g, m0);
+      }
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = it % SWC_ST;
+        if (kc > 0) mbar_wait(&S.full[s], (it / SWC_ST) & 1);
+        const double* sa = S.a[s];
+        const double* sb = S.b[s];
+#pragma unroll
+        for (int k4 = 0; k4 < SW_KC; k4 += 4) {
+          double af[4], bf[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SW_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+      }
+      mbar_wait(&S.cfull, ntile & 1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rl = wm + i * 8 + fc, r = m0 + rl;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int cl = wn + j * 8 + 2 * fr, c0 = n0 + cl;
+          const double2 cv = *reinterpret_cast<const double2*>(&S.c[cl >> 3][rl * 8 + (cl & 7)]);
+          const double v0 = sub_rn(cv.x, acc[i][j][0]);
+          const double v1 = sub_rn(cv.y, acc[i][j][1]);
+          if (r < M) {
+            double* crow = C + (int64_t)r * ldc;
+            if (c0 + 1 < N) {
+              *reinterpret_cast<double2*>(crow + c0) = make_double2(v0, v1);
+              mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+            } else if (c0 < N) {
+              crow[c0] = v0;
+              mx = fmax(mx, fabs(v0));
+            }
+          }
+        }
+      }
+    }
+  }
+  mx = block_max(mx, S.red);
+  if (t == 0 && mx > 0.0) atomic_max_abs(&st->inter_max, mx);
+}
