@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .errors import DimensionMismatch
 from .luprrp import (BlockLUFactors, ElimStats, _validate, as_matrix, flop_counters,
-                     split_packed_device, upload, _Prefault)
+                     split_packed_device, split_to_host, upload, _Prefault)
 
 
 @dataclass(frozen=True)
@@ -226,5 +226,5 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
                       finish_max=st.finish_max, swap_counts=list(map(int, swaps)),
                       flops_charged=charged, flops_executed=executed,
                       panel_multiplier_max=st.panel_multiplier_max)
-    l, u = split_packed_device(buf[:, :n], m, n, out=pre.get() if pre else None)
+    l, u = split_to_host(buf[:, :n], m, n, *pre.get()) if pre else split_packed_device(buf[:, :n], m, n)
     return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b, stats=stats)
