@@ -1433,7 +1433,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
         }
         calu_copy_r11_kernel<<<1, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
-        if (calu_r12_gemm && bj > 64 && (bj % 2 == 0)) {
+        static const int r12_min_b = getenv("PRRP_CALU_R12_MIN_B") ? atoi(getenv("PRRP_CALU_R12_MIN_B")) : 65;
+        if (calu_r12_gemm && bj >= r12_min_b && (bj % 2 == 0)) {
           // R12 = Q^T A21^T on the DMMA pipe: Q from the reflector log, A21's
           // rows gathered transposed, C = 0 - (-Q^T) A21^T (the reflectors'
           // sequential application and this product agree to a few ulps; the
