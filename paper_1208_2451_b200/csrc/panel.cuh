@@ -70,6 +70,7 @@ struct PanelArgs {
   double* xg;               // 2 x ngroups x P2_XS doubles (step-parity slots)
   unsigned long long* xflag;   // ngroups flags: epoch + k + 1 once group g published step k
   unsigned long long epoch;
+  int fused_ak;             // panel2: fused apply + next-key pass over the shared rows
 };
 
 struct Rec {

@@ -191,9 +191,108 @@ __device__ __forceinline__ void p2_apply(const P2Col& x, const double* vp, doubl
   }
 }
 
+// apply reflector k and compute the next key (p2_sumsq of the relative rows
+// r0 .. 8L+7) in one pass over the shared rows, for L >= 8 (shared rows
+// present): the register rows are updated and squared first, then every
+// shared row is loaded once, updated, stored and squared, so the pairwise
+// accumulation order is p2_sumsq's (blocks in increasing order).
+__device__ __forceinline__ double p2_apply_key(const P2Col& x, const double* vp, double beta, bool act,
+                                               bool do_apply, int L, int r0) {
+  const uint32_t va = (uint32_t)__cvta_generic_to_shared(vp);
+  double nw = 0.0;
+  if (do_apply) {
+    double d[4];
+#pragma unroll
+    for (int B = 0; B < 8; ++B) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = lds2_f64(va + 64 * B + 16 * h);
+        const int s = 2 * h;
+        if (B == 0 && s < 4) {
+          d[s] = mul_rn(v.x, x.ld(s));
+          d[s + 1] = mul_rn(v.y, x.ld(s + 1));
+        } else {
+          d[s & 3] = fma(v.x, x.ld(8 * B + s), d[s & 3]);
+          d[(s + 1) & 3] = fma(v.y, x.ld(8 * B + s + 1), d[(s + 1) & 3]);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int B = 8; B <= L; ++B) {
+      const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = lds2_f64(va + 64 * B + 16 * h);
+        d[(2 * h) & 3] = fma(v.x, lds_f64(a + (uint32_t)(2 * h) * P2_RS), d[(2 * h) & 3]);
+        d[(2 * h + 1) & 3] = fma(v.y, lds_f64(a + (uint32_t)(2 * h + 1) * P2_RS), d[(2 * h + 1) & 3]);
+      }
+    }
+    const double dot = (d[0] + d[1]) + (d[2] + d[3]);
+    nw = act ? -mul_rn(beta, dot) : 0.0;
+#pragma unroll
+    for (int B = 0; B < 8; ++B) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = lds2_f64(va + 64 * B + 16 * h);
+        const int s = 8 * B + 2 * h;
+        x.r[s] = fma(v.x, nw, x.r[s]);
+        x.r[s + 1] = fma(v.y, nw, x.r[s + 1]);
+      }
+    }
+  }
+  const bool upd = do_apply && act;
+  double S[8], T[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const double q = sq_rn(x.ld(s));
+    S[s] = s >= r0 ? q : 0.0;
+    T[s] = 0.0;
+  }
+#pragma unroll
+  for (int B = 1; B < 8; ++B)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) S[s] = add_rn(S[s], sq_rn(x.ld(8 * B + s)));
+#pragma unroll 1
+  for (int B = 8; B <= L; ++B) {
+    const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
+    double q[8];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t a0 = a + (uint32_t)(2 * h) * P2_RS;
+      double x0 = lds_f64(a0), x1 = lds_f64(a0 + P2_RS);
+      if (upd) {
+        const double2 v = lds2_f64(va + 64 * B + 16 * h);
+        x0 = fma(v.x, nw, x0);
+        x1 = fma(v.y, nw, x1);
+        sts_f64(a0, x0);
+        sts_f64(a0 + P2_RS, x1);
+      }
+      q[2 * h] = sq_rn(x0);
+      q[2 * h + 1] = sq_rn(x1);
+    }
+    if (B < L) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) S[s] = add_rn(S[s], q[s]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        T[s] = q[s];
+        if (s < r0) S[s] = add_rn(S[s], T[s]);
+      }
+    }
+  }
+  double res = p1_combine(S, r0 & 7);
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s >= r0) res = add_rn(res, T[s]);
+  return res;
+}
+
 // the warp's best column builds its reflector (p1_candidate for the split column)
+// (copy_smem = false: the shared-memory rows of v are copied by the whole warp
+// afterwards, p2_copy_smem_rows)
 __device__ __forceinline__ void p2_candidate(const P2Col& x, int r, int L, int mode, double key, double* wp,
-                                             int& skip, double& alpha, double& beta) {
+                                             int& skip, double& alpha, double& beta, bool copy_smem = true) {
   double xk = x.ld(0);
 #pragma unroll
   for (int s = 1; s < 8; ++s)
@@ -215,17 +314,26 @@ __device__ __forceinline__ void p2_candidate(const P2Col& x, int r, int L, int m
 #pragma unroll
     for (int s = 0; s < 8; s += 2) w2[4 * B + s / 2] = make_double2(x.ld(8 * B + s), x.ld(8 * B + s + 1));
   }
+  if (copy_smem) {
 #pragma unroll kP2Unr
-  for (int B = 8; B <= L; ++B) {
-    const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
+    for (int B = 8; B <= L; ++B) {
+      const uint32_t a = x.sb + (uint32_t)(8 * B - P2_W) * P2_RS;
 #pragma unroll
-    for (int s = 0; s < 8; s += 2)
-      w2[4 * B + s / 2] = make_double2(lds_f64(a + (uint32_t)s * P2_RS), lds_f64(a + (uint32_t)(s + 1) * P2_RS));
+      for (int s = 0; s < 8; s += 2)
+        w2[4 * B + s / 2] = make_double2(lds_f64(a + (uint32_t)s * P2_RS), lds_f64(a + (uint32_t)(s + 1) * P2_RS));
+    }
   }
   const double half_vtv = mul_rn(normx, add_rn(normx, fabs(xk)));
   beta = skip ? 0.0 : __drcp_rn(half_vtv);
   if (half_vtv == 0.0) skip = 1;
   if (skip) { alpha = xk; beta = 0.0; }
+}
+
+// the shared-memory rows (relative 64 .. 8L+7) of thread tw's column into v,
+// one row per lane (sb0 = shared address of row 8*KB of thread 0's column)
+__device__ __forceinline__ void p2_copy_smem_rows(uint32_t sb0, int tw, int L, double* wp, int lane) {
+  for (int i = P2_W + lane; i < 8 * (L + 1); i += 32)
+    wp[i] = lds_f64(sb0 + (uint32_t)(i - P2_W) * P2_RS + (uint32_t)tw * 8);
 }
 
 __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
@@ -291,6 +399,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
     S.fro = f;
   }
   const bool log_refl = a.refl != nullptr && c == 0;
+  const bool fused_ak = a.fused_ak != 0;
   // PRRP_PANEL_PROF=1 PRRP_PANEL_TL=<panel>: clock64 marks of thread 0 of CTA 0
   long long* tl = (a.prof && grp == 0 && c == 0 && t == 0 && a.panel_id == a.prof[6]) ? a.prof + 8 : nullptr;
 #define P2_TL(m) if (tl) tl[k * 8 + (m)] = clock64();
@@ -330,12 +439,17 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       P1Rec& wr = S.wrec[buf][warp];
       if (wl < 0) {
         if (lane == 0) { wr.key = -INFINITY; wr.pos = LLONG_MAX; wr.jl = -1; wr.skip = 1; }
-      } else if (lane == wl) {
-        int skip;
-        double alpha, beta;
-        p2_candidate(x, r, L, mode, key, S.wpub[buf][warp], skip, alpha, beta);
-        wr.key = key; wr.pos = pos; wr.jl = t;
-        wr.skip = skip; wr.alpha = alpha; wr.beta = beta;
+      } else {
+        if (lane == wl) {
+          int skip;
+          double alpha, beta;
+          p2_candidate(x, r, L, mode, key, S.wpub[buf][warp], skip, alpha, beta, false);
+          wr.key = key; wr.pos = pos; wr.jl = t;
+          wr.skip = skip; wr.alpha = alpha; wr.beta = beta;
+        }
+        if (L >= 8)
+          p2_copy_smem_rows((uint32_t)__cvta_generic_to_shared(sdata) + (uint32_t)(8 * KB) * P2_RS, warp * 32 + wl,
+                            L, S.wpub[buf][warp], lane);
       }
       __syncwarp();
     }
@@ -512,12 +626,18 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
       const bool live = on && pos >= k;
       const bool win = live && mine && wjl == t;
       if (live && !win && pos == k) pos = wpos;
-      if (!skip) p2_apply(x, vs, beta, live && !win, L);
-      if (win) pos = k;
-      if (mode == 0) {
+      if (mode == 0 && L >= 8 && fused_ak) {
+        const double nk = p2_apply_key(x, vs, beta, live && !win, !skip, L, r + 1);
+        if (win) pos = k;
+        key = (live && !win) ? nk : -1.0;
+      } else if (mode == 0) {
+        if (!skip) p2_apply(x, vs, beta, live && !win, L);
+        if (win) pos = k;
         const double nk = p2_sumsq(x, r + 1, L);
         key = (live && !win) ? nk : -1.0;
       } else {
+        if (!skip) p2_apply(x, vs, beta, live && !win, L);
+        if (win) pos = k;
         key = (live && pos == k + 1) ? 1.0 : -1.0;
       }
     }

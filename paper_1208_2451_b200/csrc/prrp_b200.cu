@@ -456,6 +456,8 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.moved = B.moved;
   a.moved_cnt = B.moved_cnt;
   a.prof = tl_prof;
+  static const int fused_ak = getenv("PRRP_P2_FUSED") ? atoi(getenv("PRRP_P2_FUSED")) : 1;
+  a.fused_ak = fused_ak;
   tbegin(PRRP_K_PANEL, s);
   const int maxc = caps().max_cluster;
   // CTAs: enough for the columns (one per thread in registers, a second in
