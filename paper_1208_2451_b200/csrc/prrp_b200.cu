@@ -136,7 +136,11 @@ DeviceCaps& caps() {
                                 (int)sizeof(SchurWSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWSmem)));
-    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SchurWCSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SchurWCSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWCSmem)));
     // largest cluster the panel engine can get with a full shared-memory CTA per SM
     for (int cs : {16, 8}) {
@@ -630,7 +634,15 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     if (wsc && vec_ok && static_claims && quantum <= 0) {
       // C staged through shared memory by TMA (read early, registers free)
       const CUtensorMap mapC = make_map(C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, SCH_BM);
-      schur_wsc_kernel<<<grid, SW_THREADS, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K, st);
+      static const int wsc_warps = getenv("PRRP_SCHUR_WSC_WARPS") ? atoi(getenv("PRRP_SCHUR_WSC_WARPS")) : 8;
+      if (wsc_warps == 4)
+        schur_wsc_kernel<4><<<grid, 5 * 32, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K, st);
+      else if (wsc_warps == 16)
+        schur_wsc_kernel<16><<<grid, 17 * 32, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K,
+                                                                         st);
+      else
+        schur_wsc_kernel<8><<<grid, SW_THREADS, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K,
+                                                                          st);
     } else if (late_c && !tl_schur_prefetch_c)
       schur_ws_kernel<false><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K,
                                                                            vec_ok, st, ctr,

@@ -510,14 +510,19 @@ struct SchurWCSmem {
   double red[40];
 };
 
-__device__ __forceinline__ void consumers_sync() {   // named barrier 1 over the 8 consumer warps
-  asm volatile("bar.sync 1, %0;" :: "n"(SW_CONS * 32) : "memory");
+template <int NCW>
+__device__ __forceinline__ void consumers_sync() {   // named barrier 1 over the consumer warps
+  asm volatile("bar.sync 1, %0;" :: "n"(NCW * 32) : "memory");
 }
 
-__global__ void __launch_bounds__(SW_THREADS, 1)
+// NCW consumer warps with 32 x (512 / NCW) warp tiles: 16, 8 (the default,
+// measured best: 78% of the DMMA peak) or 4 (61%)
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
 schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapC, double* C, int64_t ldc, int M, int N, int K,
                  DevState* st) {
+  constexpr int NJ = NCW == 16 ? 2 : NCW == 8 ? 4 : 8;   // 8-column fragments per warp
   extern __shared__ __align__(128) unsigned char sbuf[];
   SchurWCSmem& S = *reinterpret_cast<SchurWCSmem*>(sbuf);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -527,7 +532,7 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
   constexpr uint32_t kStageBytes = (SCH_BM + SCH_BN) * SW_KC * 8;
   constexpr uint32_t kCBytes = SCH_BM * SCH_BN * 8;
   if (t == 0) {
-    for (int s = 0; s < SWC_ST; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], SW_CONS); }
+    for (int s = 0; s < SWC_ST; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], NCW); }
     mbar_init(&S.cfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(&mapL) : "memory");
@@ -536,7 +541,7 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
   }
   __syncthreads();
   double mx = 0.0;
-  if (warp == SW_CONS) {
+  if (warp == NCW) {
     // ---- producer (static tiles)
     if (lane == 0) {
       uint32_t it = 0;
@@ -564,7 +569,7 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
     }
   } else {
     // ---- consumers
-    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * (8 * NJ);
     const int fr = lane & 3, fc = lane >> 2;
     uint32_t it = 0, ntile = 0;
     for (;; ++ntile) {
@@ -572,17 +577,17 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
       const int tile = *reinterpret_cast<volatile int*>(&S.tile[it % SWC_ST]);
       if (tile < 0) break;
       const int m0 = (tile / ntN) * SCH_BM, n0 = (tile % ntN) * SCH_BN;
-      consumers_sync();          // every consumer finished reading the previous tile's C
+      consumers_sync<NCW>();     // every consumer finished reading the previous tile's C
       if (t == 0) {
         mbar_expect_tx(&S.cfull, kCBytes);
 #pragma unroll 1
         for (int g = 0; g < SCH_BN / 8; ++g) tma_load_2d(&S.c[g][0], &mapC, &S.cfull, n0 + 8 * g, m0);
       }
-      double acc[4][4][2];
+      double acc[4][NJ][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       for (int kc = 0; kc < nk; ++kc, ++it) {
         const int s = it % SWC_ST;
         if (kc > 0) mbar_wait(&S.full[s], (it / SWC_ST) & 1);
@@ -590,15 +595,15 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
         const double* sb = S.b[s];
 #pragma unroll
         for (int k4 = 0; k4 < SW_KC; k4 += 4) {
-          double af[4], bf[4];
+          double af[4], bf[NJ];
 #pragma unroll
           for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SW_KC + k4 + fr) * 8 + fc];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
+          for (int j = 0; j < NJ; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
@@ -608,7 +613,7 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
       for (int i = 0; i < 4; ++i) {
         const int rl = wm + i * 8 + fc, r = m0 + rl;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           const int cl = wn + j * 8 + 2 * fr, c0 = n0 + cl;
           const double2 cv = *reinterpret_cast<const double2*>(&S.c[cl >> 3][rl * 8 + (cl & 7)]);
           const double v0 = sub_rn(cv.x, acc[i][j][0]);
