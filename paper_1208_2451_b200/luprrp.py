@@ -9,6 +9,7 @@ the reference's charging rules (luprrp.py:135-140, 168-197).
 """
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -271,6 +272,38 @@ class _Prefault:
         return self.arrays
 
 
+_POOL = None
+
+
+def _host_pool_workers():
+    return range(min(16, max(2, (os.cpu_count() or 8) // 2)))
+
+
+def _host_pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=len(_host_pool_workers()), thread_name_prefix="prrp-host")
+    return _POOL
+
+
+def _split_rows(blk, l_out, u_out, j0, r0, r1, m):
+    """Rows r0..r1 (of the chunk starting at packed column j0) into the
+    triangles: row j of U^T takes packed column j up to the diagonal, row j
+    of L^T the part below it and the unit diagonal.  Four block copies (numpy
+    releases the GIL while copying)."""
+    b = blk[r0 - j0:r1 - j0]
+    if r0 > 0:
+        u_out[r0:r1, :r0] = b[:, :r0]
+    sq = b[:, r0:r1]
+    u_out[r0:r1, r0:r1] = np.tril(sq)
+    lsq = np.triu(sq, 1)
+    np.fill_diagonal(lsq, 1.0)
+    l_out[r0:r1, r0:r1] = lsq
+    if r1 < m:
+        l_out[r0:r1, r1:] = b[:, r1:]
+
+
 def split_to_host(packed, m, n, l_out, u_out):
     """Packed L\\U (device, row-major m x n) -> the caller's zero-filled host
     arrays l_out (n x m, = L^T) and u_out (n x n, = U^T).  One device
@@ -299,6 +332,10 @@ def split_to_host(packed, m, n, l_out, u_out):
             ev.record(cs)
         pending.append((i, k, ev))
 
+    import os
+    import time
+    prof = os.environ.get("PRRP_SPLIT_PROF")
+    t_wait = t_host = 0.0
     nxt = 0
     while nxt < len(chunks) and nxt < nb - 1:
         issue(nxt)
@@ -308,18 +345,23 @@ def split_to_host(packed, m, n, l_out, u_out):
         if nxt < len(chunks):
             issue(nxt)
             nxt += 1
+        t0 = time.perf_counter()
         ev.synchronize()
+        t1 = time.perf_counter()
+        t_wait += t1 - t0
         j0, j1 = chunks[i]
-        blk = bufs[k][:(j1 - j0) * m].view(j1 - j0, m)
-        if j0 > 0:
-            ut[j0:j1, :j0].copy_(blk[:, :j0])
-        sq = blk[:, j0:j1]
-        ut[j0:j1, j0:j1].copy_(torch.tril(sq))
-        lsq = torch.triu(sq, 1)
-        lsq.diagonal().fill_(1.0)
-        lt[j0:j1, j0:j1].copy_(lsq)
-        if j1 < m:
-            lt[j0:j1, j1:].copy_(blk[:, j1:])
+        blk = bufs[k][:(j1 - j0) * m].numpy().reshape(j1 - j0, m)
+        # rows of the chunk split over the host pool (numpy copies release the GIL)
+        nw = len(_host_pool_workers())
+        step = (j1 - j0 + nw - 1) // nw
+        futs = [_host_pool().submit(_split_rows, blk, l_out, u_out, j0, r0, min(j1, r0 + step), m)
+                for r0 in range(j0, j1, step)]
+        for f in futs:
+            f.result()
+        t_host += time.perf_counter() - t1
+    if prof:
+        print(f"[split_to_host] {len(chunks)} chunks: DMA wait {1e3 * t_wait:.1f} ms, host writes {1e3 * t_host:.1f} ms",
+              flush=True)
     return l_out.T, u_out.T
 
 
