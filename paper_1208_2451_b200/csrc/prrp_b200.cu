@@ -844,21 +844,27 @@ Streams& streams() {
 }
 
 // ---------------------------------------------------------------- LU_PRRP driver
-int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm,
-                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, prrp_timing* timing, cudaStream_t s) {
-  Timer timer;
-  tl_timer = timing ? &timer : nullptr;
-  tl_schur_flops = 0.0;
-  struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
-  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
-  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
-  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
-  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
-  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
-  caps();
-  const auto host_t0 = std::chrono::steady_clock::now();
+constexpr size_t kMaxPlans = 4;   // cached graph plans per kind (LU_PRRP, CALU_PRRP)
+// Graph kernel nodes carry the priority of the stream they were captured on;
+// it only applies when the graph is instantiated with UseNodePriority (else the
+// whole graph runs at the launch stream's priority and the critical stream
+// loses its precedence over the trailing update).  PRRP_GRAPH_NODE_PRIO=0: off.
+unsigned long long graph_instantiate_flags() {
+  static const bool use = !(getenv("PRRP_GRAPH_NODE_PRIO") && atoi(getenv("PRRP_GRAPH_NODE_PRIO")) == 0);
+  return use ? (unsigned long long)cudaGraphInstantiateFlagUseNodePriority : 0ull;
+}
+
+struct LuOut {
+  DevState* st = nullptr;
+  int32_t* swaps_dev = nullptr;
+  int npanels = 0;
+};
+
+// Enqueue one LU_PRRP factorization on stream s (capturable unless the
+// panel profiler is on); buffers from `ar`.
+void luprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm, cudaStream_t s,
+                    Arena& ar, LuOut& out) {
   const int npanels = (int)((n + b - 1) / b);
-  Arena ar(s);
   DevState* st = new_state(ar, s);
   const int64_t ldl = ((m + 7) / 8) * 8;
   double* L21 = ar.get<double>((size_t)b * ldl);
@@ -1037,9 +1043,111 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     CU_TRY(cudaEventRecord(e1, sm));
     CU_TRY(cudaStreamWaitEvent(s, e1, 0));
   }
+  out.st = st;
+  out.swaps_dev = swaps_dev;
+  out.npanels = npanels;
+}
+
+// A captured LU_PRRP factorization (see CaluPlan): the direct enqueue of the
+// ~7600 launches costs the GPU launch gaps on the critical stream
+struct LuPlan {
+  double* A; int64_t lda, m, n; int b; double tau; int64_t* perm; int dev;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> bufs;
+  LuOut out;
+  uint64_t used = 0;
+  ~LuPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+std::vector<std::unique_ptr<LuPlan>>& lu_plans() {
+  static std::vector<std::unique_ptr<LuPlan>> v;
+  return v;
+}
+std::mutex g_lu_plans_mu;
+uint64_t g_lu_plan_clock = 0;
+
+int luprrp_finish(const LuOut& out, cudaStream_t s, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
+                  prrp_timing* timing, Timer* timer, std::chrono::steady_clock::time_point host_t0);
+
+int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int64_t* perm,
+                int32_t* swap_counts, prrp_stats* stats, prrp_err* err, prrp_timing* timing, cudaStream_t s) {
+  Timer timer;
+  tl_timer = timing ? &timer : nullptr;
+  tl_schur_flops = 0.0;
+  struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
+  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+  if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  caps();
+  const auto host_t0 = std::chrono::steady_clock::now();
+  // graph replay is opt-in for LU_PRRP (PRRP_LU_GRAPH=1): its host enqueue
+  // (~6.5 ms) is far shorter than the GPU work, and the replayed schedule was
+  // measured slower (44-49 vs 42-43 ms at n = 8192, b = 64; 56.7 vs 53.3 ms at
+  // b = 128) even with per-node priorities
+  static const bool lu_graph = !(getenv("PRRP_GRAPH") && atoi(getenv("PRRP_GRAPH")) == 0) &&
+                               getenv("PRRP_LU_GRAPH") && atoi(getenv("PRRP_LU_GRAPH")) != 0;
+  if (timing || panel_prof_enabled() || !lu_graph) {
+    Arena ar(s);
+    LuOut out;
+    luprrp_enqueue(A, lda, m, n, b, tau, perm, s, ar, out);
+    return luprrp_finish(out, s, swap_counts, stats, err, timing, &timer, host_t0);
+  }
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  std::unique_lock<std::mutex> plans_lock(g_lu_plans_mu);
+  auto& plans = lu_plans();
+  LuPlan* pl = nullptr;
+  for (auto& q : plans)
+    if (q->A == A && q->lda == lda && q->m == m && q->n == n && q->b == b && q->tau == tau && q->perm == perm &&
+        q->dev == dev)
+      pl = q.get();
+  if (!pl) {
+    if (plans.size() >= kMaxPlans) {
+      auto lru = std::min_element(plans.begin(), plans.end(),
+                                  [](const std::unique_ptr<LuPlan>& x, const std::unique_ptr<LuPlan>& y) {
+                                    return x->used < y->used;
+                                  });
+      CU_TRY(cudaDeviceSynchronize());
+      plans.erase(lru);
+    }
+    std::unique_ptr<LuPlan> np(new LuPlan{A, lda, m, n, b, tau, perm, dev});
+    static thread_local cudaStream_t cs = nullptr;
+    if (!cs) CU_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    CU_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    try {
+      Arena ar(cs, &np->bufs);
+      luprrp_enqueue(A, lda, m, n, b, tau, perm, cs, ar, np->out);
+    } catch (...) {
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CU_TRY(cudaStreamEndCapture(cs, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, graph_instantiate_flags());
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) fail(PRRP_ERR_CUDA, "cudaGraphInstantiate failed");
+    plans.push_back(std::move(np));
+    pl = plans.back().get();
+  }
+  pl->used = ++g_lu_plan_clock;
+  CU_TRY(cudaGraphLaunch(pl->exec, s));
+  const LuOut out = pl->out;
+  plans_lock.unlock();
+  return luprrp_finish(out, s, swap_counts, stats, err, nullptr, nullptr, host_t0);
+}
+
+int luprrp_finish(const LuOut& out, cudaStream_t s, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
+                  prrp_timing* timing, Timer* timer, std::chrono::steady_clock::time_point host_t0) {
+  const int npanels = out.npanels;
+  int32_t* swaps_dev = out.swaps_dev;
   const auto host_t1 = std::chrono::steady_clock::now();
   DevState hs;
-  read_state(st, hs, s);
+  read_state(out.st, hs, s);
   if (getenv("PRRP_HOSTTIME"))
     fprintf(stderr, "[prrp lu host] enqueue %.3f ms, then wait %.3f ms\n",
             std::chrono::duration<double, std::milli>(host_t1 - host_t0).count(),
@@ -1065,8 +1173,8 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     stats->total_swaps = 0;
     for (int v : sw) stats->total_swaps += v;
   }
-  if (timing) {
-    timer.collect(timing);
+  if (timing && timer) {
+    timer->collect(timing);
     timing->schur_flops = tl_schur_flops;
   }
   return state_to_err(hs, err);
@@ -1650,7 +1758,6 @@ std::vector<std::unique_ptr<CaluPlan>>& calu_plans() {
   static std::vector<std::unique_ptr<CaluPlan>> v;
   return v;
 }
-constexpr size_t kMaxPlans = 4;
 uint64_t g_plan_clock = 0;
 
 int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,
@@ -1746,7 +1853,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     CU_TRY(cudaStreamEndCapture(cs, &g));
     if (const char* dot = getenv("PRRP_GRAPH_DOT"))   // diagnostics: the captured dependency graph
       cudaGraphDebugDotPrint(g, dot, cudaGraphDebugDotFlagsVerbose);
-    const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, graph_instantiate_flags());
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) fail(PRRP_ERR_CUDA, "cudaGraphInstantiate failed");
     plans.push_back(std::move(np));
