@@ -124,7 +124,8 @@ int prrp_b200_dmma_peak(double ms, double* tflops, prrp_err* err);
 
 /* CALU_PRRP factorization with a binary tournament tree of `leaf_count`
  * leaves — replaces prrp.caluprrp_factor(a, b, tau, binary_tree(P))
- * (tournament.py:237-296).  Arguments as prrp_luprrp, plus
+ * (tournament.py:237-296); leaf_count == 0 selects flat_tree()
+ * (tournament.py:81-88, 202-208).  Arguments as prrp_luprrp, plus
  * tournament_charge3 (host int64[ceil(n/b)], may be NULL): 3x the
  * tournament flop charge of each panel (tournament.py:224-234), -1 for a
  * single-node panel, so the caller can rebuild the exact rational counters. */

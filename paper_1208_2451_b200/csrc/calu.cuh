@@ -335,3 +335,13 @@ __global__ void __launch_bounds__(256) calu_form_negqt_kernel(const double* refl
     }
   }
 }
+
+// flat-tree node inputs: members = [the b candidates, block rows lo .. lo+len)
+__global__ void calu_flat_inputs_kernel(const int32_t* cands, int b, int64_t lo, int len, int32_t* lpos_in,
+                                        int64_t* rowidx, const int64_t* pos2row, int64_t col0) {
+  for (int t = threadIdx.x; t < b + len; t += blockDim.x) {
+    const int32_t lp = t < b ? cands[t] : (int32_t)(lo + (t - b));
+    lpos_in[t] = lp;
+    rowidx[t] = pos2row[col0 + lp];
+  }
+}

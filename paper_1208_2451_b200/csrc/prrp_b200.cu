@@ -1232,7 +1232,12 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   tl_schur_prefetch_c = !calu_late_c;
   struct ResetPf { ~ResetPf() { tl_schur_prefetch_c = false; } } reset_pf;
   const int npanels = (int)((n + b - 1) / b);
-  const int maxnodes = 2 * P;
+  // P >= 1: binary tree over P leaves; P == 0: the flat tree (tournament.py:
+  // 81-88, 202-208: a first block of 2b rows, then b-row blocks, reduced one
+  // after the other, so one node per level and up to m/b + 1 nodes per panel)
+  const bool flat = P == 0;
+  const int maxnodes = flat ? (int)(m / std::max(1, b) + 2) : 2 * P;   // node slots per panel
+  const int nnodes = flat ? 1 : maxnodes;                               // node buffers
   // Schur launches: the tournament needs whole SMs (16-CTA clusters) at once,
   // so by default the updates run as short CTAs (classic kernel, quantum 0)
   // that hand SMs back quickly.  PRRP_CALU_NARROW: CTAs of a persistent
@@ -1269,12 +1274,13 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   double* A21t = ar.get<double>((size_t)b * ld21t);
   DevState* st_r12 = new_state(ar, s);   // the product's |C| must not enter the growth statistics
   // tree nodes
-  std::vector<NodeBufs> nodes(maxnodes);
-  const int64_t leafmax = m / std::max<int64_t>(1, std::min<int64_t>(P, std::max<int64_t>(1, m / (b + 1)))) + 1;
+  std::vector<NodeBufs> nodes(nnodes);
+  const int64_t leafmax =
+      flat ? 2 * b : m / std::max<int64_t>(1, std::min<int64_t>(P, std::max<int64_t>(1, m / (b + 1)))) + 1;
   const int64_t pnode = std::max<int64_t>(leafmax, 2 * b + 2);
-  int32_t* lpos_all = ar.get<int32_t>((size_t)maxnodes * 2 * b);
-  int64_t* rowidx_all = ar.get<int64_t>((size_t)maxnodes * 2 * b);
-  for (int i = 0; i < maxnodes; ++i) {
+  int32_t* lpos_all = ar.get<int32_t>((size_t)nnodes * 2 * b);
+  int64_t* rowidx_all = ar.get<int64_t>((size_t)nnodes * 2 * b);
+  for (int i = 0; i < nnodes; ++i) {
     NodeBufs& nb = nodes[i];
     nb.B.Rbuf = ar.get<double>((size_t)b * pnode);
     nb.B.perm = ar.get<int32_t>(pnode);
@@ -1288,11 +1294,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
     nb.lpos_in = lpos_all + (size_t)i * 2 * b;
     nb.rowidx = rowidx_all + (size_t)i * 2 * b;
   }
-  int32_t* cands = ar.get<int32_t>((size_t)2 * maxnodes * b);      // two levels (ping-pong)
+  int32_t* cands = ar.get<int32_t>((size_t)2 * nnodes * b);        // two levels (ping-pong)
   int32_t* node_swaps = ar.get<int32_t>((size_t)npanels * maxnodes);
   CU_TRY(cudaMemsetAsync(node_swaps, 0, sizeof(int32_t) * npanels * maxnodes, s));
-  const int32_t** perms_dev = ar.get<const int32_t*>(maxnodes);
-  int64_t* leaf_lo_dev = ar.get<int64_t>(maxnodes);
+  const int32_t** perms_dev = ar.get<const int32_t*>(nnodes);
+  int64_t* leaf_lo_dev = ar.get<int64_t>(nnodes);
   int64_t* pos2row = ar.get<int64_t>(m);
   int64_t* scratch = ar.get<int64_t>(3 * m);
   int32_t* log2phys = ar.get<int32_t>(m);
@@ -1302,9 +1308,9 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   int32_t* gperm = ar.get<int32_t>(b);
   int32_t* swaps_dev = ar.get<int32_t>(npanels);
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
-  for (int i0 = 0; i0 < maxnodes; i0 += 32) {   // node perm pointers (by value: capturable)
+  for (int i0 = 0; i0 < nnodes; i0 += 32) {     // node perm pointers (by value: capturable)
     PtrPack pk{};
-    const int cnt = std::min(32, maxnodes - i0);
+    const int cnt = std::min(32, nnodes - i0);
     for (int i = 0; i < cnt; ++i) pk.p[i] = nodes[i0 + i].B.perm;
     store_ptrs_kernel<<<1, 32, 0, s>>>(pk, cnt, perms_dev + i0);
   }
@@ -1430,8 +1436,41 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaStreamWaitEvent(sm, side_ev[panel - 2], 0));
         CU_TRY(cudaStreamWaitEvent(sm, fin_ev[panel - 2], 0));
       }
-      const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
-      if (p_eff == 1) {
+      const int64_t first = std::min<int64_t>(rows, 2 * bj);
+      const int64_t p_eff = flat ? 1 + (rows - first + bj - 1) / bj
+                                 : std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
+      if (p_eff > 1 && flat) {
+        // flat tree: the first block as a leaf, then one merge node per block
+        // on [candidates, block rows] (members in that order, tournament.py:206)
+        calu_leaf_lo_kernel<<<1, 64, 0, sm>>>(leaf_lo_dev, 1, rows, 0);
+        int64_t chg3 = 0;
+        int slot = 0;
+        run_level(std::vector<int64_t>{0}, std::vector<int64_t>{first}, true, col0, bj, panel, 0, slot, sm);
+        flush_after_main();
+        chg3 += qr_charge3(first, bj);
+        node_members[panel].push_back({first, slot});
+        ++slot;
+        int32_t* cur = cands;
+        int32_t* nxt = cands + (size_t)b;
+        calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
+        int level = 1;
+        for (int64_t lo = first; lo < rows; lo += bj, ++level) {
+          const int64_t len = std::min<int64_t>(bj, rows - lo);
+          calu_flat_inputs_kernel<<<1, 128, 0, sm>>>(cur, bj, lo, (int)len, lpos_all, rowidx_all, pos2row, col0);
+          run_level(std::vector<int64_t>{0}, std::vector<int64_t>{bj + len}, false, col0, bj, panel, level, slot, sm);
+          chg3 += qr_charge3(bj + len, bj);
+          node_members[panel].push_back({bj + len, slot});
+          ++slot;
+          calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
+          std::swap(cur, nxt);
+        }
+        CU_TRY(cudaGetLastError());
+        charges[panel] = chg3;
+        tbegin(PRRP_K_OTHER, sm);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
+                                                st);
+        tend(sm);
+      } else if (p_eff == 1) {
         // single node: the selector's own full order and l_block (tournament.py:168-177)
         strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Lg, ldl, Bk, st, swaps_dev, nullptr, nullptr,
                           nullptr, false, sm, pos2row + col0);
@@ -1792,7 +1831,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
   if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
   if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
-  if (P < 1) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1");
+  if (P < 0) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1 (0 selects the flat tree)");
   if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
   if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
   caps();

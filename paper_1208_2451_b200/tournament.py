@@ -2,7 +2,7 @@
 
 Keeps the reference's entry points and types (tournament.py:43-61, 237-296):
 ``caluprrp_factor(a, b, tau=2.0, tree=None)`` with ``binary_tree(P)``
-(default P = 8).  The tournament runs on the device (prrp_caluprrp): leaves
+(default P = 8) or ``flat_tree()``.  The tournament runs on the device (prrp_caluprrp): leaves
 and same-level merges execute concurrently, each as the cluster strong-RRQR
 engine over an index list of logical rows; the result is independent of that
 concurrency, as the reference's determinism contract requires
@@ -203,8 +203,7 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
     _validate(a, b, tau)
     if tree is None:
         tree = binary_tree(8)
-    if tree.shape != "binary":
-        raise NotImplementedError("the device tournament implements the binary tree (flat tree: SURVEY 8(f))")
+    leaf_count = int(tree.leaf_count) if tree.shape == "binary" else 0   # 0: the flat tree
     m, n = a.shape
     lib = _lib.device_lib()
     import torch
@@ -216,7 +215,7 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
     chg3 = (ctypes.c_int64 * npan)()
     st = _lib.PrrpStats()
     err = _lib.PrrpErr()
-    rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, m, n, b, float(tau), int(tree.leaf_count),
+    rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, m, n, b, float(tau), leaf_count,
                            ctypes.c_void_p(perm.data_ptr()), swaps, chg3, ctypes.byref(st), ctypes.byref(err),
                            _lib.stream_handle())
     _lib.raise_for(rc, err, "prrp_caluprrp")

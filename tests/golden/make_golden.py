@@ -122,6 +122,9 @@ CALU_CASES = [
     {"name": "calu_urand160_b16_P8", "gen": "urand", "n": 160, "seed": 42, "b": 16, "tau": 2.0, "P": 8},
     {"name": "calu_randn512_b32_P8", "gen": "randn", "n": 512, "seed": 42, "b": 32, "tau": 2.0, "P": 8},
     {"name": "calu_randn256_b16_P8_tau11", "gen": "randn", "n": 256, "seed": 8, "b": 16, "tau": 1.1, "P": 8},
+    # flat reduction tree (tournament.py:81-88, 202-208): "P": 0
+    {"name": "calu_flat_randn160_b16", "gen": "randn", "n": 160, "seed": 42, "b": 16, "tau": 2.0, "P": 0},
+    {"name": "calu_flat_randn256_b32", "gen": "randn", "n": 256, "seed": 5, "b": 32, "tau": 2.0, "P": 0},
 ]
 
 SRRQR_CASES = [
@@ -199,13 +202,14 @@ def main():
 
     for c in CALU_CASES:
         a = make_input(c)
-        f = prrp.caluprrp_factor(a, c["b"], c["tau"], prrp.binary_tree(c["P"]))
+        tree = prrp.binary_tree(c["P"]) if c["P"] > 0 else prrp.flat_tree()
+        f = prrp.caluprrp_factor(a, c["b"], c["tau"], tree)
         key = "calu/" + c["name"]
         arrays[key + "/perm"] = f.perm
         if a.shape[0] <= 256:
             arrays[key + "/l"] = f.l
             arrays[key + "/u"] = f.u
-        perm0, trace = prrp.tournament_select(a[:, :c["b"]], c["b"], c["tau"], prrp.binary_tree(c["P"]), "srrqr")
+        perm0, trace = prrp.tournament_select(a[:, :c["b"]], c["b"], c["tau"], tree, "srrqr")
         arrays[key + "/t_perm"] = perm0
         entry = dict(c)
         entry["input_sha"] = sha(a)

@@ -212,22 +212,25 @@ def test_luprrp_growth_stress(dev):
 
 
 def test_caluprrp_golden(dev, golden):
-    """CALU_PRRP (binary tree) against the reference's fixtures and the oracle."""
+    """CALU_PRRP (binary and flat trees) against the reference's fixtures and the oracle."""
     index, arrays = golden
     for e in index["calu"]:
         a = make_input(e)
-        f = dev.caluprrp_factor(a, e["b"], e["tau"], dev.binary_tree(e["P"]))
-        ref = orc.calu_prrp(a, e["b"], e["tau"], "binary", e["P"])
+        flat = e["P"] == 0
+        f = dev.caluprrp_factor(a, e["b"], e["tau"], dev.flat_tree() if flat else dev.binary_tree(e["P"]))
+        ref = orc.calu_prrp(a, e["b"], e["tau"], *(("flat", None) if flat else ("binary", e["P"])))
         assert np.array_equal(ref.perm, arrays["calu/" + e["name"] + "/perm"])
         _check_factors(f, ref, a)
 
 
 @pytest.mark.parametrize("n,b,P,gen", [(1024, 64, 8, "randn"), (2048, 64, 8, "randn"), (1536, 128, 8, "urand"),
-                                       (700, 32, 4, "randn"), (900, 64, 3, "urand")])
+                                       (700, 32, 4, "randn"), (900, 64, 3, "urand"), (640, 64, 0, "randn"),
+                                       (520, 128, 0, "urand")])
 def test_caluprrp_vs_oracle(dev, n, b, P, gen):
+    """P = 0: the flat tree (sequential reduction, first block 2b rows)."""
     a = orc.randn_matrix(n, 42) if gen == "randn" else orc.urand_matrix(n, 42)
-    f = dev.caluprrp_factor(a, b, 2.0, dev.binary_tree(P))
-    ref = orc.calu_prrp(a, b, 2.0, "binary", P)
+    f = dev.caluprrp_factor(a, b, 2.0, dev.flat_tree() if P == 0 else dev.binary_tree(P))
+    ref = orc.calu_prrp(a, b, 2.0, *(("flat", None) if P == 0 else ("binary", P)))
     _check_factors(f, ref, a)
 
 

@@ -78,6 +78,11 @@ def test_spec_srrqr_examples():
     assert list(res.qr.perm) == [1, 0] and res.l_block[0, 0] == pytest.approx(0.1)
 
 
+def _tree(e):
+    """(shape, leaf_count) of a CALU fixture: "P": 0 is the flat tree."""
+    return ("binary", e["P"]) if e["P"] > 0 else ("flat", None)
+
+
 @pytest.mark.parametrize("which", ["lu", "calu"])
 def test_factor_golden(golden, which):
     index, arrays = golden
@@ -87,7 +92,7 @@ def test_factor_golden(golden, which):
         if which == "lu":
             f = orc.lu_prrp(a, e["b"], e["tau"])
         else:
-            f = orc.calu_prrp(a, e["b"], e["tau"], "binary", e["P"])
+            f = orc.calu_prrp(a, e["b"], e["tau"], *_tree(e))
         key = f"{which}/" + e["name"]
         assert np.array_equal(f.perm, arrays[key + "/perm"]), e["name"]
         if key + "/l" in arrays:
@@ -102,7 +107,7 @@ def test_tournament_trace_golden(golden):
     index, arrays = golden
     for e in index["calu"]:
         a = make_input(e)
-        perm, tr = orc.tournament(a[:, :e["b"]], e["b"], e["tau"], "binary", e["P"])
+        perm, tr = orc.tournament(a[:, :e["b"]], e["b"], e["tau"], *_tree(e))
         assert np.array_equal(perm, arrays["calu/" + e["name"] + "/t_perm"])
         assert tr.leaf_count == e["trace_leaf_count"]
         got = [(n.level, n.index, n.members.tolist(), n.selected.tolist(), n.swap_count) for n in tr.nodes]
