@@ -37,7 +37,7 @@ UNIT = "GFLOP/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=8192)
@@ -127,6 +127,8 @@ class ClockSampler:
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
 
     def start(self):
+        if os.environ.get("PRRP_BENCH_NOCLOCKS"):
+            return
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
@@ -235,6 +237,8 @@ def run_device(args):
     launches = args.steps * sum(tms[-1].launches)
     ms_step = statistics.mean(times)
     value = ws * lu_flops(n) / (ms_step * 1e-3) / 1e9
+    if os.environ.get("PRRP_BENCH_STEPS"):
+        print("step ms:", [round(t, 2) for t in times], file=sys.stderr, flush=True)
 
     # roofline of the dominant kernel (Schur update on the FP64 tensor pipe)
     schur_ms = sum(t.ms[_lib.KCLASSES.index("schur")] for t in tms) / len(tms)
