@@ -162,6 +162,18 @@ DeviceCaps& caps() {
       }
       cudaGetLastError();
     }
+    // the per-call workspaces come from the stream-ordered pool: keep freed
+    // blocks mapped (the default release threshold of 0 unmaps them at every
+    // synchronisation, and re-mapping tens of MB inside the next call shows up
+    // as a multi-millisecond hiccup)
+    {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+    }
     CU_TRY(cudaMalloc(&c.sched, kSchedSlots * 2 * sizeof(int)));
     CU_TRY(cudaMemset(c.sched, 0, kSchedSlots * 2 * sizeof(int)));
     c.init = true;
