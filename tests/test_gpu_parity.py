@@ -391,3 +391,71 @@ def test_concurrent_host_threads(dev):
     for i, ref in enumerate(serial_lu + serial_calu):
         assert np.array_equal(out[i].perm, ref.perm)
         assert np.array_equal(out[i].l, ref.l) and np.array_equal(out[i].u, ref.u)
+
+
+def _device_calu(buf, n, b, P):
+    import ctypes
+    import torch
+    from paper_1208_2451_b200 import _lib
+    lib = _lib.device_lib()
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    npan = (n + b - 1) // b
+    sw = (ctypes.c_int32 * npan)()
+    chg = (ctypes.c_int64 * npan)()
+    st, err = _lib.PrrpStats(), _lib.PrrpErr()
+    rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), buf.stride(0), n, n, b, 2.0, P,
+                           ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                           _lib.stream_handle())
+    assert rc == 0, err.msg
+    return perm, st
+
+
+@pytest.mark.parametrize("cfg", ["c2_b64", "c2_b128", "c3_wilkinson", "c3_foster", "c4", "c5"])
+def test_full_size_properties(dev, cfg):
+    """BASELINE configs at their full sizes, where the CPU oracle is too slow:
+    size-independent properties.  Backward error ||PA - LU||_F / ||A||_F on the
+    device below n 2^-52; multipliers bounded by tau (LU_PRRP's strong RRQR);
+    the known growth factors of the growth-stress matrices (config 3, SURVEY
+    8(c): Wilkinson 2, Foster 2.25); a second factorization bit-identical."""
+    import torch
+    from paper_1208_2451_b200 import matgen
+    from paper_1208_2451_b200.metrics import rel_factorization_error_device
+    if cfg.startswith("c2"):
+        n, b = 8192, (64 if cfg == "c2_b64" else 128)
+        a = matgen.gen_randn(n, 42, order="C")
+    elif cfg == "c3_wilkinson":
+        n, b = 4096, 64
+        a = np.ascontiguousarray(orc.wilkinson_matrix(n))
+    elif cfg == "c3_foster":
+        n, b = 4096, 64
+        a = np.ascontiguousarray(orc.foster_matrix(n, 1.0, 1.0, 1.0))
+    elif cfg == "c4":
+        n, b = 16384, 64
+        a = matgen.gen_randn(n, 42, order="C")
+    else:
+        n, b = 32768, 128
+        a = matgen.gen_urand(n, 42, order="C")
+    A = torch.from_numpy(a).cuda()
+    del a
+    outs = []
+    for _ in range(2):
+        buf = A.clone()
+        if cfg in ("c4", "c5"):
+            perm, st = _device_calu(buf, n, b, 8)
+            growth = st.intermediate_max / st.original_max
+            pmm = None
+        else:
+            res = dev.luprrp_factor_device(buf, b, 2.0)
+            perm, growth, pmm = res.perm, res.stats.growth_factor, res.stats.panel_multiplier_max
+        outs.append((buf, perm, growth, pmm))
+    (lu0, p0, g0, pmm0), (lu1, p1, g1, _) = outs
+    assert torch.equal(p0, p1) and torch.equal(lu0, lu1) and g0 == g1
+    assert torch.equal(torch.sort(p0).values, torch.arange(n, device=p0.device))
+    res = rel_factorization_error_device(A, lu0, p0)
+    assert res < n * 2.0 ** -52, res
+    if pmm0 is not None:
+        assert pmm0 <= 2.0 * (1 + 1e-12)
+    if cfg == "c3_wilkinson":
+        assert g0 == pytest.approx(2.0, rel=1e-10)
+    if cfg == "c3_foster":
+        assert g0 == pytest.approx(2.25, rel=1e-10)
