@@ -126,6 +126,21 @@ def unit_lower_solve(l, rhs):
     return x
 
 
+def upper_solve_right(b, u):
+    """X U = B, column by column: x[:, j] /= u[j, j], then
+    x[:, j+1:] -= x[:, j] u[j, j+1:] (matcore.py:97-113)."""
+    x = fmat(b).copy(order="F")
+    n = u.shape[0]
+    for j in range(n):
+        d = u[j, j]
+        if d == 0.0:
+            raise OracleSingularFactor(f"zero diagonal at index {j}", index=j)
+        x[:, j] /= d
+        if j + 1 < n:
+            x[:, j + 1:] -= x[:, j:j + 1] * u[j:j + 1, j + 1:]
+    return x
+
+
 def maxabs(a):
     a = np.asarray(a, dtype=np.float64)
     return 0.0 if a.size == 0 else float(np.abs(a).max())      # matcore.py:116-130 'max'
@@ -513,11 +528,23 @@ class Trace:
     srr: object = None
 
 
-def pick(panel, idx, b, tau):
-    """srrqr selector with rank-deficient shrink (tournament.py:118-141)."""
+def pick(panel, idx, b, tau, selector="srrqr"):
+    """srrqr selector with rank-deficient shrink (tournament.py:118-141);
+    selector "gepp": partial pivoting on the node rows, a zero pivot at
+    column k keeps the k rows chosen so far (tournament.py:142-150)."""
     if idx.shape[0] <= b:
         return idx, idx, 0, None
     sub = panel[idx, :]
+    if selector == "gepp":
+        cols = b
+        while cols:
+            try:
+                g = gepp(sub[:, :cols])
+            except OracleSingularMatrix as exc:
+                cols = exc.column
+                continue
+            return idx[g.perm[:cols]], idx[g.perm], 0, None
+        return idx[:0], idx, 0, None
     want = b
     while want:
         try:
@@ -530,8 +557,8 @@ def pick(panel, idx, b, tau):
     return idx[:0], idx, 0, None
 
 
-def tournament(panel, b, tau, shape="binary", leaf_count=8):
-    """Tournament of strong RRQRs (tournament.py:155-217)."""
+def tournament(panel, b, tau, shape="binary", leaf_count=8, selector="srrqr"):
+    """Tournament of strong RRQRs, or of GEPPs (tournament.py:155-217)."""
     panel = fmat(panel)
     m = panel.shape[0]
     if panel.shape[1] != b:
@@ -540,7 +567,7 @@ def tournament(panel, b, tau, shape="binary", leaf_count=8):
     nodes = []
     if len(blocks) == 1:
         idx = np.arange(m, dtype=np.intp)
-        sel, order, swaps, sr = pick(panel, idx, b, tau)
+        sel, order, swaps, sr = pick(panel, idx, b, tau, selector)
         if sel.shape[0] < b:
             raise OracleRankDeficient("panel supplied too few rows", index=sel.shape[0])
         nodes.append(Node(0, 0, idx, sel, swaps))
@@ -548,7 +575,7 @@ def tournament(panel, b, tau, shape="binary", leaf_count=8):
 
     def node(level, index, idx):
         try:
-            sel, _, swaps, _ = pick(panel, idx, b, tau)
+            sel, _, swaps, _ = pick(panel, idx, b, tau, selector)
         except ArithmeticError as exc:
             exc.tree_node = (level, index)
             raise
@@ -579,12 +606,16 @@ def tournament(panel, b, tau, shape="binary", leaf_count=8):
     return perm, Trace(nodes, piv, p_eff, leaf_count, False, None)
 
 
-def _tournament_charge(trace, b):     # tournament.py:224-234 (srrqr selector)
+def _gepp_charge(rows, cols):         # tournament.py:220-221
+    return Fraction(rows * cols * cols) - Fraction(cols ** 3, 3)
+
+
+def _tournament_charge(trace, b, selector="srrqr"):     # tournament.py:224-234
     tot = Fraction(0)
     for nd in trace.nodes:
         r = int(nd.members.shape[0])
         if r > b:
-            tot += (1 + nd.swap_count) * _qr_charge(r, b)
+            tot += (1 + nd.swap_count) * _qr_charge(r, b) if selector == "srrqr" else _gepp_charge(r, b)
     return tot
 
 
@@ -629,6 +660,58 @@ def calu_prrp(a, b, tau=2.0, shape="binary", leaf_count=8, panel_limit=None):
         except ArithmeticError as exc:
             exc.panel = panel
             raise
+        fin = _finish_charge(bj, n - col0)
+        s.flops_charged += fin
+        s.flops_executed += fin
+        col0 += bj
+        panel += 1
+    return st.factors(b)
+
+
+def calu_gepp(a, b, shape="binary", leaf_count=8):
+    """Tournament-pivoted GEPP, the reference's calu_factor
+    (tournament.py:299-359): GEPP selector in every node, GEPP finish of
+    the block row without composing L21, L21 = A21 U11^-1
+    (matcore.trsm_upper_right), rank-b update."""
+    a = fmat(a)
+    _check_args(a, b, 2.0)
+    m, n = a.shape
+    st = _Work(a)
+    s = st.stats
+    col0 = 0
+    panel = 0
+    while col0 < n:
+        bj = min(b, n - col0)
+        rows = m - col0
+        width = n - col0 - bj
+        if rows > bj:
+            try:
+                rel, tr = tournament(st.w[col0:, col0:col0 + bj], bj, 2.0, shape, leaf_count, "gepp")
+            except ArithmeticError as exc:
+                exc.panel = panel
+                raise
+            st.permute_tail(col0, rel)
+            extra = _tournament_charge(tr, bj, "gepp")
+            s.flops_charged += extra
+            s.flops_executed += extra
+            s.swap_counts.append(0)
+            try:
+                st.block_row_finish(col0, bj, compose=False)
+            except ArithmeticError as exc:
+                exc.panel = panel
+                raise
+            l21 = upper_solve_right(st.w[col0 + bj:, col0:col0 + bj], st.w[col0:col0 + bj, col0:col0 + bj])
+            cost = Fraction((rows - bj) * bj * bj + 2 * bj * (rows - bj) * width)
+            s.flops_charged += cost
+            s.flops_executed += cost
+            st.store_multipliers_and_update(col0, bj, l21)
+        else:
+            s.swap_counts.append(0)
+            try:
+                st.block_row_finish(col0, bj)
+            except ArithmeticError as exc:
+                exc.panel = panel
+                raise
         fin = _finish_charge(bj, n - col0)
         s.flops_charged += fin
         s.flops_executed += fin

@@ -56,6 +56,16 @@ def make_input(spec):
     raise ValueError(kind)
 
 
+def gepp_calu_input(spec):
+    """Input of a calu_factor fixture: make_input + the optional zeroed
+    block ("zero": [r0, r1, cols]) that starves one tournament leaf."""
+    a = np.array(make_input(spec), order="F")
+    if "zero" in spec:
+        r0, r1, cols = spec["zero"]
+        a[r0:r1, :cols] = 0.0
+    return a
+
+
 def srrqr_input(spec, arrays):
     key = "srrqr/" + spec["name"] + "/a"
     if key in arrays:

@@ -127,6 +127,29 @@ CALU_CASES = [
     {"name": "calu_flat_randn256_b32", "gen": "randn", "n": 256, "seed": 5, "b": 32, "tau": 2.0, "P": 0},
 ]
 
+# calu_factor (tournament-pivoted GEPP, tournament.py:299-359); "zero": rows
+# [r0, r1) x columns [0, c) zeroed, so a leaf of the first panel is
+# numerically rank deficient and passes on fewer than b rows
+GEPP_CALU_CASES = [
+    {"name": "gcalu_randn256_b8_P8", "gen": "randn", "n": 256, "seed": 42, "b": 8, "P": 8},
+    {"name": "gcalu_randn200_b16_P4", "gen": "randn", "n": 200, "seed": 9, "b": 16, "P": 4},
+    {"name": "gcalu_urand160_b16_P8", "gen": "urand", "n": 160, "seed": 42, "b": 16, "P": 8},
+    {"name": "gcalu_randn512_b64_P8", "gen": "randn", "n": 512, "seed": 42, "b": 64, "P": 8},
+    {"name": "gcalu_tall200x120_b16_P3", "gen": "randn", "m": 200, "n": 120, "seed": 3, "b": 16, "P": 3},
+    {"name": "gcalu_flat_randn160_b16", "gen": "randn", "n": 160, "seed": 42, "b": 16, "P": 0},
+    {"name": "gcalu_zeroleaf160_b16_P4", "gen": "randn", "n": 160, "seed": 6, "b": 16, "P": 4, "zero": [0, 40, 16]},
+    {"name": "gcalu_wilkinson64_b8_P4", "gen": "wilkinson", "n": 64, "b": 8, "P": 4},
+]
+
+
+def gepp_calu_input(c):
+    a = make_input(c).copy(order="F")
+    if "zero" in c:
+        r0, r1, cols = c["zero"]
+        a[r0:r1, :cols] = 0.0
+    return a
+
+
 SRRQR_CASES = [
     {"name": "eye_pad", "data": np.hstack([np.eye(4), np.zeros((4, 3))]).tolist(), "b": 4, "tau": 2.0},
     {"name": "one_ten", "data": [[1.0, 10.0]], "b": 1, "tau": 2.0},
@@ -149,7 +172,7 @@ def srrqr_input(c):
 
 def main():
     index = {"blas": str(np.__config__.CONFIG["Build Dependencies"]["blas"].get("openblas configuration", "")),
-             "lu": [], "lu_errors": [], "calu": [], "srrqr": [], "c1": None}
+             "lu": [], "lu_errors": [], "calu": [], "gepp_calu": [], "srrqr": [], "c1": None}
     arrays = {}
 
     for c in SRRQR_CASES:
@@ -221,6 +244,23 @@ def main():
                           for nd in trace.nodes]
         entry["trace_leaf_count"] = int(trace.leaf_count)
         index["calu"].append(entry)
+
+    for c in GEPP_CALU_CASES:
+        a = gepp_calu_input(c)
+        tree = prrp.binary_tree(c["P"]) if c["P"] > 0 else prrp.flat_tree()
+        f = prrp.calu_factor(a, c["b"], tree)
+        key = "gepp_calu/" + c["name"]
+        arrays[key + "/perm"] = f.perm
+        arrays[key + "/l"] = f.l
+        arrays[key + "/u"] = f.u
+        perm0, trace = prrp.tournament_select(a[:, :c["b"]], c["b"], 2.0, tree, "gepp")
+        arrays[key + "/t_perm"] = perm0
+        entry = dict(c)
+        entry["input_sha"] = sha(a)
+        entry["stats"] = stats_dict(f.stats)
+        entry["trace"] = [{"level": nd.level, "index": nd.index, "members": nd.members.tolist(),
+                           "selected": nd.selected.tolist()} for nd in trace.nodes]
+        index["gepp_calu"].append(entry)
 
     # Config 1 of BASELINE.json: randn(1024, 42), b=64, tau=2
     a = matgen.gen_randn(1024, 42)

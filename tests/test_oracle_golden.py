@@ -12,7 +12,7 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-from conftest import make_input, srrqr_input
+from conftest import gepp_calu_input, make_input, srrqr_input
 from oracle import prrp_oracle as orc
 
 
@@ -113,6 +113,31 @@ def test_tournament_trace_golden(golden):
         got = [(n.level, n.index, n.members.tolist(), n.selected.tolist(), n.swap_count) for n in tr.nodes]
         ref = [(n["level"], n["index"], n["members"], n["selected"], n["swap_count"]) for n in e["trace"]]
         assert got == ref
+
+
+def test_gepp_calu_golden(golden):
+    """calu_factor (tournament.py:299-359): the oracle restatement against
+    the reference's own outputs -- factors, row order, exact rational flop
+    counters, growth statistics, and the GEPP tournament trace including
+    rank-deficient leaves (zeroed block, Wilkinson)."""
+    index, arrays = golden
+    exact = _same_blas(index)
+    assert len(index["gepp_calu"]) >= 8
+    for e in index["gepp_calu"]:
+        a = gepp_calu_input(e)
+        assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == e["input_sha"], e["name"]
+        shape, lc = _tree(e)
+        f = orc.calu_gepp(a, e["b"], shape, lc or 8)
+        key = "gepp_calu/" + e["name"]
+        assert np.array_equal(f.perm, arrays[key + "/perm"]), e["name"]
+        _close(f.l, arrays[key + "/l"], exact)
+        _close(f.u, arrays[key + "/u"], exact)
+        _check_stats(f.stats, e["stats"], exact)
+        perm, tr = orc.tournament(a[:, :e["b"]], e["b"], 2.0, shape, lc or 8, "gepp")
+        assert np.array_equal(perm, arrays[key + "/t_perm"]), e["name"]
+        got = [(n.level, n.index, n.members.tolist(), n.selected.tolist()) for n in tr.nodes]
+        ref = [(n["level"], n["index"], n["members"], n["selected"]) for n in e["trace"]]
+        assert got == ref, e["name"]
 
 
 def test_error_contract_golden(golden):
