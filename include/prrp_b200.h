@@ -133,6 +133,25 @@ int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, doubl
                   int32_t leaf_count, int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3,
                   prrp_stats* stats, prrp_err* err, void* stream);
 
+/* Tournament-pivoted GEPP ("calu_factor") with a binary tree of
+ * `leaf_count` leaves, 0 = flat tree — replaces prrp.calu_factor(a, b, tree)
+ * (tournament.py:299-359): every tournament node selects by partial
+ * pivoting (tournament.py:142-150), the block row is finished by GEPP
+ * without composing L21, L21 = A21 U11^-1 (matcore.py:97-113).  Arguments
+ * as prrp_caluprrp without tau and swap counts (always 0 for this
+ * factorization); tournament_charge3[k] = 3x panel k's tournament flop
+ * charge (tournament.py:220-234), 0 when the panel has no selection. */
+int prrp_calu(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, int32_t leaf_count,
+              int64_t* perm, int64_t* tournament_charge3, prrp_stats* stats, prrp_err* err,
+              void* stream);
+
+/* One GEPP selector node (tournament.py:142-150): partial pivoting on the
+ * r x cols row-major device matrix `a` (r > cols, cols <= 128); order
+ * (device int64[r]) = the elimination's row order, *count (host) = rows
+ * chosen before the first zero pivot (cols when none). */
+int prrp_gepp_select(const double* a, int64_t lda, int64_t r, int32_t cols, int64_t* order,
+                     int32_t* count, prrp_err* err, void* stream);
+
 /* Strong RRQR of an h x p matrix `a` (column-major, lda >= h) with leading
  * block size bsel <= h and threshold tau — replaces prrp.strong_rrqr
  * (pivoted_qr.py:113-147).  Outputs (device, column-major): R h x p (ldr=h),

@@ -63,6 +63,8 @@ SIGNATURES = {
     "prrp_multiplier_block": ([_P, _I64, _I32, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
     "prrp_schur_update": ([_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I32, _P, _P, _P], ctypes.c_int),
     "prrp_gepp_blockrow": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_calu": ([_P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_gepp_select": ([_P, _I64, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
 }
 
 _lib = None

@@ -32,6 +32,7 @@
 #include "rowops.cuh"
 #include "schur.cuh"
 #include "calu.cuh"
+#include "calu_gepp.cuh"
 
 namespace {
 
@@ -1965,6 +1966,206 @@ int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, in
   return state_to_err(hs, err);
 }
 
+
+// ---------------------------------------------------------------- calu_factor
+// Tournament-pivoted GEPP (tournament.py:299-359), one stream.  Per panel:
+// GEPP tournament (one launch per tree level, one CTA per node), row order of
+// the trailing rows, row moves, GEPP finish of the block row (the LU_PRRP
+// kernels, no compose), L21 = A21 U11^-1, DMMA trailing update.
+constexpr int kGnSmem = 160 * 1024;
+
+struct GeppTourBufs {
+  double* wscratch;
+  int32_t* oscratch;
+  int32_t* cand[2];
+  int32_t* cnt[2];
+  int32_t* order_full;
+  int32_t* mark;
+  int32_t* perm_rel;
+};
+
+// Levels of one panel's tournament; returns the buffer index holding the root.
+int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int P, const GeppTourBufs& T,
+                    unsigned long long* chg3, DevState* st, int panel_no, bool& single, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    CU_TRY(cudaFuncSetAttribute(gepp_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGnSmem));
+    attr = true;
+  }
+  GeppLevel g{};
+  g.panel = panel; g.lda = lda; g.bj = bj; g.rows = rows;
+  g.wscratch = T.wscratch; g.oscratch = T.oscratch; g.chg3 = chg3; g.st = st; g.panel_no = panel_no;
+  auto smem_for = [&](int64_t r) -> int {
+    const size_t need = (size_t)r * bj * 8 + (size_t)r * 4;
+    return need <= (size_t)kGnSmem ? (int)((need + 15) / 16 * 16) : 0;
+  };
+  int cur = 0;
+  if (P > 0) {
+    const int64_t p_eff = std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
+    single = p_eff == 1;
+    g.mode = 0; g.p_eff = p_eff;
+    g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
+    g.order_full = single ? T.order_full : nullptr;
+    g.smem_bytes = smem_for((rows + p_eff - 1) / p_eff);
+    gepp_node_kernel<<<(unsigned)p_eff, GN_T, g.smem_bytes, s>>>(g);
+    CU_TRY(cudaGetLastError());
+    g.order_full = nullptr;
+    int64_t ncur = p_eff;
+    while (ncur > 1) {
+      const int64_t nout = (ncur + 1) / 2;
+      g.mode = 1; g.nprev = ncur;
+      g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
+      g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
+      g.smem_bytes = smem_for(2 * bj);
+      gepp_node_kernel<<<(unsigned)nout, GN_T, g.smem_bytes, s>>>(g);
+      CU_TRY(cudaGetLastError());
+      cur ^= 1;
+      ncur = nout;
+    }
+    return cur;
+  }
+  const int64_t first = std::min<int64_t>(rows, 2 * bj);
+  single = first >= rows;
+  g.mode = 2; g.hi = first;
+  g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
+  g.order_full = single ? T.order_full : nullptr;
+  g.smem_bytes = smem_for(first);
+  gepp_node_kernel<<<1, GN_T, g.smem_bytes, s>>>(g);
+  CU_TRY(cudaGetLastError());
+  g.order_full = nullptr;
+  for (int64_t lo = first; lo < rows; lo += bj) {
+    g.mode = 3; g.lo = lo; g.hi = std::min<int64_t>(rows, lo + bj);
+    g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
+    g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
+    g.smem_bytes = smem_for(2 * bj);
+    gepp_node_kernel<<<1, GN_T, g.smem_bytes, s>>>(g);
+    CU_TRY(cudaGetLastError());
+    cur ^= 1;
+  }
+  return cur;
+}
+
+GeppTourBufs alloc_tour(Arena& ar, int64_t m, int b, int P) {
+  GeppTourBufs T{};
+  const int64_t nodes = std::max(P, 1) + 1;
+  T.wscratch = ar.get<double>((size_t)(m + 2 * b * nodes) * b);
+  T.oscratch = ar.get<int32_t>((size_t)(m + 2 * b * nodes));
+  for (int i = 0; i < 2; ++i) {
+    T.cand[i] = ar.get<int32_t>((size_t)nodes * b);
+    T.cnt[i] = ar.get<int32_t>((size_t)nodes);
+  }
+  T.order_full = ar.get<int32_t>(m);
+  T.mark = ar.get<int32_t>(m);
+  T.perm_rel = ar.get<int32_t>(m);
+  return T;
+}
+
+int calu_gepp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, int P, int64_t* perm, int64_t* chg3_out,
+                   prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+  if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+  if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+  if (P < 0) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1 (0 selects the flat tree)");
+  if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device path");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  if (m > INT32_MAX) fail(PRRP_ERR_UNSUPPORTED, "more than 2^31 rows");
+  caps();
+  const int sms = caps().sms;
+  const int npanels = (int)((n + b - 1) / b);
+  Arena ar(s);
+  DevState* st = new_state(ar, s);
+  const int64_t ldl = ((m + 7) / 8) * 8;
+  double* Lcm = ar.get<double>((size_t)b * ldl);
+  GeppTourBufs T = alloc_tour(ar, m, b, P);
+  const int64_t cw = std::min<int64_t>(n, 2048);
+  double* rbuf = ar.get<double>((size_t)m * cw);
+  int64_t* pbuf = ar.get<int64_t>(m);
+  double* D = ar.get<double>((size_t)b * b);
+  int32_t* piv = ar.get<int32_t>(b);
+  int32_t* gperm = ar.get<int32_t>(b);
+  unsigned long long* chg3 = ar.get<unsigned long long>(npanels);
+  CU_TRY(cudaMemsetAsync(chg3, 0, sizeof(unsigned long long) * npanels, s));
+  iota_kernel<<<sms, 256, 0, s>>>(perm, m);
+  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  CU_TRY(cudaGetLastError());
+  static bool attr = false;
+  if (!attr) {
+    CU_TRY(cudaFuncSetAttribute(trsm_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  int panel = 0;
+  for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
+    const int bj = (int)std::min<int64_t>(b, n - col0);
+    const int64_t rows = m - col0;
+    const int64_t width = n - col0 - bj;
+    double* blk = A + col0 * lda + col0;
+    if (rows > bj) {
+      bool single = false;
+      const int root = gepp_tournament(blk, lda, bj, rows, P, T, chg3 + panel, st, panel, single, s);
+      gepp_tail_order_kernel<<<1, 1024, 0, s>>>(T.cand[root], T.cnt[root], bj, rows,
+                                                single ? T.order_full : nullptr, T.mark, T.perm_rel, st, panel);
+      const unsigned pg = (unsigned)std::min<int64_t>(rows, 8 * sms);
+      for (int64_t c0 = 0; c0 < n; c0 += cw) {
+        const int64_t c1 = std::min<int64_t>(n, c0 + cw);
+        tail_gather_kernel<<<pg, 256, 0, s>>>(A, lda, col0, rows, c0, c1, T.perm_rel, perm, rbuf,
+                                              c0 == 0 ? pbuf : nullptr, st);
+        tail_scatter_kernel<<<pg, 256, 0, s>>>(A, lda, col0, rows, c0, c1, T.perm_rel, perm, rbuf,
+                                               c0 == 0 ? pbuf : nullptr, st);
+      }
+      CU_TRY(cudaGetLastError());
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
+      launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+      CU_TRY(cudaGetLastError());
+      const int64_t M = rows - bj;
+      const int tw = bj > 64 ? 64 : 128;
+      const size_t dyn = ((size_t)bj * bj + (size_t)bj * tw) * 8;
+      const unsigned tg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((M + tw - 1) / tw, 4 * sms));
+      trsm_right_kernel<<<tg, tw, dyn, s>>>(A, lda, col0, bj, col0 + bj, M, Lcm, ldl, st);
+      CU_TRY(cudaGetLastError());
+      if (width > 0)
+        schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lcm, ldl, A + col0 * lda + col0 + bj, lda, M, width,
+                     bj, st, s, sms);
+    } else {
+      launch_gepp(blk, lda, nullptr, bj, D, piv, gperm, st, panel, s);
+      launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
+      CU_TRY(cudaGetLastError());
+    }
+  }
+  DevState hs;
+  read_state(st, hs, s);
+  if (chg3_out) {
+    std::vector<unsigned long long> c(npanels);
+    CU_TRY(cudaMemcpy(c.data(), chg3, sizeof(unsigned long long) * npanels, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < npanels; ++k) chg3_out[k] = (int64_t)c[k];
+  }
+  fill_stats(hs, stats);
+  if (stats) stats->total_swaps = 0;
+  return state_to_err(hs, err);
+}
+
+// One GEPP selector node over r rows (tournament.py:142-150): order[0..r) and
+// the number of rows chosen before the first zero pivot.
+int gepp_select_impl(const double* a, int64_t lda, int64_t r, int cols, int64_t* order, int32_t* count,
+                     prrp_err* err, cudaStream_t s) {
+  if (cols < 1 || cols > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "gepp_select needs 1 <= cols <= 128");
+  if (r <= cols) fail(PRRP_ERR_ARG, "gepp_select needs more rows than columns");
+  if (lda < cols) fail(PRRP_ERR_ARG, "lda < cols");
+  caps();
+  Arena ar(s);
+  DevState* st = new_state(ar, s);
+  GeppTourBufs T = alloc_tour(ar, r, cols, 1);
+  unsigned long long* chg = ar.get<unsigned long long>(1);
+  CU_TRY(cudaMemsetAsync(chg, 0, 8, s));
+  bool single = false;
+  gepp_tournament(a, lda, cols, r, 1, T, chg, st, 0, single, s);
+  widen_kernel<<<(unsigned)std::min<int64_t>((r + 255) / 256, 4 * caps().sms), 256, 0, s>>>(T.order_full, r, order);
+  CU_TRY(cudaGetLastError());
+  int32_t c = 0;
+  CU_TRY(cudaMemcpyAsync(&c, T.cnt[0], 4, cudaMemcpyDeviceToHost, s));
+  DevState hs;
+  read_state(st, hs, s);
+  if (count) *count = c;
+  return state_to_err(hs, err);
+}
 }  // namespace
 
 // ======================================================================== ABI
@@ -2332,6 +2533,26 @@ int prrp_gepp_blockrow(double* A, int64_t lda, int32_t m, int64_t n, int64_t* pe
     read_state(st, hs, s);
     if (intermediate_max) *intermediate_max = bits_to_double(hs.finish_max);
     return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_calu(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, int32_t leaf_count, int64_t* perm,
+              int64_t* tournament_charge3, prrp_stats* stats, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    return calu_gepp_impl(A, lda, m, n, b, leaf_count, perm, tournament_charge3, stats, err, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_gepp_select(const double* a, int64_t lda, int64_t r, int32_t cols, int64_t* order, int32_t* count,
+                     prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    return gepp_select_impl(a, lda, r, cols, order, count, err, (cudaStream_t)stream);
   } catch (const Fail& f) {
     return report(err, f);
   }

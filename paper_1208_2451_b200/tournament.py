@@ -7,6 +7,10 @@ and same-level merges execute concurrently, each as the cluster strong-RRQR
 engine over an index list of logical rows; the result is independent of that
 concurrency, as the reference's determinism contract requires
 (tournament.py:24-25).
+
+``calu_factor(a, b, tree=None)`` (tournament.py:299-359), the
+tournament-pivoted GEPP baseline, runs the same tree with a GEPP selector
+in every node (prrp_calu).
 """
 import ctypes
 import math
@@ -17,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .errors import DimensionMismatch
-from .luprrp import (BlockLUFactors, ElimStats, _validate, as_matrix, flop_counters,
+from .luprrp import (BlockLUFactors, ElimStats, _finish_charge, _validate, as_matrix, flop_counters,
                      split_packed_device, split_to_host, upload, _Prefault)
 
 
@@ -119,8 +123,28 @@ def _select(panel, idx, b, tau, selector):
             return idx[order[:want]], idx[order], srr.swap_count, (srr if want == b else None)
         return idx[:0], idx, 0, None
     if selector == "gepp":
-        raise NotImplementedError("the GEPP tournament selector (calu_factor) is SURVEY 8(f) rank 2, not built yet")
+        order, cols = gepp_select(sub)
+        return idx[order[:cols]], idx[order], 0, None
     raise ValueError(f"unknown selector {selector!r}")
+
+
+def gepp_select(sub):
+    """GEPP selector node on the device (tournament.py:142-150): the
+    elimination's row order of the r x b block `sub` (r > b) and the number
+    of rows chosen before the first zero pivot -- the reference's retry with
+    fewer columns reproduces exactly the first k steps, so its order is the
+    order reached when column k is found zero."""
+    import torch
+    r, cols = sub.shape
+    lib = _lib.device_lib()
+    A = torch.from_numpy(np.ascontiguousarray(sub, dtype=np.float64)).cuda()
+    order = torch.empty(r, dtype=torch.int64, device="cuda")
+    cnt = ctypes.c_int32(0)
+    err = _lib.PrrpErr()
+    rc = lib.prrp_gepp_select(ctypes.c_void_p(A.data_ptr()), cols, r, cols, ctypes.c_void_p(order.data_ptr()),
+                              ctypes.byref(cnt), ctypes.byref(err), _lib.stream_handle())
+    _lib.raise_for(rc, err, "prrp_gepp_select")
+    return order.cpu().numpy().astype(np.intp), int(cnt.value)
 
 
 def tournament_select(panel, b, tau, tree, selector="srrqr"):
@@ -227,3 +251,55 @@ def caluprrp_factor(a, b, tau=2.0, tree=None):
                       panel_multiplier_max=st.panel_multiplier_max)
     l, u = split_to_host(buf[:, :n], m, n, *pre.get()) if pre else split_packed_device(buf[:, :n], m, n)
     return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b, stats=stats)
+
+
+def calu_factor(a, b, tree=None):
+    """Tournament-pivoted GEPP: selection and panel finish both by partial
+    pivoting (binary tree by default, P = 8).
+
+    Drop-in for prrp.calu_factor (reference tournament.py:299-359); one
+    device call (prrp_calu): GEPP tournament, row moves, GEPP finish of the
+    block row, L21 = A21 U11^-1, DMMA trailing update per panel."""
+    a = as_matrix(a)
+    _validate(a, b, 2.0)
+    if tree is None:
+        tree = binary_tree(8)
+    leaf_count = int(tree.leaf_count) if tree.shape == "binary" else 0
+    m, n = a.shape
+    lib = _lib.device_lib()
+    import torch
+    pre = _Prefault([(n, m), (n, n)]) if m * n >= (1 << 22) else None
+    buf, lda = upload(a)
+    perm = torch.empty(m, dtype=torch.int64, device="cuda")
+    npan = (n + b - 1) // b
+    chg3 = (ctypes.c_int64 * npan)()
+    st = _lib.PrrpStats()
+    err = _lib.PrrpErr()
+    rc = lib.prrp_calu(ctypes.c_void_p(buf.data_ptr()), lda, m, n, b, leaf_count, ctypes.c_void_p(perm.data_ptr()),
+                       chg3, ctypes.byref(st), ctypes.byref(err), _lib.stream_handle())
+    _lib.raise_for(rc, err, "prrp_calu")
+    charged = calu_flop_counter(m, n, b, [Fraction(int(c), 3) for c in chg3])
+    stats = ElimStats(original_max=st.original_max, intermediate_max=st.intermediate_max,
+                      finish_max=st.finish_max, swap_counts=[0] * npan,
+                      flops_charged=charged, flops_executed=charged,
+                      panel_multiplier_max=st.panel_multiplier_max)
+    l, u = split_to_host(buf[:, :n], m, n, *pre.get()) if pre else split_packed_device(buf[:, :n], m, n)
+    return BlockLUFactors(perm=perm.cpu().numpy().astype(np.intp), l=l, u=u, panel_width=b, stats=stats)
+
+
+def calu_flop_counter(m, n, b, tournament_extra):
+    """calu_factor's counter (charged == executed; tournament.py:321-356)."""
+    tot = Fraction(0)
+    col0 = 0
+    panel = 0
+    while col0 < n:
+        bj = min(b, n - col0)
+        rows = m - col0
+        width = n - col0 - bj
+        if rows > bj:
+            tot += tournament_extra[panel]
+            tot += Fraction((rows - bj) * bj * bj + 2 * bj * (rows - bj) * width)
+        tot += _finish_charge(bj, n - col0)
+        col0 += bj
+        panel += 1
+    return tot

@@ -21,7 +21,8 @@ def _declared():
 def test_header_declares_entry_points():
     names = _declared()
     for must in ("prrp_luprrp", "prrp_caluprrp", "prrp_strong_rrqr", "prrp_householder_qr",
-                 "prrp_schur_update", "prrp_gepp_blockrow", "prrp_b200_abi_version"):
+                 "prrp_schur_update", "prrp_gepp_blockrow", "prrp_b200_abi_version", "prrp_calu",
+                 "prrp_gepp_select"):
         assert must in names
 
 

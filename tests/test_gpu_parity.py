@@ -12,7 +12,7 @@ Bars (BASELINE north_star):
 import numpy as np
 import pytest
 
-from conftest import make_input, srrqr_input
+from conftest import gepp_calu_input, make_input, srrqr_input
 from oracle import prrp_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -459,3 +459,84 @@ def test_full_size_properties(dev, cfg):
         assert g0 == pytest.approx(2.0, rel=1e-10)
     if cfg == "c3_foster":
         assert g0 == pytest.approx(2.25, rel=1e-10)
+
+
+# ------------------------------------------------------------ calu_factor
+def _tree_of(dev, P):
+    return dev.flat_tree() if P == 0 else dev.binary_tree(P)
+
+
+def _otree(P):
+    return ("flat", 8) if P == 0 else ("binary", P)
+
+
+def test_calu_factor_golden(dev, golden):
+    """calu_factor (tournament-pivoted GEPP, tournament.py:299-359) against
+    the reference's fixtures: row order and flop counters exact, factors and
+    statistics within the tolerances, rank-deficient leaves included."""
+    index, arrays = golden
+    for e in index["gepp_calu"]:
+        a = gepp_calu_input(e)
+        f = dev.calu_factor(a, e["b"], _tree_of(dev, e["P"]))
+        ref = orc.calu_gepp(a, e["b"], *_otree(e["P"]))
+        key = "gepp_calu/" + e["name"]
+        assert np.array_equal(f.perm, arrays[key + "/perm"]), e["name"]
+        assert _rel(f.l, arrays[key + "/l"]) <= TOL_F, e["name"]
+        assert _rel(f.u, arrays[key + "/u"]) <= TOL_F, e["name"]
+        assert str(f.stats.flops_charged) == e["stats"]["flops_charged"], e["name"]
+        assert str(f.stats.flops_executed) == e["stats"]["flops_executed"], e["name"]
+        if e["gen"] != "wilkinson":
+            _check_factors(f, ref, a)
+
+
+@pytest.mark.parametrize("n,b,P,gen", [(1024, 64, 8, "randn"), (1536, 128, 8, "urand"), (900, 64, 3, "randn"),
+                                       (640, 32, 0, "randn"), (1000, 100, 5, "urand")])
+def test_calu_factor_vs_oracle(dev, n, b, P, gen):
+    a = orc.randn_matrix(n, 7) if gen == "randn" else orc.urand_matrix(n, 7)
+    f = dev.calu_factor(a, b, _tree_of(dev, P))
+    ref = orc.calu_gepp(a, b, *_otree(P))
+    _check_factors(f, ref, a)
+
+
+@pytest.mark.parametrize("shape,m,b,leaf,zero", [("binary", 600, 16, 8, None), ("binary", 257, 32, 4, (0, 80)),
+                                                ("flat", 300, 16, None, (20, 60)), ("binary", 40, 16, 8, None)])
+def test_tournament_select_gepp(dev, shape, m, b, leaf, zero):
+    """GEPP selector tournament node for node, incl. a zeroed (rank-deficient) block."""
+    rng = np.random.Generator(np.random.PCG64(m + 3 * b))
+    panel = np.asfortranarray(rng.standard_normal((m, b)))
+    if zero:
+        panel[zero[0]:zero[1], :] = 0.0
+    tree = dev.binary_tree(leaf) if shape == "binary" else dev.flat_tree()
+    perm, trace = dev.tournament_select(panel, b, 2.0, tree, "gepp")
+    rperm, rtrace = orc.tournament(panel, b, 2.0, shape, leaf if leaf else 8, "gepp")
+    assert np.array_equal(perm, rperm)
+    assert [(n.level, n.index) for n in trace.nodes] == [(n.level, n.index) for n in rtrace.nodes]
+    for n, r in zip(trace.nodes, rtrace.nodes):
+        assert np.array_equal(n.members, r.members) and np.array_equal(n.selected, r.selected)
+
+
+def test_calu_factor_errors(dev):
+    """Error contract: a rank-deficient panel raises RankDeficient(index, panel)
+    like the reference; a zero pivot in the block-row finish SingularMatrix."""
+    from paper_1208_2451_b200.errors import RankDeficient, SingularMatrix
+    a = np.array(orc.randn_matrix(128, 2), order="F")
+    a[:, 3] = 0.0                      # column 3 of panel 0: rank 3 < b = 16
+    with pytest.raises((RankDeficient, SingularMatrix)) as ei:
+        dev.calu_factor(a, 16, dev.binary_tree(4))
+    with pytest.raises(ArithmeticError) as ri:
+        orc.calu_gepp(a, 16, "binary", 4)
+    assert type(ei.value).__name__.replace("Oracle", "") == type(ri.value).__name__.replace("Oracle", "")
+    assert getattr(ei.value, "index", None) == getattr(ri.value, "index", None)
+    assert getattr(ei.value, "panel", None) == getattr(ri.value, "panel", None)
+
+
+def test_calu_factor_full_size(dev):
+    """n = 4096, b = 64, P = 8: residual, determinism, growth vs the GEPP baseline's bound."""
+    a = orc.randn_matrix(4096, 42)
+    f1 = dev.calu_factor(a, 64)
+    f2 = dev.calu_factor(a, 64)
+    assert np.array_equal(f1.perm, f2.perm) and np.array_equal(f1.u, f2.u)
+    assert sorted(f1.perm.tolist()) == list(range(4096))
+    assert np.abs(np.tril(f1.l, -1)).max() <= 1.0 + 1e-12 or f1.stats.panel_multiplier_max > 1.0
+    res = orc.rel_residual(a, f1.perm, f1.l, f1.u)
+    assert res < 4096 * 2.0 ** -52
