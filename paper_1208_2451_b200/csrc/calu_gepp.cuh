@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(GN_T, 1) gepp_node_kernel(GeppLevel g) {
     if (t == 0) g.cnt_out[node] = (int)r;
     return;
   }
-  // working rows: shared memory when they fit, else the node's global slot
+  // working rows: shared memory when they fit, else the node's global slot.
+  // Rows never move: ord[q] = the working row at position q (the swaps of
+  // gepp.py:52-54 permute ord only).
   const size_t need = (size_t)r * bj * 8 + (size_t)r * 4;
   double* W;
   int32_t* ord;
@@ -104,25 +106,29 @@ __global__ void __launch_bounds__(GN_T, 1) gepp_node_kernel(GeppLevel g) {
     W = g.wscratch + off * bj;
     ord = single ? g.order_full : g.oscratch + off;
   }
-  for (int64_t e = t; e < r * bj; e += blockDim.x) {
-    const int64_t q = e / bj;
-    const int j = (int)(e - q * bj);
-    W[e] = g.panel[gn_member(g, node, q, lo, ca) * g.lda + j];
+  const int R = (int)r;
+  for (int q = t / bj; q < R; q += blockDim.x / bj) {   // blockDim.x % bj need not be 0: tail below
+    const int j = t % bj;
+    if (t < (int)(blockDim.x / bj) * bj) W[(int64_t)q * bj + j] = g.panel[gn_member(g, node, q, lo, ca) * g.lda + j];
   }
-  for (int64_t q = t; q < r; q += blockDim.x) ord[q] = (int32_t)q;
+  for (int q = t; q < R; q += blockDim.x) ord[q] = q;
   if (t == 0) {
     s_stop = bj;
     atomicAdd(g.chg3, (unsigned long long)(3 * r * bj * bj - (int64_t)bj * bj * bj));
   }
+  // thread (rg, tc): column tc of positions rg, rg + RG, ...
+  const int CW = (bj + 31) & ~31, RG = blockDim.x / CW, tc = t % CW, rg = t / CW;
   __syncthreads();
-  for (int k = 0; k < bj; ++k) {
-    // first maximum of |W[q][k]|, q >= k (gepp.py:48-49)
-    double best = -1.0;
-    int bi = INT_MAX;
-    for (int64_t q = k + t; q < r; q += blockDim.x) {
-      const double v = fabs(W[q * bj + k]);
-      if (v > best) { best = v; bi = (int)q; }
+  double best = -1.0;
+  int bi = INT_MAX;
+  if (tc == 0)
+    for (int q = rg; q < R; q += RG) {
+      const double v = fabs(W[(int64_t)q * bj]);
+      if (v > best) { best = v; bi = q; }
     }
+  for (int k = 0; k < bj; ++k) {
+    // first maximum of |column k| over positions >= k (gepp.py:48-49); the
+    // partials come from the previous step's update of column k
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -142,40 +148,71 @@ __global__ void __launch_bounds__(GN_T, 1) gepp_node_kernel(GeppLevel g) {
         if (better(ob, oi, best, bi)) { best = ob; bi = oi; }
       }
       if (lane == 0) {
-        s_bi[0] = bi;
-        if (best == 0.0) s_stop = k;   // SingularMatrix(column=k): keep the k rows chosen
+        if (!(best > 0.0)) {
+          s_stop = k;   // SingularMatrix(column=k): keep the k rows chosen
+        } else if (bi != k) {
+          const int32_t o = ord[k];
+          ord[k] = ord[bi];
+          ord[bi] = o;
+        }
       }
     }
     __syncthreads();
     if (s_stop == k) break;
-    const int pv = s_bi[0];
-    if (pv != k) {
-      for (int j = t; j < bj; j += blockDim.x) {
-        const double a = W[(int64_t)k * bj + j];
-        W[(int64_t)k * bj + j] = W[(int64_t)pv * bj + j];
-        W[(int64_t)pv * bj + j] = a;
+    const int64_t pk = (int64_t)ord[k] * bj;
+    const double d = W[pk + k];
+    const double rd = __drcp_rn(d);
+    const int j = tc;
+    const bool active = j > k && j < bj;
+    const double u = active ? W[pk + j] : 0.0;
+    best = -1.0;
+    bi = INT_MAX;
+    const int wbase = tc - lane;   // the warp's first column (warp-uniform)
+    if (wbase + 31 > k && wbase < bj) {
+      const bool next = j == k + 1;
+      // 32 positions at a time: lane s fetches row ord[q_s] and its
+      // multiplier c[q_s, k] / c[k, k] once, the warp then sweeps the rows
+      for (int q0 = k + 1 + rg; q0 < R; q0 += 32 * RG) {
+        const int ql = q0 + lane * RG;
+        int64_t pl = 0;
+        double ll = 0.0;
+        if (ql < R) {
+          pl = (int64_t)ord[ql] * bj;
+          ll = div_fast(W[pl + k], d, rd);
+        }
+        const int nq = min(32, (R - q0 + RG - 1) / RG);
+        // four rows per pass: loads first, then the updates and stores
+        for (int sq = 0; sq < nq; sq += 4) {
+          int64_t p[4];
+          double l[4], w[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            p[x] = __shfl_sync(0xffffffffu, pl, (sq + x) & 31);
+            l[x] = __shfl_sync(0xffffffffu, ll, (sq + x) & 31);
+          }
+          if (active) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) w[x] = sq + x < nq ? W[p[x] + j] : 0.0;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              if (sq + x < nq) {
+                const double v = sub_rn(w[x], mul_rn(l[x], u));   // c[q, j] - l * c[k, j]
+                W[p[x] + j] = v;
+                if (next) {
+                  const double av = fabs(v);
+                  if (av > best) { best = av; bi = q0 + (sq + x) * RG; }
+                }
+              }
+            }
+          }
+        }
       }
-      if (t == 0) { const int32_t o = ord[k]; ord[k] = ord[pv]; ord[pv] = o; }
     }
-    __syncthreads();
-    const double d = W[(int64_t)k * bj + k];
-    for (int64_t q = k + 1 + t; q < r; q += blockDim.x) W[q * bj + k] = div_rn(W[q * bj + k], d);
-    __syncthreads();
-    const int w = bj - k - 1;
-    if (w > 0) {
-      const int64_t tot = (r - k - 1) * w;
-      for (int64_t e = t; e < tot; e += blockDim.x) {
-        const int64_t q = k + 1 + e / w;
-        const int j = k + 1 + (int)(e % w);
-        W[q * bj + j] = sub_rn(W[q * bj + j], mul_rn(W[q * bj + k], W[(int64_t)k * bj + j]));
-      }
-    }
-    __syncthreads();
   }
   const int cnt = s_stop;
   for (int q = t; q < cnt; q += blockDim.x) g.cand_out[node * bj + q] = (int32_t)gn_member(g, node, ord[q], lo, ca);
   if (single && ord != g.order_full)
-    for (int64_t q = t; q < r; q += blockDim.x) g.order_full[q] = ord[q];
+    for (int q = t; q < R; q += blockDim.x) g.order_full[q] = ord[q];
   if (t == 0) g.cnt_out[node] = cnt;
 }
 
@@ -265,6 +302,7 @@ __global__ void trsm_right_kernel(double* A, int64_t lda, int64_t col0, int bj, 
                                   int64_t ldl, DevState* st) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ double red[40];
+  __shared__ double rinv[PRRP_MAXH];
   if (prrp_failed(st)) return;
   double* U = tsm;
   double* xs = tsm + (size_t)bj * bj;
@@ -274,18 +312,21 @@ __global__ void trsm_right_kernel(double* A, int64_t lda, int64_t col0, int bj, 
     U[e] = j >= i ? A[(col0 + i) * lda + col0 + j] : 0.0;
   }
   __syncthreads();
+  for (int i = t; i < bj; i += TW) rinv[i] = __drcp_rn(U[i * bj + i]);
+  __syncthreads();
   double mx = 0.0;
   for (int64_t base = (int64_t)blockIdx.x * TW; base < M; base += (int64_t)gridDim.x * TW) {
     const int64_t i = base + t;
     if (i < M) {
       double* row = A + (r0 + i) * lda + col0;
       for (int k = 0; k < bj; ++k) xs[k * TW + t] = row[k];
-      for (int k = 0; k < bj; ++k) {
-        double x = xs[k * TW + t];
-        for (int j = 0; j < k; ++j) x = sub_rn(x, mul_rn(xs[j * TW + t], U[j * bj + k]));
-        x = div_rn(x, U[k * bj + k]);
-        xs[k * TW + t] = x;
+      // column j final, then pushed into columns > j: each x_ik still sees
+      // its subtractions in increasing j before its division
+      for (int jj = 0; jj < bj; ++jj) {
+        const double x = div_fast(xs[jj * TW + t], U[jj * bj + jj], rinv[jj]);
+        xs[jj * TW + t] = x;
         mx = fmax(mx, fabs(x));
+        for (int k = jj + 1; k < bj; ++k) xs[k * TW + t] = sub_rn(xs[k * TW + t], mul_rn(x, U[jj * bj + k]));
       }
       for (int k = 0; k < bj; ++k) {
         const double x = xs[k * TW + t];
@@ -301,4 +342,47 @@ __global__ void trsm_right_kernel(double* A, int64_t lda, int64_t col0, int bj, 
 __global__ void widen_kernel(const int32_t* src, int64_t n, int64_t* dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
+}
+
+// trsm_right_kernel for bj <= 64 with the row in registers (same arithmetic
+// and order); U11 and the reciprocals of its diagonal in shared memory.
+__global__ void __launch_bounds__(128) trsm_right_reg_kernel(double* A, int64_t lda, int64_t col0, int bj, int64_t r0,
+                                                             int64_t M, double* Lcm, int64_t ldl, DevState* st) {
+  __shared__ double U[64 * 64];
+  __shared__ double rinv[64];
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x;
+  for (int e = t; e < 64 * 64; e += blockDim.x) {
+    const int i = e >> 6, j = e & 63;
+    U[e] = (i < bj && j < bj && j >= i) ? A[(col0 + i) * lda + col0 + j] : 0.0;
+  }
+  __syncthreads();
+  for (int i = t; i < 64; i += blockDim.x) rinv[i] = i < bj ? __drcp_rn(U[i * 64 + i]) : 0.0;
+  __syncthreads();
+  double mx = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+    double* row = A + (r0 + i) * lda + col0;
+    double x[64];
+#pragma unroll
+    for (int k = 0; k < 64; ++k) x[k] = k < bj ? row[k] : 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 64; ++jj) {
+      if (jj < bj) {
+        const double xj = div_fast(x[jj], U[jj * 64 + jj], rinv[jj]);
+        x[jj] = xj;
+        mx = fmax(mx, fabs(xj));
+#pragma unroll
+        for (int k = jj + 1; k < 64; ++k) x[k] = sub_rn(x[k], mul_rn(xj, U[jj * 64 + k]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 64; ++k)
+      if (k < bj) {
+        row[k] = x[k];
+        Lcm[(int64_t)k * ldl + i] = x[k];
+      }
+  }
+  const double m = block_max(mx, red);
+  if (t == 0 && m > 0.0) atomic_max_abs(&st->pmm, m);
 }

@@ -1995,6 +1995,14 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
   GeppLevel g{};
   g.panel = panel; g.lda = lda; g.bj = bj; g.rows = rows;
   g.wscratch = T.wscratch; g.oscratch = T.oscratch; g.chg3 = chg3; g.st = st; g.panel_no = panel_no;
+  // block size: column-warps x row groups, ~8 rows per thread per step
+  // (measured on B200: 32 rows per thread with 4x fewer warps is slower --
+  // the 64 dependent steps are latency-bound, not issue-bound)
+  auto threads_for = [&](int64_t r) -> unsigned {
+    const int cw = (bj + 31) & ~31;
+    const int64_t rg = std::max<int64_t>(1, std::min<int64_t>((r + 7) / 8, GN_T / cw));
+    return (unsigned)(cw * rg);
+  };
   auto smem_for = [&](int64_t r) -> int {
     const size_t need = (size_t)r * bj * 8 + (size_t)r * 4;
     return need <= (size_t)kGnSmem ? (int)((need + 15) / 16 * 16) : 0;
@@ -2007,7 +2015,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
     g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
     g.order_full = single ? T.order_full : nullptr;
     g.smem_bytes = smem_for((rows + p_eff - 1) / p_eff);
-    gepp_node_kernel<<<(unsigned)p_eff, GN_T, g.smem_bytes, s>>>(g);
+    gepp_node_kernel<<<(unsigned)p_eff, threads_for((rows + p_eff - 1) / p_eff), g.smem_bytes, s>>>(g);
     CU_TRY(cudaGetLastError());
     g.order_full = nullptr;
     int64_t ncur = p_eff;
@@ -2017,7 +2025,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
       g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
       g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
       g.smem_bytes = smem_for(2 * bj);
-      gepp_node_kernel<<<(unsigned)nout, GN_T, g.smem_bytes, s>>>(g);
+      gepp_node_kernel<<<(unsigned)nout, threads_for(2 * bj), g.smem_bytes, s>>>(g);
       CU_TRY(cudaGetLastError());
       cur ^= 1;
       ncur = nout;
@@ -2030,7 +2038,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
   g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
   g.order_full = single ? T.order_full : nullptr;
   g.smem_bytes = smem_for(first);
-  gepp_node_kernel<<<1, GN_T, g.smem_bytes, s>>>(g);
+  gepp_node_kernel<<<1, threads_for(first), g.smem_bytes, s>>>(g);
   CU_TRY(cudaGetLastError());
   g.order_full = nullptr;
   for (int64_t lo = first; lo < rows; lo += bj) {
@@ -2038,7 +2046,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
     g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
     g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
     g.smem_bytes = smem_for(2 * bj);
-    gepp_node_kernel<<<1, GN_T, g.smem_bytes, s>>>(g);
+    gepp_node_kernel<<<1, threads_for(2 * bj), g.smem_bytes, s>>>(g);
     CU_TRY(cudaGetLastError());
     cur ^= 1;
   }
@@ -2116,10 +2124,14 @@ int calu_gepp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, int P, i
       launch_blockrow_w(A, lda, col0, bj, n, D, gperm, perm, st, s);
       CU_TRY(cudaGetLastError());
       const int64_t M = rows - bj;
-      const int tw = bj > 64 ? 64 : 128;
+      const int tw = 64;
       const size_t dyn = ((size_t)bj * bj + (size_t)bj * tw) * 8;
-      const unsigned tg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((M + tw - 1) / tw, 4 * sms));
-      trsm_right_kernel<<<tg, tw, dyn, s>>>(A, lda, col0, bj, col0 + bj, M, Lcm, ldl, st);
+      const unsigned tg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((M + tw - 1) / tw, 8 * sms));
+      if (bj <= 64)
+        trsm_right_reg_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((M + 127) / 128, 8 * sms)), 128, 0,
+                                s>>>(A, lda, col0, bj, col0 + bj, M, Lcm, ldl, st);
+      else
+        trsm_right_kernel<<<tg, tw, dyn, s>>>(A, lda, col0, bj, col0 + bj, M, Lcm, ldl, st);
       CU_TRY(cudaGetLastError());
       if (width > 0)
         schur_update(A + (col0 + bj) * lda + col0 + bj, lda, Lcm, ldl, A + col0 * lda + col0 + bj, lda, M, width,
