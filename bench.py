@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--secondary-b", type=int, default=128, help="also report this panel width (0 = off)")
     ap.add_argument("--calu-n", type=int, default=16384,
                     help="also time CALU_PRRP (BASELINE config 4: randn(n), b=64, binary tree P=8); 0 = off")
+    ap.add_argument("--gcalu-n", type=int, default=8192, help="calu_factor (GEPP tournament) size (0 = off)")
     ap.add_argument("--calu5-n", type=int, default=32768,
                     help="also time CALU_PRRP (BASELINE config 5 on 1 GPU: U(-1,1), b=128, P=8); 0 = off")
     return ap.parse_args()
@@ -283,7 +284,7 @@ def run_device(args):
         extra["secondary"] = {"b": args.secondary_b, "ms_per_step": ms2,
                               "value": ws * lu_flops(n) / (ms2 * 1e-3) / 1e9, "unit": UNIT}
 
-    def calu_line(cn, cb, gen, label, reps=2):
+    def calu_line(cn, cb, gen, label, reps=2, gepp=False):
         """CALU_PRRP (binary tree, P = 8) on a device-resident matrix; the first two
         calls capture and upload the factorization's CUDA graph (untimed)."""
         import ctypes
@@ -304,9 +305,14 @@ def run_device(args):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rc = lib.prrp_caluprrp(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, float(tau), 8,
-                                   ctypes.c_void_p(cperm.data_ptr()), sw, chg, ctypes.byref(cst), ctypes.byref(cerr),
+            if gepp:   # calu_factor: the GEPP-tournament baseline (one stream, no graph)
+                rc = lib.prrp_calu(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, 8,
+                                   ctypes.c_void_p(cperm.data_ptr()), chg, ctypes.byref(cst), ctypes.byref(cerr),
                                    _lib.stream_handle())
+            else:
+                rc = lib.prrp_caluprrp(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, float(tau), 8,
+                                       ctypes.c_void_p(cperm.data_ptr()), sw, chg, ctypes.byref(cst),
+                                       ctypes.byref(cerr), _lib.stream_handle())
             e1.record()
             e1.synchronize()
             _lib.raise_for(rc, cerr, "prrp_caluprrp")
@@ -316,6 +322,11 @@ def run_device(args):
         del cprist, cwork, cperm
         torch.cuda.empty_cache()
         v = lu_flops(cn) / (cms * 1e-3) / 1e9
+        if gepp:
+            return {"workload": f"calu_factor (GEPP tournament) {label}({cn}, seed {args.seed}), b={cb}, binary "
+                                "tree P=8, 1 GPU", "ms_per_step": cms, "value": v, "unit": UNIT,
+                    "growth_factor": cst.intermediate_max / cst.original_max,
+                    "timing": f"CUDA events around prrp_calu, mean of {reps} steps after 2 untimed"}
         return {"workload": f"CALU_PRRP {label}({cn}, seed {args.seed}), b={cb}, tau={tau}, binary tree P=8, 1 GPU",
                 "ms_per_step": cms, "value": v, "unit": UNIT,
                 "fp64_peak_fraction": (v / 1e3) / pk.value if pk.value else None,
@@ -329,6 +340,9 @@ def run_device(args):
     # BASELINE config 5 on one GPU: CALU_PRRP, U(-1,1) n = 32768 (8 GiB), b = 128, P = 8
     if args.calu5_n and rank == 0:
         extra["calu_config5"] = calu_line(args.calu5_n, 128, "urand", "urand")
+    # the reference's tournament-pivoted GEPP baseline (tournament.py:299-359), SURVEY 8(f)
+    if args.gcalu_n and rank == 0:
+        extra["calu_factor"] = calu_line(args.gcalu_n, 64, "randn", "randn", gepp=True)
 
     # end to end through the public API: host input in pinned memory -> device -> factors on host
     e2e = None
