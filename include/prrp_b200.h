@@ -152,6 +152,14 @@ int prrp_calu(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, int32_t l
 int prrp_gepp_select(const double* a, int64_t lda, int64_t r, int32_t cols, int64_t* order,
                      int32_t* count, prrp_err* err, void* stream);
 
+/* gepp_factor of an m x n row-major device matrix of any shape (gepp.py:39-65),
+ * in place: packed L\U (unit lower multipliers below the diagonal), row
+ * order perm (device int64[m]), running max of the live trailing block
+ * (intermediate_max) and max|A| (original_max), host doubles.  A zero pivot
+ * column k -> PRRP_ERR_SINGULAR_MATRIX with err->column = k. */
+int prrp_gepp(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* intermediate_max,
+              double* original_max, prrp_err* err, void* stream);
+
 /* Strong RRQR of an h x p matrix `a` (column-major, lda >= h) with leading
  * block size bsel <= h and threshold tau — replaces prrp.strong_rrqr
  * (pivoted_qr.py:113-147).  Outputs (device, column-major): R h x p (ldr=h),

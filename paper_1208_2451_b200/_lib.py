@@ -65,6 +65,7 @@ SIGNATURES = {
     "prrp_gepp_blockrow": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),
     "prrp_calu": ([_P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_gepp_select": ([_P, _I64, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_gepp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
 }
 
 _lib = None

@@ -33,6 +33,7 @@
 #include "schur.cuh"
 #include "calu.cuh"
 #include "calu_gepp.cuh"
+#include "gepp_full.cuh"
 
 namespace {
 
@@ -2178,6 +2179,33 @@ int gepp_select_impl(const double* a, int64_t lda, int64_t r, int cols, int64_t*
   if (count) *count = c;
   return state_to_err(hs, err);
 }
+
+// gepp_factor of any shape (gepp.py:39-65): unblocked, two launches per step.
+int gepp_full_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* imax, double* omax,
+                   prrp_err* err, cudaStream_t s) {
+  if (m < 1 || n < 1) fail(PRRP_ERR_DIM, "gepp needs a non-empty matrix");
+  if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
+  caps();
+  const int sms = caps().sms;
+  Arena ar(s);
+  DevState* st = new_state(ar, s);
+  iota_kernel<<<sms, 256, 0, s>>>(perm, m);
+  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  const int64_t steps = std::min(m, n);
+  for (int64_t k = 0; k < steps; ++k) {
+    gf_pivot_kernel<<<1, 1024, 0, s>>>(A, lda, m, n, k, perm, st);
+    if (k + 1 < m) {
+      const int64_t groups = (m - k - 1 + GF_ROWS - 1) / GF_ROWS;
+      gf_update_kernel<<<(unsigned)std::min<int64_t>(groups, 8 * sms), 256, 0, s>>>(A, lda, m, n, k, st);
+    }
+  }
+  CU_TRY(cudaGetLastError());
+  DevState hs;
+  read_state(st, hs, s);
+  if (imax) *imax = bits_to_double(hs.inter_max);
+  if (omax) *omax = bits_to_double(hs.orig_max);
+  return state_to_err(hs, err);
+}
 }  // namespace
 
 // ======================================================================== ABI
@@ -2565,6 +2593,16 @@ int prrp_gepp_select(const double* a, int64_t lda, int64_t r, int32_t cols, int6
   clear_err(err);
   try {
     return gepp_select_impl(a, lda, r, cols, order, count, err, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_gepp(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* intermediate_max,
+              double* original_max, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    return gepp_full_impl(A, lda, m, n, perm, intermediate_max, original_max, err, (cudaStream_t)stream);
   } catch (const Fail& f) {
     return report(err, f);
   }

@@ -1,8 +1,11 @@
 """Partial-pivoting LU of a block row on the device (reference gepp.py:39-65).
 
-The factorizations use GEPP only as the finisher of the b x w block row
-(luprrp.py:107-127); this entry point exposes that device path for
-m <= 128 rows (the standalone GEPP baseline is out of scope)."""
+The factorizations use GEPP as the finisher of the b x w block row
+(luprrp.py:107-127): block rows (m <= 128 <= ... n >= m) take that fused
+device path (prrp_gepp_blockrow).  Every other shape -- the standalone GEPP
+baseline of the paper's comparisons -- runs the unblocked device
+elimination prrp_gepp (one pivot and one update launch per step, same
+arithmetic as the reference)."""
 import ctypes
 from dataclasses import dataclass
 
@@ -28,24 +31,34 @@ class GeppFactors:
 
 
 def gepp_factor(a):
-    """Factor an m x n block row (m <= min(n, 128)) with partial pivoting."""
+    """Factor an m x n matrix (any shape) with partial pivoting (gepp.py:39-65)."""
     import torch
     c = np.asarray(a, dtype=np.float64)
     if c.ndim != 2:
         raise DimensionMismatch(f"expected a 2-D array, got ndim={c.ndim}")
     m, n = c.shape
-    if not (1 <= m <= 128 and n >= m):
-        raise NotImplementedError("device GEPP covers the b x w block rows of the factorizations (m <= 128, n >= m)")
     lib = _lib.device_lib()
-    A = torch.from_numpy(np.ascontiguousarray(c)).cuda()
+    if m == 0 or n == 0:
+        raise DimensionMismatch("gepp_factor needs a non-empty matrix")
+    s = min(m, n)
+    ld = n + (n & 1)
+    A = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    A[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(c)))
     P = torch.empty(m, dtype=torch.int64, device="cuda")
     im = ctypes.c_double(0)
+    om = ctypes.c_double(0)
     err = _lib.PrrpErr()
-    rc = lib.prrp_gepp_blockrow(ctypes.c_void_p(A.data_ptr()), n, m, n, ctypes.c_void_p(P.data_ptr()),
-                                ctypes.byref(im), ctypes.byref(err), _lib.stream_handle())
+    if m <= 128 and n >= m:
+        rc = lib.prrp_gepp_blockrow(ctypes.c_void_p(A.data_ptr()), ld, m, n, ctypes.c_void_p(P.data_ptr()),
+                                    ctypes.byref(im), ctypes.byref(err), _lib.stream_handle())
+        om.value = float(np.abs(c).max())
+    else:
+        rc = lib.prrp_gepp(ctypes.c_void_p(A.data_ptr()), ld, m, n, ctypes.c_void_p(P.data_ptr()),
+                           ctypes.byref(im), ctypes.byref(om), ctypes.byref(err), _lib.stream_handle())
     _lib.raise_for(rc, err, "gepp_factor")
-    packed = A.cpu().numpy()
-    l = np.tril(packed[:, :m], -1) + np.eye(m)
-    u = np.triu(packed)
+    packed = A[:, :n].cpu().numpy()
+    l = np.tril(packed[:, :s], -1)
+    np.fill_diagonal(l, 1.0)
+    u = np.triu(packed[:s, :])
     return GeppFactors(perm=P.cpu().numpy().astype(np.intp), l=np.asfortranarray(l), u=np.asfortranarray(u),
-                       intermediate_max=float(im.value), original_max=float(np.abs(c).max()) if c.size else 0.0)
+                       intermediate_max=float(im.value), original_max=float(om.value))

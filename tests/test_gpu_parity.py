@@ -540,3 +540,27 @@ def test_calu_factor_full_size(dev):
     assert np.abs(np.tril(f1.l, -1)).max() <= 1.0 + 1e-12 or f1.stats.panel_multiplier_max > 1.0
     res = orc.rel_residual(a, f1.perm, f1.l, f1.u)
     assert res < 4096 * 2.0 ** -52
+
+
+@pytest.mark.parametrize("m,n", [(300, 300), (500, 200), (150, 400), (1024, 1024), (64, 200), (257, 3)])
+def test_gepp_factor_any_shape_bit_exact(dev, m, n):
+    """gepp_factor (gepp.py:39-65) of any shape against the oracle: row order,
+    L, U and both growth statistics bit for bit."""
+    rng = np.random.Generator(np.random.PCG64(m * 7 + n))
+    a = rng.standard_normal((m, n))
+    g, r = dev.gepp_factor(a), orc.gepp(a)
+    assert np.array_equal(g.perm, r.perm)
+    assert np.array_equal(g.l, r.l) and np.array_equal(g.u, r.u)
+    assert g.intermediate_max == r.intermediate_max and g.original_max == r.original_max
+
+
+def test_gepp_factor_singular_column(dev):
+    from paper_1208_2451_b200.errors import SingularMatrix
+    a = np.array(orc.randn_matrix(200, 4), order="F")
+    a[:, 17] = a[:, 3]            # column 17 becomes exactly dependent only after elimination: use a zero column
+    a[:, 17] = 0.0
+    with pytest.raises(SingularMatrix) as ei:
+        dev.gepp_factor(a)
+    with pytest.raises(ArithmeticError) as ri:
+        orc.gepp(a)
+    assert ei.value.column == ri.value.column == 17
