@@ -77,12 +77,13 @@ __global__ void __launch_bounds__(256) gf_update_kernel(double* A, int64_t lda, 
     }
     __syncthreads();
     if (w > 0) {
-      for (int64_t e = t; e < (int64_t)nr * w; e += blockDim.x) {
-        const int r = (int)(e / w);
-        const int64_t j = k + 1 + (e - (int64_t)r * w);
-        const double v = sub_rn(A[(q0 + r) * lda + j], mul_rn(s_l[r], A[k * lda + j]));
-        A[(q0 + r) * lda + j] = v;
-        mx = fmax(mx, fabs(v));
+      for (int64_t j = k + 1 + t; j < n; j += blockDim.x) {
+        const double u = A[k * lda + j];
+        for (int r = 0; r < nr; ++r) {
+          const double v = sub_rn(A[(q0 + r) * lda + j], mul_rn(s_l[r], u));
+          A[(q0 + r) * lda + j] = v;
+          mx = fmax(mx, fabs(v));
+        }
       }
     }
   }
