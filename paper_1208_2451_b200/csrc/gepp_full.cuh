@@ -77,13 +77,20 @@ __global__ void __launch_bounds__(256) gf_update_kernel(double* A, int64_t lda, 
     }
     __syncthreads();
     if (w > 0) {
+      // all GF_ROWS loads in flight before the stores (the compiler cannot
+      // reorder a load past a store to A)
       for (int64_t j = k + 1 + t; j < n; j += blockDim.x) {
         const double u = A[k * lda + j];
-        for (int r = 0; r < nr; ++r) {
-          const double v = sub_rn(A[(q0 + r) * lda + j], mul_rn(s_l[r], u));
-          A[(q0 + r) * lda + j] = v;
-          mx = fmax(mx, fabs(v));
-        }
+        double v[GF_ROWS];
+#pragma unroll
+        for (int r = 0; r < GF_ROWS; ++r) v[r] = r < nr ? A[(q0 + r) * lda + j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < GF_ROWS; ++r)
+          if (r < nr) {
+            v[r] = sub_rn(v[r], mul_rn(s_l[r], u));
+            A[(q0 + r) * lda + j] = v[r];
+            mx = fmax(mx, fabs(v[r]));
+          }
       }
     }
   }
