@@ -124,6 +124,8 @@ DeviceCaps& caps() {
     set_max_dyn((const void*)blockrow_kernel);
     set_max_dyn((const void*)compose_kernel);
     set_max_dyn((const void*)gepp_diag_kernel);
+    set_max_dyn((const void*)gepp_node_kernel);
+    set_max_dyn((const void*)trsm_right_kernel);
     for (const void* fn : {(const void*)trsm_w_kernel<1>, (const void*)trsm_w_kernel<2>, (const void*)trsm_w_kernel<3>,
                            (const void*)trsm_w_kernel<4>, (const void*)compose_w_kernel<1>, (const void*)compose_w_kernel<2>,
                            (const void*)compose_w_kernel<3>, (const void*)compose_w_kernel<4>,
@@ -1988,11 +1990,6 @@ struct GeppTourBufs {
 // Levels of one panel's tournament; returns the buffer index holding the root.
 int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int P, const GeppTourBufs& T,
                     unsigned long long* chg3, DevState* st, int panel_no, bool& single, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    CU_TRY(cudaFuncSetAttribute(gepp_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGnSmem));
-    attr = true;
-  }
   GeppLevel g{};
   g.panel = panel; g.lda = lda; g.bj = bj; g.rows = rows;
   g.wscratch = T.wscratch; g.oscratch = T.oscratch; g.chg3 = chg3; g.st = st; g.panel_no = panel_no;
@@ -2096,11 +2093,6 @@ int calu_gepp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, int P, i
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
   maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
   CU_TRY(cudaGetLastError());
-  static bool attr = false;
-  if (!attr) {
-    CU_TRY(cudaFuncSetAttribute(trsm_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
   int panel = 0;
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
