@@ -57,6 +57,9 @@ __device__ __forceinline__ int64_t gn_member(const GeppLevel& g, int node, int64
   return q < ca ? g.cand_in[q] : g.lo + (q - ca);
 }
 
+// SM: the node's rows live in shared memory (the launch guarantees they fit),
+// so the sweeps compile to LDS/STS instead of generic loads
+template <bool SM>
 __global__ void __launch_bounds__(GN_T, 1) gepp_node_kernel(GeppLevel g) {
   extern __shared__ __align__(16) double gsm[];
   __shared__ double s_best[32];
@@ -95,10 +98,9 @@ __global__ void __launch_bounds__(GN_T, 1) gepp_node_kernel(GeppLevel g) {
   // working rows: shared memory when they fit, else the node's global slot.
   // Rows never move: ord[q] = the working row at position q (the swaps of
   // gepp.py:52-54 permute ord only).
-  const size_t need = (size_t)r * bj * 8 + (size_t)r * 4;
   double* W;
   int32_t* ord;
-  if (need <= (size_t)g.smem_bytes) {
+  if (SM) {
     W = gsm;
     ord = reinterpret_cast<int32_t*>(gsm + (size_t)r * bj);
   } else {

@@ -124,7 +124,7 @@ DeviceCaps& caps() {
     set_max_dyn((const void*)blockrow_kernel);
     set_max_dyn((const void*)compose_kernel);
     set_max_dyn((const void*)gepp_diag_kernel);
-    set_max_dyn((const void*)gepp_node_kernel);
+    set_max_dyn((const void*)gepp_node_kernel<true>);
     set_max_dyn((const void*)trsm_right_kernel);
     for (const void* fn : {(const void*)trsm_w_kernel<1>, (const void*)trsm_w_kernel<2>, (const void*)trsm_w_kernel<3>,
                            (const void*)trsm_w_kernel<4>, (const void*)compose_w_kernel<1>, (const void*)compose_w_kernel<2>,
@@ -2001,6 +2001,10 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
     const int64_t rg = std::max<int64_t>(1, std::min<int64_t>((r + 7) / 8, GN_T / cw));
     return (unsigned)(cw * rg);
   };
+  auto launch_node = [&](unsigned grid, unsigned threads) {
+    if (g.smem_bytes > 0) gepp_node_kernel<true><<<grid, threads, g.smem_bytes, s>>>(g);
+    else gepp_node_kernel<false><<<grid, threads, 0, s>>>(g);
+  };
   auto smem_for = [&](int64_t r) -> int {
     const size_t need = (size_t)r * bj * 8 + (size_t)r * 4;
     return need <= (size_t)kGnSmem ? (int)((need + 15) / 16 * 16) : 0;
@@ -2013,7 +2017,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
     g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
     g.order_full = single ? T.order_full : nullptr;
     g.smem_bytes = smem_for((rows + p_eff - 1) / p_eff);
-    gepp_node_kernel<<<(unsigned)p_eff, threads_for((rows + p_eff - 1) / p_eff), g.smem_bytes, s>>>(g);
+    launch_node((unsigned)p_eff, threads_for((rows + p_eff - 1) / p_eff));
     CU_TRY(cudaGetLastError());
     g.order_full = nullptr;
     int64_t ncur = p_eff;
@@ -2023,7 +2027,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
       g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
       g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
       g.smem_bytes = smem_for(2 * bj);
-      gepp_node_kernel<<<(unsigned)nout, threads_for(2 * bj), g.smem_bytes, s>>>(g);
+      launch_node((unsigned)nout, threads_for(2 * bj));
       CU_TRY(cudaGetLastError());
       cur ^= 1;
       ncur = nout;
@@ -2036,7 +2040,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
   g.cand_out = T.cand[0]; g.cnt_out = T.cnt[0];
   g.order_full = single ? T.order_full : nullptr;
   g.smem_bytes = smem_for(first);
-  gepp_node_kernel<<<1, threads_for(first), g.smem_bytes, s>>>(g);
+  launch_node(1, threads_for(first));
   CU_TRY(cudaGetLastError());
   g.order_full = nullptr;
   for (int64_t lo = first; lo < rows; lo += bj) {
@@ -2044,7 +2048,7 @@ int gepp_tournament(const double* panel, int64_t lda, int bj, int64_t rows, int 
     g.cand_in = T.cand[cur]; g.cnt_in = T.cnt[cur];
     g.cand_out = T.cand[cur ^ 1]; g.cnt_out = T.cnt[cur ^ 1];
     g.smem_bytes = smem_for(2 * bj);
-    gepp_node_kernel<<<1, threads_for(2 * bj), g.smem_bytes, s>>>(g);
+    launch_node(1, threads_for(2 * bj));
     CU_TRY(cudaGetLastError());
     cur ^= 1;
   }
