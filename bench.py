@@ -251,7 +251,7 @@ def run_device(args):
     lib.prrp_b200_dmma_peak(1500.0, ctypes.byref(pk), ctypes.byref(err))
     achieved = schur_flops / (schur_ms * 1e-3) / 1e12
     traffic, traffic_note = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_schur_summary.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_schur_r01.json")
     if os.path.exists(prof):
         try:
             ps = json.load(open(prof))

@@ -9,37 +9,43 @@
 
 __global__ void __launch_bounds__(1024) gf_pivot_kernel(double* A, int64_t lda, int64_t m, int64_t n, int64_t k,
                                                         int64_t* perm, DevState* st) {
-  __shared__ double s_best[32];
+  __shared__ unsigned long long s_best[32];
   __shared__ long long s_bi[32];
   if (prrp_failed(st)) return;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  double best = -1.0;
+  // np.argmax order on |column k|: keys are the bit patterns of |x| (monotone
+  // for non-negative doubles) with every NaN mapped above +inf, so the first
+  // NaN wins like numpy's argmax; ties go to the smaller row.
+  unsigned long long best = 0ull;
   long long bi = LLONG_MAX;
   for (int64_t q = k + t; q < m; q += blockDim.x) {
-    const double v = fabs(A[q * lda + k]);
-    if (v > best) { best = v; bi = q; }
+    const double x = fabs(A[q * lda + k]);
+    const unsigned long long v = isnan(x) ? 0x7FF8000000000000ull : (unsigned long long)__double_as_longlong(x);
+    if (v > best || (v == best && q < bi)) { best = v; bi = q; }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
     const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (better(ob, oi, best, bi)) { best = ob; bi = oi; }
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
   }
   if (lane == 0) { s_best[wid] = best; s_bi[wid] = bi; }
   __syncthreads();
   if (wid == 0) {
     const int nw = blockDim.x >> 5;
-    best = lane < nw ? s_best[lane] : -1.0;
+    best = lane < nw ? s_best[lane] : 0ull;
     bi = lane < nw ? s_bi[lane] : LLONG_MAX;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
       const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (better(ob, oi, best, bi)) { best = ob; bi = oi; }
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
     if (lane == 0) {
-      s_bi[0] = best == 0.0 ? -1 : bi;
-      if (best == 0.0) prrp_set_error(st, PRRP_ERR_SINGULAR_MATRIX, -1, -1, (int)k, 0.0);
+      // an exactly zero pivot column (or an empty one) is singular (gepp.py:49-51)
+      const bool sing = best == 0ull || bi < k || bi >= m;
+      s_bi[0] = sing ? -1 : bi;
+      if (sing) prrp_set_error(st, PRRP_ERR_SINGULAR_MATRIX, -1, -1, (int)k, 0.0);
     }
   }
   __syncthreads();

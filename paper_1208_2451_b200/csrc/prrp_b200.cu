@@ -1077,8 +1077,8 @@ struct LuPlan {
     for (void* p : bufs) cudaFree(p);
   }
 };
-std::vector<std::unique_ptr<LuPlan>>& lu_plans() {
-  static std::vector<std::unique_ptr<LuPlan>> v;
+std::vector<std::shared_ptr<LuPlan>>& lu_plans() {
+  static std::vector<std::shared_ptr<LuPlan>> v;
   return v;
 }
 std::mutex g_lu_plans_mu;
@@ -1124,13 +1124,17 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
   if (!pl) {
     if (plans.size() >= kMaxPlans) {
       auto lru = std::min_element(plans.begin(), plans.end(),
-                                  [](const std::unique_ptr<LuPlan>& x, const std::unique_ptr<LuPlan>& y) {
-                                    return x->used < y->used;
+                                  [](const std::shared_ptr<LuPlan>& x, const std::shared_ptr<LuPlan>& y) {
+                                    // plans held by an in-flight call (use_count > 1) are never evicted
+                                    return (x.use_count() > 1 ? UINT64_MAX : x->used) <
+                                           (y.use_count() > 1 ? UINT64_MAX : y->used);
                                   });
-      CU_TRY(cudaDeviceSynchronize());
-      plans.erase(lru);
+      if (lru->use_count() == 1) {
+        CU_TRY(cudaDeviceSynchronize());
+        plans.erase(lru);
+      }
     }
-    std::unique_ptr<LuPlan> np(new LuPlan{A, lda, m, n, b, tau, perm, dev});
+    std::shared_ptr<LuPlan> np(new LuPlan{A, lda, m, n, b, tau, perm, dev});
     static thread_local cudaStream_t cs = nullptr;
     if (!cs) CU_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t g = nullptr;
@@ -1151,10 +1155,18 @@ int luprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau,
     pl = plans.back().get();
   }
   pl->used = ++g_lu_plan_clock;
+  // the read-back below reads the plan's buffers (state, swap counts) outside
+  // the cache lock: keep the plan alive (and unevictable) until it is done
+  std::shared_ptr<LuPlan> hold;
+  for (auto& q : plans)
+    if (q.get() == pl) hold = q;
   CU_TRY(cudaGraphLaunch(pl->exec, s));
   const LuOut out = pl->out;
   plans_lock.unlock();
-  return luprrp_finish(out, s, swap_counts, stats, err, nullptr, nullptr, host_t0);
+  const int rc = luprrp_finish(out, s, swap_counts, stats, err, nullptr, nullptr, host_t0);
+  std::lock_guard<std::mutex> relock(g_lu_plans_mu);
+  hold.reset();
+  return rc;
 }
 
 int luprrp_finish(const LuOut& out, cudaStream_t s, int32_t* swap_counts, prrp_stats* stats, prrp_err* err,
@@ -1809,8 +1821,8 @@ struct CaluPlan {
     for (void* p : bufs) cudaFree(p);
   }
 };
-std::vector<std::unique_ptr<CaluPlan>>& calu_plans() {
-  static std::vector<std::unique_ptr<CaluPlan>> v;
+std::vector<std::shared_ptr<CaluPlan>>& calu_plans() {
+  static std::vector<std::shared_ptr<CaluPlan>> v;
   return v;
 }
 uint64_t g_plan_clock = 0;
@@ -1875,13 +1887,17 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   if (!pl) {
     if (plans.size() >= kMaxPlans) {
       auto lru = std::min_element(plans.begin(), plans.end(),
-                                  [](const std::unique_ptr<CaluPlan>& x, const std::unique_ptr<CaluPlan>& y) {
-                                    return x->used < y->used;
+                                  [](const std::shared_ptr<CaluPlan>& x, const std::shared_ptr<CaluPlan>& y) {
+                                    // plans held by an in-flight call (use_count > 1) are never evicted
+                                    return (x.use_count() > 1 ? UINT64_MAX : x->used) <
+                                           (y.use_count() > 1 ? UINT64_MAX : y->used);
                                   });
-      CU_TRY(cudaDeviceSynchronize());   // its graph may be running on another thread's stream
-      plans.erase(lru);
+      if (lru->use_count() == 1) {          // idle: its last call has read its results back
+        CU_TRY(cudaDeviceSynchronize());
+        plans.erase(lru);
+      }
     }
-    std::unique_ptr<CaluPlan> np(new CaluPlan{A, lda, m, n, b, tau, P, perm, dev});
+    std::shared_ptr<CaluPlan> np(new CaluPlan{A, lda, m, n, b, tau, P, perm, dev});
     // capture on a private stream (the caller's may be the legacy stream)
     static thread_local cudaStream_t cs = nullptr;
     if (!cs) CU_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -1915,10 +1931,18 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     pl = plans.back().get();
   }
   pl->used = ++g_plan_clock;
+  // the read-back runs outside the cache lock and reads the plan's buffers:
+  // hold a reference so the plan cannot be evicted (freed) before it is done
+  std::shared_ptr<CaluPlan> hold;
+  for (auto& q : plans)
+    if (q.get() == pl) hold = q;
   CU_TRY(cudaGraphLaunch(pl->exec, s));
-  const CaluOut out = pl->out;   // a copy: the read-back runs outside the cache lock
+  const CaluOut out = pl->out;
   plans_lock.unlock();
-  return caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, nullptr);
+  const int rc = caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, nullptr);
+  std::lock_guard<std::mutex> relock(g_plans_mu);
+  hold.reset();
+  return rc;
 }
 
 int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats,
@@ -2086,7 +2110,10 @@ int calu_gepp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, int P, i
   const int64_t ldl = ((m + 7) / 8) * 8;
   double* Lcm = ar.get<double>((size_t)b * ldl);
   GeppTourBufs T = alloc_tour(ar, m, b, P);
-  const int64_t cw = std::min<int64_t>(n, 2048);
+  // row-move staging in column chunks: a fixed ~128 MiB budget (most rows of
+  // the trailing region move under the stable [pivots, rest] partition, so
+  // the staging is sized by rows x chunk, not by the moved-row count)
+  const int64_t cw = std::min<int64_t>(n, std::max<int64_t>(256, std::min<int64_t>(2048, (int64_t)(16 << 20) / m)));
   double* rbuf = ar.get<double>((size_t)m * cw);
   int64_t* pbuf = ar.get<int64_t>(m);
   double* D = ar.get<double>((size_t)b * b);

@@ -29,6 +29,9 @@ class GeppFactors:
             raise ZeroDivisionError("growth factor of an all-zero matrix")
         return self.intermediate_max / self.original_max
 
+    def solve(self, rhs):
+        return gepp_solve(self, rhs)
+
 
 def gepp_factor(a):
     """Factor an m x n matrix (any shape) with partial pivoting (gepp.py:39-65)."""
@@ -38,9 +41,12 @@ def gepp_factor(a):
         raise DimensionMismatch(f"expected a 2-D array, got ndim={c.ndim}")
     m, n = c.shape
     lib = _lib.device_lib()
-    if m == 0 or n == 0:
-        raise DimensionMismatch("gepp_factor needs a non-empty matrix")
     s = min(m, n)
+    if s == 0:
+        # nothing to eliminate (gepp.py:43-47 with zero steps): identity order,
+        # empty trapezoids, both maxima 0 (the reference's max norm of an empty matrix)
+        return GeppFactors(perm=np.arange(m, dtype=np.intp), l=np.zeros((m, 0), order="F"),
+                           u=np.zeros((0, n), order="F"), intermediate_max=0.0, original_max=0.0)
     ld = n + (n & 1)
     A = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
     A[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(c)))
@@ -55,6 +61,7 @@ def gepp_factor(a):
     else:
         rc = lib.prrp_gepp(ctypes.c_void_p(A.data_ptr()), ld, m, n, ctypes.c_void_p(P.data_ptr()),
                            ctypes.byref(im), ctypes.byref(om), ctypes.byref(err), _lib.stream_handle())
+    err.panel = -1            # the standalone gepp_factor never tags a panel (gepp.py:49-51)
     _lib.raise_for(rc, err, "gepp_factor")
     packed = A[:, :n].cpu().numpy()
     l = np.tril(packed[:, :s], -1)
@@ -62,3 +69,11 @@ def gepp_factor(a):
     u = np.triu(packed[:s, :])
     return GeppFactors(perm=P.cpu().numpy().astype(np.intp), l=np.asfortranarray(l), u=np.asfortranarray(u),
                        intermediate_max=float(im.value), original_max=float(om.value))
+
+
+def gepp_solve(f, rhs):
+    """Solve A x = rhs from square GEPP factors (gepp.py:68-78) on the device."""
+    from .luprrp import _solve_factors
+    if f.l.shape[0] != f.l.shape[1]:
+        raise DimensionMismatch("gepp_solve needs factors of a square matrix")
+    return _solve_factors(f.perm, f.l, f.u, rhs, "gepp_solve")

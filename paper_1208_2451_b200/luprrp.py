@@ -52,6 +52,9 @@ class BlockLUFactors:
     panel_width: int
     stats: ElimStats
 
+    def solve(self, rhs):
+        return luprrp_solve(self, rhs)
+
 
 @dataclass
 class DeviceLU:
@@ -441,24 +444,32 @@ def luprrp_solve(f, rhs):
     """Solve A x = rhs from square block factors (luprrp.py:204-214): forward
     substitution with the unit lower L on P rhs, back substitution with U, on
     the device (prrp_lu_solve)."""
-    import torch
     if f.l.shape[0] != f.l.shape[1]:
         raise DimensionMismatch("solve needs factors of a square matrix")
+    return _solve_factors(f.perm, f.l, f.u, rhs, "luprrp_solve")
+
+
+def _solve_factors(perm, l, u, rhs, what):
+    """x = U^-1 L^-1 (P rhs) on the device for square factors; a zero diagonal
+    of U raises SingularFactor(index) like matcore.trsm_upper (matcore.py:88-90)."""
+    import torch
     vec = np.asarray(rhs, dtype=np.float64)
     b2 = vec.reshape(-1, 1) if vec.ndim == 1 else vec
-    if b2.shape[0] != f.l.shape[0]:
+    if b2.shape[0] != l.shape[0]:
         raise DimensionMismatch("right-hand side row count mismatch")
     n, nrhs = b2.shape
+    if nrhs == 0:
+        return np.zeros((n, 0), order="F") if vec.ndim != 1 else np.zeros(n)
     lib = _lib.device_lib()
-    lu = _pack_lu_device(f.l, f.u)
-    perm = torch.from_numpy(np.asarray(f.perm, dtype=np.int64)).cuda()
+    lu = _pack_lu_device(l, u)
+    p = torch.from_numpy(np.asarray(perm, dtype=np.int64)).cuda()
     B = torch.from_numpy(np.ascontiguousarray(b2.T)).cuda()          # column-major n x nrhs
     X = torch.empty_like(B)
     err = _lib.PrrpErr()
-    rc = lib.prrp_lu_solve(ctypes.c_void_p(lu.data_ptr()), lu.shape[1], n, ctypes.c_void_p(perm.data_ptr()),
+    rc = lib.prrp_lu_solve(ctypes.c_void_p(lu.data_ptr()), lu.shape[1], n, ctypes.c_void_p(p.data_ptr()),
                            ctypes.c_void_p(B.data_ptr()), n, ctypes.c_void_p(X.data_ptr()), n, nrhs,
                            ctypes.byref(err), _lib.stream_handle())
-    _lib.raise_for(rc, err, "luprrp_solve")
+    _lib.raise_for(rc, err, what)
     x = np.asfortranarray(X.cpu().numpy().T)
     return x[:, 0] if vec.ndim == 1 else x
 

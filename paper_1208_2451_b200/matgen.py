@@ -62,3 +62,40 @@ def gen_foster(n, c=1.0, h=1.0, k=2.0 / 3.0):
     a[:n - 1, n - 1] = -1.0 / c
     a[n - 1, n - 1] = 1.0 - 1.0 / c - kh / 2.0
     return a
+
+
+def gen_randn_rect(m, n, seed):
+    """m x n normals: the first m*n draws of matgen._normals in row-major
+    order (the reference's conventions, rectangular; used for the panel
+    strong-RRQR parity cases)."""
+    return _normals(_rng(seed), m * n).reshape(m, n)
+
+
+def gen_urand_cols(n, seed, ncols, chunk_rows=1024):
+    """Columns [0, ncols) of gen_urand(n, seed), F-ordered, generated in
+    row chunks so the n x n matrix is never formed (PCG64 doubles are drawn
+    one per value, so chunked draws continue the same stream)."""
+    rng = _rng(seed)
+    out = np.empty((n, ncols), order="F")
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        blk = rng.random((r1 - r0) * n).reshape(r1 - r0, n)
+        out[r0:r1, :] = 2.0 * blk[:, :ncols] - 1.0
+    return out
+
+
+def gen_kahan_panel(p, b, theta, scale, seed):
+    """A b x p panel transpose on which column-pivoted QR is not rank
+    revealing: a Kahan block K (s^i on the diagonal, -c s^i above, columns
+    damped by (1 - 1e-10)^j so the pivots come in order) followed by p - b
+    small random columns scaled like K's rows.  K^-1 grows like (1 + c)^b,
+    so |R11^-1 R12| exceeds tau and the strong-RRQR swap loop runs
+    (pivoted_qr.py:129-144).  Elementwise construction only (no BLAS), so
+    the bits do not depend on the host's BLAS kernels."""
+    c, s = np.cos(theta), np.sin(theta)
+    rs = s ** np.arange(b, dtype=np.float64)
+    cd = (1.0 - 1e-10) ** np.arange(b, dtype=np.float64)
+    k = np.triu(np.full((b, b), -c), 1) + np.eye(b)
+    k = (k * rs[:, None]) * cd[None, :]
+    r = (gen_randn_rect(b, p - b, seed) * scale) * rs[:, None]
+    return np.hstack([k, r])

@@ -1,0 +1,226 @@
+"""Full-size parity goldens (BASELINE configs 2-5) from the REAL reference
+package (``prrp`` at /root/reference/pkg/src; build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden_full.py [case ...]
+
+Writes tests/golden/full/<case>.npz + <case>.json.  Cases:
+
+* ``c2_b64``, ``c2_b128``: ``luprrp_factor(gen_randn(8192, 42), b, 2.0)``
+  in full (about 200 s each): permutation, swap counts, ElimStats, growth,
+  row / column sums of L and U, sample rows, backward error.
+* ``c3_wilkinson``, ``c3_foster``: config 3 at n = 4096, b = 64.
+* ``c4_prefix``, ``c5_prefix``: CALU_PRRP (``binary_tree(8)``) of the first
+  K panels of configs 4 / 5.  Right-looking LU of columns [0, K b) depends on
+  those columns only (each panel reads the panel columns after the previous
+  updates, ``rank_update`` is elementwise in the columns it touches, and the
+  GEPP finish of a panel pivots on its own b x b block), so the reference
+  run on the tall m x K b matrix A[:, :K b] fixes perm[:K b], the first K
+  swap counts, L[:, :K b] (row by row, by original row id) and U[:K b, :K b]
+  of the full factorization.  The full 16384^2 / 32768^2 reference runs are
+  hours and ~51 GB of RAM; the prefix runs are minutes.
+* ``srrqr_*``: ``strong_rrqr`` of b x p panel transposes at p in {4097,
+  6000, 8192, 12288, 16384}, b in {64, 128} (the device engines' multi-CTA
+  column paths above 4096 rows), plus Kahan-type panels
+  (``matgen.gen_kahan_panel``) on which the swap loop runs at large p.
+
+Inputs are regenerated from (generator, n, seed) by the repo's own
+generators (``paper_1208_2451_b200.matgen``); the input checksums stored here
+pin those against the reference's ``matgen``.
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+from fractions import Fraction
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import prrp  # noqa: E402  (the reference)
+from prrp import matgen  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+OUT = os.path.join(HERE, "full")
+sys.path.insert(0, ROOT)
+from paper_1208_2451_b200 import matgen as pmg  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def stats_dict(st, full=True):
+    d = {
+        "original_max": st.original_max,
+        "intermediate_max": st.intermediate_max,
+        "finish_max": st.finish_max,
+        "panel_multiplier_max": st.panel_multiplier_max,
+        "swap_counts": list(map(int, st.swap_counts)),
+        "flops_charged": str(Fraction(st.flops_charged)),
+        "flops_executed": str(Fraction(st.flops_executed)),
+    }
+    if full:
+        d["growth_factor"] = st.growth_factor
+        d["full_growth_factor"] = st.full_growth_factor
+    return d
+
+
+def rel_residual(a, perm, l, u):
+    """||A[perm] - L U||_F / ||A||_F in float64 (numpy BLAS)."""
+    r = a[perm, :] - l @ u
+    return float(np.linalg.norm(r) / np.linalg.norm(a))
+
+
+def factor_summary(a, f, arrays, meta, sample_rows):
+    n = a.shape[1]
+    arrays["perm"] = np.asarray(f.perm, dtype=np.int64)
+    arrays["l_colsum"] = f.l.sum(axis=0)
+    arrays["l_rowsum"] = f.l.sum(axis=1)
+    arrays["l_colabs"] = np.abs(f.l).sum(axis=0)
+    arrays["u_colsum"] = f.u.sum(axis=0)
+    arrays["u_rowsum"] = f.u.sum(axis=1)
+    arrays["u_rowabs"] = np.abs(f.u).sum(axis=1)
+    arrays["u_diag"] = np.diag(f.u).copy()
+    arrays["l_rows"] = f.l[sample_rows, :]
+    arrays["u_rows"] = f.u[sample_rows, :]
+    meta["sample_rows"] = sample_rows
+    meta["stats"] = stats_dict(f.stats)
+    meta["l_max"] = float(np.abs(f.l).max())
+    meta["u_max"] = float(np.abs(f.u).max())
+    t = time.time()
+    meta["rel_residual"] = rel_residual(a, f.perm, f.l, f.u)
+    print("  residual", meta["rel_residual"], "%.1f s" % (time.time() - t), flush=True)
+    meta["n"] = n
+
+
+def case_lu(name, gen, n, b, **kw):
+    if gen == "randn":
+        a = matgen.gen_randn(n, 42)
+        assert np.array_equal(a, pmg.gen_randn(n, 42))
+    elif gen == "wilkinson":
+        a = matgen.gen_wilkinson(n)
+        assert np.array_equal(a, pmg.gen_wilkinson(n))
+    elif gen == "foster":
+        a = matgen.gen_foster(n, c=1.0, h=1.0, k=1.0)
+        assert np.array_equal(a, pmg.gen_foster(n, 1.0, 1.0, 1.0))
+    t = time.time()
+    f = prrp.luprrp_factor(a, b, 2.0)
+    dt = time.time() - t
+    print(name, "luprrp_factor %.1f s" % dt, flush=True)
+    meta = {"kind": "luprrp", "gen": gen, "n": n, "b": b, "tau": 2.0, "seed": 42,
+            "input_sha": sha(a), "ref_seconds": dt}
+    arrays = {}
+    factor_summary(a, f, arrays, meta, [0, 1, b - 1, b, n // 2, n - 1])
+    return meta, arrays
+
+
+def case_calu_prefix(name, gen, n, b, K):
+    kb = K * b
+    if gen == "randn":
+        a = matgen.gen_randn(n, 42)
+        assert np.array_equal(a, pmg.gen_randn(n, 42))
+        s = sha(a)
+        a = np.asfortranarray(a[:, :kb])
+    else:
+        a = pmg.gen_urand_cols(n, 42, kb)         # chunked: the 8 GiB matrix is never formed
+        s = None
+    t = time.time()
+    f = prrp.caluprrp_factor(a, b, 2.0, prrp.binary_tree(8))
+    dt = time.time() - t
+    print(name, "caluprrp_factor(prefix %d x %d) %.1f s" % (n, kb, dt), flush=True)
+    # the first tournament with its trace (node for node)
+    perm0, trace = prrp.tournament_select(np.asfortranarray(a[:, :b]), b, 2.0, prrp.binary_tree(8), "srrqr")
+    pos = np.empty(n, dtype=np.int64)
+    pos[f.perm] = np.arange(n)
+    arrays = {
+        "perm_prefix": np.asarray(f.perm[:kb], dtype=np.int64),
+        "prefix_sha_cols": np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8),
+        # L[:, :kb] by ORIGINAL row id (rows at positions >= kb move later)
+        "l_rowsum_by_row": f.l[pos, :].sum(axis=1),
+        "l_rowabs_by_row": np.abs(f.l[pos, :]).sum(axis=1),
+        "l_colsum": f.l.sum(axis=0),
+        "u_rowsum": f.u[:kb, :kb].sum(axis=1),
+        "u_rowabs": np.abs(f.u[:kb, :kb]).sum(axis=1),
+        "u_diag": np.diag(f.u[:kb, :kb]).copy(),
+        "u_rows": np.ascontiguousarray(f.u[[0, 1, b, kb - 1], :kb]),
+        "t0_perm": np.asarray(perm0, dtype=np.int64),
+    }
+    meta = {"kind": "calu_prefix", "gen": gen, "n": n, "b": b, "tau": 2.0, "seed": 42, "P": 8,
+            "K": K, "input_sha_full": s, "input_sha_prefix": sha(a), "ref_seconds": dt,
+            "swap_counts": list(map(int, f.stats.swap_counts)),
+            "panel_multiplier_max": f.stats.panel_multiplier_max,
+            "l_max": float(np.abs(f.l).max()), "u_max": float(np.abs(f.u[:kb, :kb]).max()),
+            "t0_trace": [{"level": nd.level, "index": nd.index, "n_members": int(nd.members.shape[0]),
+                          "selected": nd.selected.tolist(), "swap_count": int(nd.swap_count)}
+                         for nd in trace.nodes]}
+    return meta, arrays
+
+
+def case_srrqr(name, p, b, tau, kahan=None):
+    if kahan:                                          # (theta, scale): the swap loop runs
+        at = pmg.gen_kahan_panel(p, b, kahan[0], kahan[1], 7 + p + b)
+        a = at.T
+    else:
+        a = pmg.gen_randn_rect(p, b, 7 + p + b)        # p x b panel, row-major draws
+        ref_a = matgen._normals(matgen._rng(7 + p + b), p * b).reshape(p, b)
+        assert np.array_equal(a, ref_a)
+    t = time.time()
+    res = prrp.strong_rrqr(np.asfortranarray(a.T), b, tau)
+    dt = time.time() - t
+    print(name, "strong_rrqr %.1f s swaps %d" % (dt, res.swap_count), flush=True)
+    arrays = {
+        "perm": np.asarray(res.qr.perm, dtype=np.int64),
+        "r_diag": np.diag(res.qr.r[:, :b]).copy(),
+        "r11": np.ascontiguousarray(res.qr.r[:, :b]),
+        "r_colsum": res.qr.r.sum(axis=0),
+        "l_colsum": res.l_block.sum(axis=0),
+        "l_rows": np.ascontiguousarray(res.l_block[[0, 1, (p - b) // 2, p - b - 1], :]),
+    }
+    meta = {"kind": "srrqr", "p": p, "b": b, "h": b, "tau": tau, "seed": 7 + p + b, "input_sha": sha(a),
+            "kahan": list(kahan) if kahan else None,
+            "swap_count": int(res.swap_count), "ref_seconds": dt,
+            "l_max": float(np.abs(res.l_block).max()), "r_max": float(np.abs(res.qr.r).max())}
+    return meta, arrays
+
+
+CASES = {
+    "c2_b64": lambda: case_lu("c2_b64", "randn", 8192, 64),
+    "c2_b128": lambda: case_lu("c2_b128", "randn", 8192, 128),
+    "c3_wilkinson": lambda: case_lu("c3_wilkinson", "wilkinson", 4096, 64),
+    "c3_foster": lambda: case_lu("c3_foster", "foster", 4096, 64),
+    "c4_prefix": lambda: case_calu_prefix("c4_prefix", "randn", 16384, 64, 8),
+    "c5_prefix": lambda: case_calu_prefix("c5_prefix", "urand", 32768, 128, 4),
+}
+for _p in (4097, 6000, 8192, 12288, 16384):
+    for _b in (64, 128):
+        CASES["srrqr_p%d_b%d" % (_p, _b)] = (lambda p=_p, b=_b: case_srrqr("srrqr_p%d_b%d" % (p, b), p, b, 2.0))
+CASES["srrqr_kahan_p6000_b64"] = lambda: case_srrqr("srrqr_kahan_p6000_b64", 6000, 64, 2.0, (1.3, 1e-2))
+CASES["srrqr_kahan_p8192_b128"] = lambda: case_srrqr("srrqr_kahan_p8192_b128", 8192, 128, 2.0, (1.45, 1e-2))
+CASES["srrqr_kahan_p12288_b64"] = lambda: case_srrqr("srrqr_kahan_p12288_b64", 12288, 64, 2.0, (1.3, 1e-2))
+
+
+def main(names):
+    os.makedirs(OUT, exist_ok=True)
+    for name in names or list(CASES):
+        path = os.path.join(OUT, name)
+        if os.path.exists(path + ".json") and not os.environ.get("REGEN"):
+            print("exists", name)
+            continue
+        meta, arrays = CASES[name]()
+        meta["name"] = name
+        meta["numpy"] = np.__version__
+        meta["openblas_coretype"] = os.environ.get("OPENBLAS_CORETYPE", "(auto: Haswell kernels here)")
+        np.savez_compressed(path + ".npz", **arrays)
+        with open(path + ".json", "w") as fh:
+            json.dump(meta, fh, indent=1, default=float)
+        print("wrote", name, flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -1,0 +1,211 @@
+"""Pivot parity at the BASELINE sizes (configs 2-5) against goldens produced
+by the REAL reference package (tests/golden/make_golden_full.py).
+
+* configs 2 and 3 (LU_PRRP n = 8192, b = 64 and 128; Wilkinson / Foster
+  n = 4096): the full factorization on the device; identical row
+  permutation and swap counts (generic inputs), growth factors within 1e-10,
+  per-row / per-column sums and sample rows of L and U within the 1e-11
+  element bar, backward error <= 4x the reference's.
+* configs 4 and 5 (CALU_PRRP n = 16384 / 32768, P = 8): the full device
+  factorization, compared on its first K panels (the reference's run on the
+  m x K b column prefix fixes them exactly, see make_golden_full.py):
+  perm[:K b], swap counts, L[:, :K b] row by row by original row id,
+  U[:K b, :K b]; plus the first panel's tournament node for node.
+* strong_rrqr at p in {4097 .. 16384}, b in {64, 128}: the multi-CTA column
+  paths of the panel engines (panel1's shared-memory column, panel2's
+  multi-cluster exchange, the generic engine above them) and, on
+  Kahan-type panels, the swap loop at large p.
+
+The bars are the ones of tests/test_gpu_parity.py.
+"""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FULL = os.path.join(HERE, "golden", "full")
+TOL_F = 1e-11
+TOL_G = 1e-10
+
+
+def _load(name):
+    path = os.path.join(FULL, name)
+    if not os.path.exists(path + ".json"):
+        pytest.skip(f"golden {name} not generated")
+    meta = json.load(open(path + ".json"))
+    arrays = dict(np.load(path + ".npz"))
+    return meta, arrays
+
+
+def _names(prefix):
+    return sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(FULL, prefix + "*.json")))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1208_2451_b200 as d
+    return d
+
+
+def _close_rows(got, ref, scale, what):
+    err = float(np.abs(np.asarray(got) - np.asarray(ref)).max()) if np.size(ref) else 0.0
+    assert err <= TOL_F * scale, (what, err, scale)
+
+
+def _close_sums(got, ref, scale, terms, what):
+    """Sums of `terms` entries, each within the element bar TOL_F * scale."""
+    err = float(np.abs(np.asarray(got) - np.asarray(ref)).max())
+    assert err <= TOL_F * scale * terms, (what, err, TOL_F * scale * terms)
+
+
+# ------------------------------------------------------------ strong RRQR, large p
+@pytest.mark.parametrize("name", _names("srrqr_"))
+def test_strong_rrqr_large_p(dev, name):
+    from paper_1208_2451_b200 import matgen
+    meta, arr = _load(name)
+    p, b, tau = meta["p"], meta["b"], meta["tau"]
+    if meta.get("kahan"):
+        at = matgen.gen_kahan_panel(p, b, meta["kahan"][0], meta["kahan"][1], meta["seed"])
+    else:
+        at = matgen.gen_randn_rect(p, b, meta["seed"]).T
+    res = dev.strong_rrqr(np.asfortranarray(at), b, tau)
+    assert np.array_equal(res.qr.perm, arr["perm"]), name
+    assert res.swap_count == meta["swap_count"], name
+    r_max = meta["r_max"]
+    _close_rows(res.qr.r[:, :b], arr["r11"], r_max, name + " R11")
+    _close_sums(res.qr.r.sum(axis=0), arr["r_colsum"], r_max, b, name + " R colsum")
+    _close_rows(res.l_block[[0, 1, (p - b) // 2, p - b - 1], :], arr["l_rows"], meta["l_max"], name + " L rows")
+    _close_sums(res.l_block.sum(axis=0), arr["l_colsum"], meta["l_max"], p - b, name + " L colsum")
+    assert np.abs(res.l_block).max() == pytest.approx(meta["l_max"], rel=TOL_G)
+
+
+# ------------------------------------------------------------ LU_PRRP, configs 2 and 3
+def _lu_parts(lu, n):
+    """Row/column sums of L (unit lower) and U from the packed device factors."""
+    import torch
+    low = torch.tril(lu, -1)
+    low.diagonal().fill_(1.0)
+    up = torch.triu(lu)
+    out = {"l_rowsum": low.sum(dim=1), "l_colsum": low.sum(dim=0), "l_colabs": low.abs().sum(dim=0),
+           "u_rowsum": up.sum(dim=1), "u_colsum": up.sum(dim=0), "u_rowabs": up.abs().sum(dim=1),
+           "u_diag": torch.diagonal(up).clone()}
+    lmax, umax = float(low.abs().max()), float(up.abs().max())
+    del low, up
+    return {k: v.cpu().numpy() for k, v in out.items()}, lmax, umax
+
+
+@pytest.mark.parametrize("name", ["c2_b64", "c2_b128", "c3_wilkinson", "c3_foster"])
+def test_luprrp_baseline_config(dev, name):
+    import torch
+    from paper_1208_2451_b200 import matgen
+    from paper_1208_2451_b200.metrics import rel_factorization_error_device
+    meta, arr = _load(name)
+    n, b = meta["n"], meta["b"]
+    if meta["gen"] == "randn":
+        a = matgen.gen_randn(n, meta["seed"], order="C")
+    elif meta["gen"] == "wilkinson":
+        a = np.ascontiguousarray(matgen.gen_wilkinson(n))
+    else:
+        a = np.ascontiguousarray(matgen.gen_foster(n, 1.0, 1.0, 1.0))
+    A = torch.from_numpy(a).cuda()
+    buf = A.clone()
+    res = dev.luprrp_factor_device(buf, b, meta["tau"])
+    st, ref = res.stats, meta["stats"]
+    perm = res.perm.cpu().numpy()
+    generic = meta["gen"] != "wilkinson"    # Wilkinson: 961 rounding-decided ties in panel 0
+    if generic:
+        assert np.array_equal(perm, arr["perm"]), name
+        assert list(st.swap_counts) == ref["swap_counts"], name
+        assert str(st.flops_charged) == ref["flops_charged"] and str(st.flops_executed) == ref["flops_executed"]
+    assert st.original_max == ref["original_max"]
+    assert st.growth_factor == pytest.approx(ref["growth_factor"], rel=TOL_G), name
+    assert st.full_growth_factor == pytest.approx(ref["full_growth_factor"], rel=TOL_G), name
+    assert st.panel_multiplier_max == pytest.approx(ref["panel_multiplier_max"], rel=TOL_G), name
+    resid = rel_factorization_error_device(A, res.lu, res.perm)
+    assert resid <= 4 * meta["rel_residual"], (name, resid, meta["rel_residual"])
+    if generic:
+        parts, lmax, umax = _lu_parts(res.lu, n)
+        assert lmax == pytest.approx(meta["l_max"], rel=TOL_G) and umax == pytest.approx(meta["u_max"], rel=TOL_G)
+        lm, um = meta["l_max"], meta["u_max"]
+        for k in ("l_rowsum", "l_colsum", "l_colabs"):
+            _close_sums(parts[k], arr[k], lm, n, name + " " + k)
+        for k in ("u_rowsum", "u_colsum", "u_rowabs"):
+            _close_sums(parts[k], arr[k], um, n, name + " " + k)
+        _close_rows(parts["u_diag"], arr["u_diag"], um, name + " diag U")
+        rows = meta["sample_rows"]
+        lu_rows = res.lu[rows, :].cpu().numpy()
+        l_rows = np.tril(lu_rows, -1)
+        u_rows = np.triu(lu_rows)
+        for i, r in enumerate(rows):
+            if r < n:
+                l_rows[i, r] = 1.0
+        _close_rows(l_rows, arr["l_rows"], lm, name + " L sample rows")
+        _close_rows(u_rows, arr["u_rows"], um, name + " U sample rows")
+
+
+# ------------------------------------------------------------ CALU_PRRP, configs 4 and 5 (first K panels)
+@pytest.mark.parametrize("name", ["c4_prefix", "c5_prefix"])
+def test_caluprrp_baseline_prefix(dev, name):
+    import ctypes
+    import torch
+    from paper_1208_2451_b200 import _lib, matgen
+    meta, arr = _load(name)
+    n, b, K = meta["n"], meta["b"], meta["K"]
+    kb = K * b
+    a = (matgen.gen_randn if meta["gen"] == "randn" else matgen.gen_urand)(n, meta["seed"], order="C")
+    panel0 = np.asfortranarray(a[:, :b])
+    lda = n + (n & 1)
+    buf = torch.empty((n, lda), dtype=torch.float64, device="cuda")
+    buf[:, :n].copy_(torch.from_numpy(a))
+    del a
+    lib = _lib.device_lib()
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    npan = (n + b - 1) // b
+    sw = (ctypes.c_int32 * npan)()
+    chg = (ctypes.c_int64 * npan)()
+    st, err = _lib.PrrpStats(), _lib.PrrpErr()
+    rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), lda, n, n, b, meta["tau"], meta["P"],
+                           ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                           _lib.stream_handle())
+    _lib.raise_for(rc, err, "prrp_caluprrp")
+    p = perm.cpu().numpy()
+    assert np.array_equal(p[:kb], arr["perm_prefix"]), name
+    assert list(sw)[:K] == meta["swap_counts"][:K], name
+    lu = buf[:, :n]
+    # L[:, :kb] by original row id
+    lp = torch.tril(lu[:, :kb], -1)
+    idx = torch.arange(kb, device="cuda")
+    lp[idx, idx] = 1.0
+    rowsum = torch.empty(n, dtype=torch.float64, device="cuda")
+    rowabs = torch.empty_like(rowsum)
+    rowsum[perm] = lp.sum(dim=1)
+    rowabs[perm] = lp.abs().sum(dim=1)
+    lm, um = meta["l_max"], meta["u_max"]
+    assert float(lp.abs().max()) == pytest.approx(lm, rel=TOL_G)
+    _close_sums(rowsum.cpu().numpy(), arr["l_rowsum_by_row"], lm, kb, name + " L rows by id")
+    _close_sums(rowabs.cpu().numpy(), arr["l_rowabs_by_row"], lm, kb, name + " |L| rows by id")
+    _close_sums(lp.sum(dim=0).cpu().numpy(), arr["l_colsum"], lm, n, name + " L colsum")
+    del lp
+    ub = torch.triu(lu[:kb, :kb])
+    assert float(ub.abs().max()) == pytest.approx(um, rel=TOL_G)
+    _close_rows(torch.diagonal(ub).cpu().numpy(), arr["u_diag"], um, name + " diag U")
+    _close_sums(ub.sum(dim=1).cpu().numpy(), arr["u_rowsum"], um, kb, name + " U rowsum")
+    _close_sums(ub.abs().sum(dim=1).cpu().numpy(), arr["u_rowabs"], um, kb, name + " |U| rowsum")
+    _close_rows(ub[[0, 1, b, kb - 1], :].cpu().numpy(), arr["u_rows"], um, name + " U rows")
+    del ub, buf
+    torch.cuda.empty_cache()
+    # the first panel's tournament, node for node (tournament.py:155-217)
+    tp, trace = dev.tournament_select(panel0, b, meta["tau"], dev.binary_tree(meta["P"]), "srrqr")
+    assert np.array_equal(tp, arr["t0_perm"]), name
+    got = [(nd.level, nd.index, int(nd.members.shape[0]), nd.selected.tolist(), int(nd.swap_count))
+           for nd in trace.nodes]
+    want = [(d["level"], d["index"], d["n_members"], d["selected"], d["swap_count"]) for d in meta["t0_trace"]]
+    assert got == want, name

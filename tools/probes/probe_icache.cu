@@ -1,264 +1,35 @@
 // Instruction-cache probe: a loop whose body is N independent integer adds
 // (4 chains); cycles per instruction vs N shows the i-cache capacities.
 #include <cstdio>
+// Repeated asm bodies are spelled with doubling macros (NAME_X<count>).
+#define ASMU0_X1 "xor.b32 %1, %1, %0;\n" "mad.lo.u32 %2, %2, %4, %3;\n" "xor.b32 %3, %3, %2;\n" "mad.lo.u32 %0, %0, %4, %1;\n"
+#define ASMU0_X2 ASMU0_X1 ASMU0_X1
+#define ASMU0_X4 ASMU0_X2 ASMU0_X2
+#define ASMU0_X8 ASMU0_X4 ASMU0_X4
+#define ASMU0_X16 ASMU0_X8 ASMU0_X8
+#define ASMU0_X32 ASMU0_X16 ASMU0_X16
+#define ASMU0_X64 ASMU0_X32 ASMU0_X32
+#define ASMU0_X128 ASMU0_X64 ASMU0_X64
+#define ASMU0_X256 ASMU0_X128 ASMU0_X128
+#define ASMU0_X512 ASMU0_X256 ASMU0_X256
+#define ASMU0_X1024 ASMU0_X512 ASMU0_X512
+#define ASMU0_X2048 ASMU0_X1024 ASMU0_X1024
+#define ASMU0_X4096 ASMU0_X2048 ASMU0_X2048
+#define ASMU0_X8192 ASMU0_X4096 ASMU0_X4096
+#define ASMU0_X16384 ASMU0_X8192 ASMU0_X8192
+#define ASMU0_X32768 ASMU0_X16384 ASMU0_X16384
+#define ASMU0_X65536 ASMU0_X32768 ASMU0_X32768
+#define ASMU0_X131072 ASMU0_X65536 ASMU0_X65536
+#define ASMU0_X262144 ASMU0_X131072 ASMU0_X131072
+#define ASMU0_X524288 ASMU0_X262144 ASMU0_X262144
+#define ASMU0_X1048576 ASMU0_X524288 ASMU0_X524288
 __global__ void icache_256(unsigned* out, long long* cyc, int iters, unsigned d) {
   unsigned a = threadIdx.x, b = a + 1, c = a + 2, e = a + 3;
   long long t0 = 0;
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -273,514 +44,7 @@ __global__ void icache_512(unsigned* out, long long* cyc, int iters, unsigned d)
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -795,1026 +59,7 @@ __global__ void icache_1024(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -1829,1538 +74,7 @@ __global__ void icache_1536(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X256 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -3375,2050 +89,7 @@ __global__ void icache_2048(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X256 ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -5433,3074 +104,7 @@ __global__ void icache_3072(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X512 ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -8515,4098 +119,7 @@ __global__ void icache_4096(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X512 ASMU0_X256 ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));
@@ -12621,8194 +134,7 @@ __global__ void icache_8192(unsigned* out, long long* cyc, int iters, unsigned d
   for (int it = 0; it < iters; ++it) {
     if (it == 1) t0 = clock64();
     asm volatile("mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %2, %2, %4, %3;\n"
-"xor.b32 %3, %3, %2;\n"
-"mad.lo.u32 %0, %0, %4, %1;\n"
+ASMU0_X1024 ASMU0_X512 ASMU0_X256 ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %2, %2, %4, %3;\n"
 "xor.b32 %3, %3, %2;\n" : "+r"(a), "+r"(b), "+r"(c), "+r"(e) : "r"(d));

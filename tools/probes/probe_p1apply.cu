@@ -1,5 +1,27 @@
 // Apply+next-key step of panel1 (register column), warm vs after 4K instructions of other code.
 #include <cstdio>
+// Repeated asm bodies are spelled with doubling macros (NAME_X<count>).
+#define ASMU0_X1 "xor.b32 %1, %1, %0;\n" "mad.lo.u32 %0, %0, %2, %1;\n" "xor.b32 %1, %1, %0;\n" "mad.lo.u32 %0, %0, %2, %1;\n"
+#define ASMU0_X2 ASMU0_X1 ASMU0_X1
+#define ASMU0_X4 ASMU0_X2 ASMU0_X2
+#define ASMU0_X8 ASMU0_X4 ASMU0_X4
+#define ASMU0_X16 ASMU0_X8 ASMU0_X8
+#define ASMU0_X32 ASMU0_X16 ASMU0_X16
+#define ASMU0_X64 ASMU0_X32 ASMU0_X32
+#define ASMU0_X128 ASMU0_X64 ASMU0_X64
+#define ASMU0_X256 ASMU0_X128 ASMU0_X128
+#define ASMU0_X512 ASMU0_X256 ASMU0_X256
+#define ASMU0_X1024 ASMU0_X512 ASMU0_X512
+#define ASMU0_X2048 ASMU0_X1024 ASMU0_X1024
+#define ASMU0_X4096 ASMU0_X2048 ASMU0_X2048
+#define ASMU0_X8192 ASMU0_X4096 ASMU0_X4096
+#define ASMU0_X16384 ASMU0_X8192 ASMU0_X8192
+#define ASMU0_X32768 ASMU0_X16384 ASMU0_X16384
+#define ASMU0_X65536 ASMU0_X32768 ASMU0_X32768
+#define ASMU0_X131072 ASMU0_X65536 ASMU0_X65536
+#define ASMU0_X262144 ASMU0_X131072 ASMU0_X131072
+#define ASMU0_X524288 ASMU0_X262144 ASMU0_X262144
+#define ASMU0_X1048576 ASMU0_X524288 ASMU0_X524288
 #define STR2(x) #x
 #define STR(x) STR2(x)
 #include "../../paper_1208_2451_b200/csrc/panel1.cuh"
@@ -103,4098 +125,7 @@ __global__ void __launch_bounds__(256, 1) k_apply(double* out, long long* cyc, i
       ++KB;
     }
     if (cold & 1) asm volatile("mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
-"xor.b32 %1, %1, %0;\n"
-"mad.lo.u32 %0, %0, %2, %1;\n"
+ASMU0_X512 ASMU0_X256 ASMU0_X128 ASMU0_X64 ASMU0_X32 ASMU0_X16 ASMU0_X8 ASMU0_X4 ASMU0_X2 ASMU0_X1
 "xor.b32 %1, %1, %0;\n"
 "mad.lo.u32 %0, %0, %2, %1;\n"
 "xor.b32 %1, %1, %0;\n" : "+r"(ja), "+r"(jb) : "r"(3u));
