@@ -14,30 +14,44 @@
 #pragma once
 #include "lsolve.cuh"
 
-// node input rows for a merge level: lpos_in[node][0..2b) = children's
-// candidates (panel-relative logical positions); rowidx = physical rows
-__global__ void calu_merge_inputs_kernel(const int32_t* cands, int b, int nchild, int32_t* lpos_in,
-                                         int64_t* rowidx, const int64_t* pos2row, int64_t col0, int stride) {
+// node input rows for a merge level: lpos_in[node][0..2b) = [left child's
+// candidates, right child's candidates] (panel-relative logical positions),
+// rowidx = physical rows.  A child that was rank deficient passes fewer than
+// b candidates (tournament.py:131-137): the members then close up and the
+// unused tail is dead (-1: a zero row, never selected); live_out = members.
+__global__ void calu_merge_inputs_kernel(const int32_t* cands, const int32_t* ccnt, int b, int nchild,
+                                         int32_t* lpos_in, int64_t* rowidx, int32_t* live_out,
+                                         const int64_t* pos2row, int64_t col0, int stride) {
   const int node = blockIdx.x;
+  const int cl = ccnt[2 * node];
+  const int cr = 2 * node + 1 < nchild ? ccnt[2 * node + 1] : 0;
   for (int t = threadIdx.x; t < 2 * b; t += blockDim.x) {
-    const int child = 2 * node + t / b;
-    if (child >= nchild) continue;
-    const int32_t lp = cands[child * b + (t % b)];
+    int32_t lp = -1;
+    if (t < cl) lp = cands[(2 * node) * b + t];
+    else if (t < cl + cr) lp = cands[(2 * node + 1) * b + (t - cl)];
     lpos_in[node * stride + t] = lp;
-    rowidx[node * stride + t] = pos2row[col0 + lp];
+    rowidx[node * stride + t] = lp >= 0 ? pos2row[col0 + lp] : -1;
   }
+  if (threadIdx.x == 0) live_out[node] = cl + cr;
 }
 
-// selected candidates of each node: cands_out[node][q] = lpos(node, perm[q]), q < b.
+// selected candidates of each node: cands_out[node][q] = lpos(node, perm[q]),
+// q < cnt_out[node] = wants[node] (b, fewer after a rank-deficient retry, or
+// the members of a merge node that passed them through).
 // Leaves (lpos_in == nullptr): lpos(node, j) = leaf_lo[node] + j.
 __global__ void calu_select_kernel(const int32_t* const* perms, const int32_t* lpos_in, const int64_t* leaf_lo,
-                                   int b, int32_t* cands_out, int stride) {
+                                   int b, const int32_t* wants, const int32_t* lives, int merge, int32_t* cands_out,
+                                   int32_t* cnt_out, int stride) {
   const int node = blockIdx.x;
   const int32_t* perm = perms[node];
-  for (int q = threadIdx.x; q < b; q += blockDim.x) {
+  const int cnt = min(wants[node], b);
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
     const int32_t j = perm[q];
     cands_out[node * b + q] = lpos_in ? lpos_in[node * stride + j] : (int32_t)(leaf_lo[node] + j);
   }
+  if (threadIdx.x == 0) cnt_out[node] = cnt;
+  (void)lives;
+  (void)merge;
 }
 
 // Reorder the trailing region [col0, col0+rows) after the tournament.
@@ -49,15 +63,21 @@ __global__ void calu_select_kernel(const int32_t* const* perms, const int32_t* l
 // the vacated slots.  Outputs: new pos2row, moved list (dst slot, src slot
 // relative to col0) for permute_kernel, log2phys[t] = physical slot of
 // logical position b+t (for scattering L21).  One block.
-__global__ void __launch_bounds__(1024) calu_reorder_kernel(const int32_t* pivots, const int32_t* perm_full,
-                                                            int order_mode, int b, int64_t rows, int64_t col0,
-                                                            int64_t* pos2row, int64_t* scratch /* 3*rows */,
-                                                            int32_t* moved, int32_t* moved_cnt, int32_t* log2phys,
-                                                            DevState* st) {
+__global__ void __launch_bounds__(1024) calu_reorder_kernel(const int32_t* pivots, const int32_t* pivot_cnt,
+                                                            const int32_t* perm_full, int order_mode, int b,
+                                                            int64_t rows, int64_t col0, int64_t* pos2row,
+                                                            int64_t* scratch /* 3*rows */, int32_t* moved,
+                                                            int32_t* moved_cnt, int32_t* log2phys, DevState* st,
+                                                            int panel) {
   __shared__ int s_cnt[33];
   __shared__ int64_t pv_slot[PRRP_MAXH], vsl[PRRP_MAXH];
   __shared__ int dsl[PRRP_MAXH], s_np, s_nd;
   if (prrp_failed(st)) return;
+  // the tournament supplied fewer than b independent rows (tournament.py:210-213)
+  if (order_mode == 0 && *pivot_cnt < b) {
+    if (threadIdx.x == 0) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, *pivot_cnt, -1, 0.0);
+    return;
+  }
   const int t = threadIdx.x, T = blockDim.x;
   int64_t* oldp = scratch;                 // old pos2row (relative slots)
   int64_t* flag = scratch + rows;          // per logical position: pivot rank + 1, else 0
@@ -336,12 +356,18 @@ __global__ void __launch_bounds__(256) calu_form_negqt_kernel(const double* refl
   }
 }
 
-// flat-tree node inputs: members = [the b candidates, block rows lo .. lo+len)
-__global__ void calu_flat_inputs_kernel(const int32_t* cands, int b, int64_t lo, int len, int32_t* lpos_in,
-                                        int64_t* rowidx, const int64_t* pos2row, int64_t col0) {
+// flat-tree node inputs: members = [the candidates (b, fewer after a
+// rank-deficient node), block rows lo .. lo+len), dead rows after them
+__global__ void calu_flat_inputs_kernel(const int32_t* cands, const int32_t* ccnt, int b, int64_t lo, int len,
+                                        int32_t* lpos_in, int64_t* rowidx, int32_t* live_out,
+                                        const int64_t* pos2row, int64_t col0) {
+  const int c = ccnt[0];
   for (int t = threadIdx.x; t < b + len; t += blockDim.x) {
-    const int32_t lp = t < b ? cands[t] : (int32_t)(lo + (t - b));
+    int32_t lp = -1;
+    if (t < c) lp = cands[t];
+    else if (t < c + len) lp = (int32_t)(lo + (t - c));
     lpos_in[t] = lp;
-    rowidx[t] = pos2row[col0 + lp];
+    rowidx[t] = lp >= 0 ? pos2row[col0 + lp] : -1;
   }
+  if (threadIdx.x == 0) live_out[0] = c + len;
 }

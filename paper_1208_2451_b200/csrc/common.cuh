@@ -29,7 +29,24 @@ struct DevState {
   // strong-RRQR candidates: worst |lt| and its row-major flat index
   double cand_max;
   long long cand_flat;
+  // error ordering: the reference stops at the FIRST failure in its
+  // sequential order (panel, then tournament level, then node index); the
+  // device runs nodes of a level (and look-ahead panels) concurrently, so
+  // the recorded error is the one with the smallest (panel, level, index).
+  unsigned long long err_inv;      // ~rank of the recorded error (larger = earlier)
+  int err_lock;
 };
+
+// A row of zeros: a CALU tournament merge node whose children passed fewer
+// than b candidates (rank-deficient nodes, tournament.py:131-137) keeps its
+// static width 2b; the missing members are "dead" (row index -1) and read as
+// this zero row.  Dead members sit after every live one, so with first-max
+// ties they are never chosen, and they add exact zeros to every sum.
+__device__ __align__(16) double g_zero_row[PRRP_MAXH];
+
+__device__ __forceinline__ const double* member_row(const double* src, int64_t ld, int64_t row) {
+  return row < 0 ? g_zero_row : src + row * ld;
+}
 
 __device__ __forceinline__ bool prrp_failed(const DevState* st) {
   return *(volatile const int*)&st->code != 0;
@@ -37,14 +54,25 @@ __device__ __forceinline__ bool prrp_failed(const DevState* st) {
 
 __device__ __forceinline__ void prrp_set_error(DevState* st, int code, int panel, int index,
                                                int column, double worst, int tl = -1, int ti = -1) {
-  if (atomicCAS(&st->code, 0, code) == 0) {
+  const unsigned long long rank = ((unsigned long long)(panel + 1) << 42) |
+                                  ((unsigned long long)(tl + 1) << 21) | (unsigned long long)(ti + 1);
+  const unsigned long long inv = ~rank;
+  while (atomicCAS(&st->err_lock, 0, 1) != 0) {
+  }
+  __threadfence();
+  if (*(volatile int*)&st->code == 0 || inv > *(volatile unsigned long long*)&st->err_inv) {
+    st->err_inv = inv;
     st->panel = panel;
     st->index = index;
     st->column = column;
     st->worst = worst;
     st->tree_level = tl;
     st->tree_index = ti;
+    __threadfence();
+    atomicExch(&st->code, code);
   }
+  __threadfence();
+  atomicExch(&st->err_lock, 0);
 }
 
 __device__ __forceinline__ void atomic_max_abs(unsigned long long* slot, double v) {

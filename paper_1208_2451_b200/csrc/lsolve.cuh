@@ -66,9 +66,12 @@ __device__ int r11_checks(const double* r11, int bsel, double fro, DevState* st,
 
 // r11_checks by one warp (ballots over the diagonal; same codes and indices):
 // the first k with |r_kk| < eps*fro, else the last i with r_ii == 0.
+// want != nullptr (a CALU tournament node, tournament.py:131-137): a rank
+// failure is not an error; the node retries with want = the failing index,
+// so it is recorded there (else want = bsel).
 template <typename Diag>
 __device__ int r11_checks_warp(Diag diag, int bsel, double fro, DevState* st, int panel, bool report, int tl = -1,
-                               int ti = -1) {
+                               int ti = -1, int32_t* want = nullptr) {
   const int lane = threadIdx.x & 31;
   const double thr = PRRP_EPS * fro;
   int first_rank = -1, last_zero = -1;
@@ -81,13 +84,17 @@ __device__ int r11_checks_warp(Diag diag, int bsel, double fro, DevState* st, in
     if (bz) last_zero = k0 + 31 - __clz(bz);
   }
   if (first_rank >= 0) {
-    if (report && lane == 0) prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, first_rank, -1, 0.0, tl, ti);
+    if (report && lane == 0) {
+      if (want) *want = first_rank;
+      else prrp_set_error(st, PRRP_ERR_RANK_DEFICIENT, panel, first_rank, -1, 0.0, tl, ti);
+    }
     return 1;
   }
   if (last_zero >= 0) {
     if (report && lane == 0) prrp_set_error(st, PRRP_ERR_SINGULAR_FACTOR, panel, last_zero, -1, 0.0, tl, ti);
     return 1;
   }
+  if (report && lane == 0 && want) *want = bsel;
   return 0;
 }
 
@@ -148,16 +155,18 @@ __device__ void reduce_worst(double& worst, long long& wflat, double* red_d, lon
 // [bsel + b*TW, ...).  Block 0 performs the rank / singular checks.
 __global__ void __launch_bounds__(TRSM_TW) trsm_kernel(const double* Rbuf, int64_t p, int bsel, double* L21,
                                                       int64_t ldl, double* cand, long long* cand_flat,
-                                                      DevState* st, int panel, const double* fro) {
+                                                      DevState* st, int panel, const double* fro, int tl, int ti,
+                                                      const int32_t* live, int32_t* want) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
-  if (prrp_failed(st)) return;
+  if (prrp_failed(st) || (live && *live <= bsel)) return;
   double* r11 = sm;
   double* xs = sm + bsel * (bsel + 1) / 2;
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) r11_checks(r11, bsel, *fro, st, panel, true);
+  if (blockIdx.x == 0 && threadIdx.x < 32)
+    r11_checks_warp([&](int k) { return r11[upk(k, k)]; }, bsel, *fro, st, panel, true, tl, ti, want);
   double worst = -1.0;
   long long wflat = LLONG_MAX;
   trsm_tile(Rbuf, p, bsel, r11, xs, blockDim.x, bsel + (int64_t)blockIdx.x * blockDim.x, L21, ldl, worst, wflat);
@@ -427,47 +436,44 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
   const int c = (int)cl.block_rank(), C = (int)cl.num_blocks();
   const int t = threadIdx.x;
 
-  // reduce the fast-path candidates
+  // a tournament merge node whose children passed <= bsel rows in total
+  // selects nothing: its members go up as they are (tournament.py:128-129)
+  if (node_passes(a)) {
+    if (c == 0) {
+      for (int64_t q = t; q < a.p; q += blockDim.x) a.perm[q] = (int32_t)q;
+      if (t == 0) {
+        *a.want = *a.live;
+        f.swaps_dev[a.swap_slot] = 0;
+        if (a.node_rows) a.node_rows[a.swap_slot] = *a.live;
+      }
+    }
+    return;
+  }
+
+  // Multipliers lt = R11^-1 R12 for a leading block of bs rows over this
+  // cluster (tiles strided by CTA), then the cluster-wide worst |lt| with its
+  // row-major flat index.  Returns the first rank-deficient diagonal (node
+  // mode: the caller retries with fewer rows) or -1; other failures are
+  // reported and return -2.
   double worst = -1.0;
   long long wflat = LLONG_MAX;
-  for (int i = t; i < a.ncand; i += blockDim.x) {
-    const double w = a.cand[i];
-    const long long fl = a.cand_flat[i];
-    if (w > worst || (w == worst && fl < wflat)) { worst = w; wflat = fl; }
-  }
-  reduce_worst(worst, wflat, red_d, red_l);
-
-  int swaps = 0;
-  const int64_t ncol = a.p - a.bsel;
-  while (ncol > 0 && worst > a.tau) {
-    if (swaps >= f.swap_cap) {
-      if (c == 0 && t == 0)
-        prrp_set_error(a.st, PRRP_ERR_NONCONVERGENCE, a.panel_id, -1, -1, worst, a.tree_level, a.tree_index);
-      return;
-    }
-    const int i = (int)(wflat / ncol);
-    const int64_t jj = wflat % ncol;
-    cl.sync();
-    if (c == 0 && t == 0) {
-      const int32_t x = a.perm[i];
-      a.perm[i] = a.perm[a.bsel + jj];
-      a.perm[a.bsel + jj] = x;
-    }
-    cl.sync();
-    engine_run(a, 1, a.perm, dyn_smem, S);
-    cl.sync();
-    // rank check + multipliers over this cluster
+  auto cluster_multipliers = [&](int bs) -> int {
     double* r11 = dyn_smem;
-    double* xs = dyn_smem + a.bsel * (a.bsel + 1) / 2;
-    load_r11(a.Rbuf, a.p, a.bsel, r11);
+    double* xs = dyn_smem + bs * (bs + 1) / 2;
+    load_r11(a.Rbuf, a.p, bs, r11);
     __syncthreads();
-    if (r11_checks(r11, a.bsel, *a.fro, a.st, a.panel_id, c == 0 && t == 0, a.tree_level, a.tree_index)) return;
+    if (a.want) {
+      for (int k = 0; k < bs; ++k)
+        if (fabs(r11[upk(k, k)]) < PRRP_EPS * *a.fro) return k;
+    }
+    if (r11_checks(r11, bs, *a.fro, a.st, a.panel_id, c == 0 && t == 0, a.tree_level, a.tree_index)) return -2;
     worst = -1.0;
     wflat = LLONG_MAX;
-    const int TW = min((int)blockDim.x, a.bsel > 64 ? 64 : 128);
-    const int64_t ntile = (ncol + TW - 1) / TW;
+    const int64_t nc = a.p - bs;
+    const int TW = min((int)blockDim.x, bs > 64 ? 64 : 128);
+    const int64_t ntile = (nc + TW - 1) / TW;
     for (int64_t tile = c; tile < ntile; tile += C) {
-      trsm_tile(a.Rbuf, a.p, a.bsel, r11, xs, TW, a.bsel + tile * TW, a.L21, a.ldl, worst, wflat);
+      trsm_tile(a.Rbuf, a.p, bs, r11, xs, TW, bs + tile * TW, a.L21, a.ldl, worst, wflat);
       __syncthreads();
     }
     reduce_worst(worst, wflat, red_d, red_l);
@@ -490,14 +496,80 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
     __syncthreads();
     worst = s_worst;
     wflat = s_flat;
+    cl.sync();   // the next use of S / dyn_smem may overwrite what other CTAs still read
+    return -1;
+  };
+
+  int bs = a.bsel;
+  int swaps = 0;
+  if (a.want && *a.want < a.bsel) {
+    // rank-deficient tournament node (tournament.py:131-137): the reference
+    // retries strong_rrqr with want = the failing index; the QRCP is the same,
+    // so only the multipliers (and a possible swap loop) are redone
+    bs = *a.want;
+    while (bs > 0) {
+      const int k = cluster_multipliers(bs);
+      if (k == -2) return;
+      if (k < 0) break;
+      bs = k;
+    }
+  } else {
+    // reduce the fast-path candidates
+    for (int i = t; i < a.ncand; i += blockDim.x) {
+      const double w = a.cand[i];
+      const long long fl = a.cand_flat[i];
+      if (w > worst || (w == worst && fl < wflat)) { worst = w; wflat = fl; }
+    }
+    reduce_worst(worst, wflat, red_d, red_l);
+  }
+
+  // the strong-RRQR interchange loop (pivoted_qr.py:129-144) with leading block bs
+  while (bs > 0 && a.p - bs > 0 && worst > a.tau) {
+    const int64_t ncol = a.p - bs;
+    if (swaps >= f.swap_cap) {
+      if (c == 0 && t == 0)
+        prrp_set_error(a.st, PRRP_ERR_NONCONVERGENCE, a.panel_id, -1, -1, worst, a.tree_level, a.tree_index);
+      return;
+    }
+    const int i = (int)(wflat / ncol);
+    const int64_t jj = wflat % ncol;
+    cl.sync();
+    if (c == 0 && t == 0) {
+      const int32_t x = a.perm[i];
+      a.perm[i] = a.perm[bs + jj];
+      a.perm[bs + jj] = x;
+    }
+    cl.sync();
+    engine_run(a, 1, a.perm, dyn_smem, S);
+    cl.sync();
+    const int k = cluster_multipliers(bs);
+    if (k == -2) return;
+    if (k >= 0) {
+      // node: the re-check after a swap failed at k -> a fresh strong RRQR with
+      // want = k (the column-pivoted QR from scratch, then its multipliers)
+      bs = k;
+      swaps = 0;
+      engine_run(a, 0, a.perm, dyn_smem, S);
+      cl.sync();
+      while (bs > 0) {
+        const int k2 = cluster_multipliers(bs);
+        if (k2 == -2) return;
+        if (k2 < 0) break;
+        bs = k2;
+      }
+      continue;
+    }
     ++swaps;
   }
+  const int64_t ncol = a.p - bs;
   cl.sync();
   if (c != 0) return;
 
   if (t == 0) {
     f.swaps_dev[a.swap_slot] = swaps;
     a.st->swaps = swaps;
+    if (a.want) *a.want = bs;
+    if (a.node_rows) a.node_rows[a.swap_slot] = (int32_t)(a.live ? *a.live : a.p);
     // tournament nodes (tree_level >= 0) select rows only; the panel's
     // multiplier statistic comes from its final L21 (tournament.py:274)
     if (ncol > 0 && a.tree_level < 0) atomic_max_abs(&a.st->pmm, worst);

@@ -71,7 +71,15 @@ struct PanelArgs {
   unsigned long long* xflag;   // ngroups flags: epoch + k + 1 once group g published step k
   unsigned long long epoch;
   int fused_ak;             // panel2: fused apply + next-key pass over the shared rows
+  // CALU tournament nodes (tournament.py:118-152); all nullptr elsewhere
+  const int32_t* live;      // members actually present (<= p; the rest are dead zero rows);
+                            // live <= bsel: the node passes its members through unselected
+  int32_t* want;            // out: rows the node selects (< bsel after a rank-deficient retry)
+  int32_t* node_rows;       // out (per node slot, like swaps_out): live member count
 };
+
+// "this node passes its members through" (tournament.py:128-129: idx.shape[0] <= b)
+__device__ __forceinline__ bool node_passes(const PanelArgs& a) { return a.live && *a.live <= a.bsel; }
 
 struct Rec {
   double key;
@@ -161,7 +169,7 @@ __device__ void engine_run(const PanelArgs& a, int mode, const int32_t* perm_in,
     const int64_t q = j0 + jl;
     const int64_t j = mode == 0 ? q : (int64_t)perm_in[q];
     const int64_t row = a.rowidx ? a.rowidx[j] : j;
-    const double* s = a.src + row * a.ld;
+    const double* s = member_row(a.src, a.ld, row);
     ColRef col = col_ref(a, sdata, c, jl);
     for (int i = lane; i < h; i += 32) col[i] = s[i];
   }
@@ -351,6 +359,6 @@ __device__ void engine_run(const PanelArgs& a, int mode, const int32_t* perm_in,
 __global__ void __launch_bounds__(1024, 1) panel_qrcp_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double dyn_smem[];
   __shared__ PanelShared S;
-  if (prrp_failed(a.st)) return;
+  if (prrp_failed(a.st) || node_passes(a)) return;
   engine_run(a, a.mode, a.perm, dyn_smem, S);
 }

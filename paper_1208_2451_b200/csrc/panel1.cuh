@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
     p1_bar_init(bar0);
     p1_bar_init(bar1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    S.failed = prrp_failed(a.st);
+    S.failed = prrp_failed(a.st) || node_passes(a);
   }
   cl.sync();
   // every CTA follows CTA 0's reading of the error flag (a concurrent kernel
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(P1_T, 1) panel_qrcp1_kernel(PanelArgs a) {
     const int64_t qq = j0 + jl;
     const int64_t j = mode == 0 ? qq : (int64_t)a.perm[qq];
     const int64_t row = a.rowidx ? a.rowidx[j] : j;
-    return a.src + row * a.ld;
+    return member_row(a.src, a.ld, row);
   };
   if (on_r) {
     const double2* s = reinterpret_cast<const double2*>(src_row(jl_r));

@@ -337,6 +337,7 @@ __device__ __forceinline__ void p2_copy_smem_rows(uint32_t sb0, int tw, int L, d
 }
 
 __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
+  if (node_passes(a)) return;   // uniform over the cluster (read before any cluster barrier)
   extern __shared__ __align__(16) double sdata[];      // (P2_H - P2_W) x P2_T shared rows
   __shared__ __align__(16) P2Shared S;
   cg::cluster_group cl = cg::this_cluster();
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(P2_T, 1) panel_qrcp2_kernel(PanelArgs a) {
     const int64_t qq = j0 + t;
     const int64_t j = mode == 0 ? qq : (int64_t)a.perm[qq];
     const int64_t row = a.rowidx ? a.rowidx[j] : j;
-    const double2* src = reinterpret_cast<const double2*>(a.src + row * a.ld);
+    const double2* src = reinterpret_cast<const double2*>(member_row(a.src, a.ld, row));
 #pragma unroll
     for (int i = 0; i < P2_W / 2; ++i) { const double2 v = src[i]; rr[2 * i] = v.x; rr[2 * i + 1] = v.y; }
 #pragma unroll 8

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double sdata[];      // P64_E x P64_T smem columns
   __shared__ P64Shared S;
   cg::cluster_group cl = cg::this_cluster();
-  if (prrp_failed(a.st)) return;
+  if (prrp_failed(a.st) || node_passes(a)) return;
   const int C = (int)cl.num_blocks();
   const int c = (int)cl.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
     const int64_t qq = j0 + jl;
     const int64_t j = mode == 0 ? qq : (int64_t)a.perm[qq];
     const int64_t row = a.rowidx ? a.rowidx[j] : j;
-    return a.src + row * a.ld;
+    return member_row(a.src, a.ld, row);
   };
   if (on_r) {
     const double* s = src_row(jl_r);

@@ -423,6 +423,10 @@ struct PanelBuffers {
   int32_t* moved_cnt = nullptr;
   double* xg = nullptr;                   // multi-cluster panel exchange slots (panel2.cuh)
   unsigned long long* xflag = nullptr;
+  // CALU tournament nodes (see PanelArgs::live / want / node_rows)
+  const int32_t* live = nullptr;
+  int32_t* want = nullptr;
+  int32_t* node_rows = nullptr;
 };
 
 constexpr int kP2MaxGroups = 4;
@@ -478,6 +482,9 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   a.prof = tl_prof;
   static const int fused_ak = getenv("PRRP_P2_FUSED") ? atoi(getenv("PRRP_P2_FUSED")) : 1;
   a.fused_ak = fused_ak;
+  a.live = B.live;
+  a.want = B.want;
+  a.node_rows = B.node_rows;
   tbegin(PRRP_K_PANEL, s);
   const int maxc = caps().max_cluster;
   // CTAs: enough for the columns (one per thread in registers, a second in
@@ -536,7 +543,7 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       const int nb = (int)((ncol + tw - 1) / tw);
       // generic path keeps one candidate per 128 positions: at most kMaxCand blocks
       if (nb > kMaxCand) fail(PRRP_ERR_UNSUPPORTED, "generic trsm path limited to 131072 rows");
-      trsm_kernel<<<nb, tw, ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro);
+      trsm_kernel<<<nb, tw, ((size_t)bsel * (bsel + 1) / 2 + (size_t)bsel * tw) * 8, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti, B.live, B.want);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nb, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
@@ -546,20 +553,21 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       const int64_t cpb = TC_COLS;
       const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
       if (bsel <= 64)
-        trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti);
+        trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti,
+                                           B.live, B.want);
       else
         trsm_c2_kernel<<<nbv, TC_T, kTrsmC2Smem, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro,
-                                                       tl, ti);
+                                                       tl, ti, B.live, B.want);
       tend(s);
       CU_TRY(cudaGetLastError());
       launch_finalize(a, B, bsel, p, h, tau, nbv, D, piv, gperm, swaps_dev, do_gepp, st, panel, s);
       return;
     }
     switch ((bsel + 31) / 32) {
-      case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
-      case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
-      case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
-      default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti); break;
+      case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti, B.live, B.want); break;
+      case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti, B.live, B.want); break;
+      case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti, B.live, B.want); break;
+      default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, dyn, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti, B.live, B.want); break;
     }
     tend(s);
     CU_TRY(cudaGetLastError());
@@ -1247,6 +1255,8 @@ struct CaluOut {
   DevState* st = nullptr;
   int32_t* swaps_dev = nullptr;
   int32_t* node_swaps = nullptr;
+  int32_t* node_rows = nullptr;
+  int64_t n = 0;
   std::vector<int64_t> charges;
   std::vector<std::vector<std::pair<int64_t, int>>> node_members;   // (members, node slot)
   int npanels = 0, maxnodes = 0, b = 0;
@@ -1323,6 +1333,14 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
     nb.rowidx = rowidx_all + (size_t)i * 2 * b;
   }
   int32_t* cands = ar.get<int32_t>((size_t)2 * nnodes * b);        // two levels (ping-pong)
+  // per node: candidates passed up (< b after a rank-deficient node,
+  // tournament.py:131-137), live members of a merge node, and per slot the
+  // member count for the flop charges (tournament.py:224-234)
+  int32_t* ccnt = ar.get<int32_t>((size_t)2 * nnodes);
+  int32_t* want_all = ar.get<int32_t>((size_t)nnodes);
+  int32_t* live_all = ar.get<int32_t>((size_t)nnodes);
+  int32_t* node_rows = ar.get<int32_t>((size_t)npanels * maxnodes);
+  CU_TRY(cudaMemsetAsync(node_rows, 0, sizeof(int32_t) * npanels * maxnodes, s));
   int32_t* node_swaps = ar.get<int32_t>((size_t)npanels * maxnodes);
   CU_TRY(cudaMemsetAsync(node_swaps, 0, sizeof(int32_t) * npanels * maxnodes, s));
   const int32_t** perms_dev = ar.get<const int32_t*>(nnodes);
@@ -1370,7 +1388,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaEventCreateWithFlags(&qe, cudaEventDisableTiming));
         leaf_qrcp_ev.push_back(qe);
       }
-      strong_rrqr_panel(A + col0, lda, bj, cnt[i], bj, tau, panel, nodes[i].L21, nodes[i].ldl, nodes[i].B, st,
+      PanelBuffers nbuf = nodes[i].B;
+      nbuf.live = leaves ? nullptr : live_all + i;
+      nbuf.want = want_all + i;
+      nbuf.node_rows = node_rows + (size_t)panel * maxnodes;
+      strong_rrqr_panel(A + col0, lda, bj, cnt[i], bj, tau, panel, nodes[i].L21, nodes[i].ldl, nbuf, st,
                         node_swaps + (size_t)panel * maxnodes, nullptr, nullptr, nullptr, false, ns, ridx,
                         slot0 + i, level, i, qe);
     }
@@ -1480,23 +1502,29 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         ++slot;
         int32_t* cur = cands;
         int32_t* nxt = cands + (size_t)b;
-        calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
+        int32_t* ccur = ccnt;
+        int32_t* cnxt = ccnt + 1;
+        calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, want_all, live_all, 0, cur, ccur,
+                                              2 * b);
         int level = 1;
         for (int64_t lo = first; lo < rows; lo += bj, ++level) {
           const int64_t len = std::min<int64_t>(bj, rows - lo);
-          calu_flat_inputs_kernel<<<1, 128, 0, sm>>>(cur, bj, lo, (int)len, lpos_all, rowidx_all, pos2row, col0);
+          calu_flat_inputs_kernel<<<1, 128, 0, sm>>>(cur, ccur, bj, lo, (int)len, lpos_all, rowidx_all, live_all,
+                                                     pos2row, col0);
           run_level(std::vector<int64_t>{0}, std::vector<int64_t>{bj + len}, false, col0, bj, panel, level, slot, sm);
           chg3 += qr_charge3(bj + len, bj);
           node_members[panel].push_back({bj + len, slot});
           ++slot;
-          calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
+          calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, want_all, live_all, 1, nxt, cnxt,
+                                                2 * b);
           std::swap(cur, nxt);
+          std::swap(ccur, cnxt);
         }
         CU_TRY(cudaGetLastError());
         charges[panel] = chg3;
         tbegin(PRRP_K_OTHER, sm);
-        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
-                                                st);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, ccur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc,
+                                                log2phys, st, panel);
         tend(sm);
       } else if (p_eff == 1) {
         // single node: the selector's own full order and l_block (tournament.py:168-177)
@@ -1504,8 +1532,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                           nullptr, false, sm, pos2row + col0);
         flush_after_main();
         tbegin(PRRP_K_OTHER, sm);
-        calu_reorder_kernel<<<1, 1024, 0, sm>>>(nullptr, Bk.perm, 1, bj, rows, col0, pos2row, scratch, mv, mc,
-                                                log2phys, st);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(nullptr, nullptr, Bk.perm, 1, bj, rows, col0, pos2row, scratch, mv,
+                                                mc, log2phys, st, panel);
         tend(sm);
       } else {
         // leaves: contiguous logical blocks, first blocks larger (tournament.py:64-88)
@@ -1538,14 +1566,18 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         slot += (int)p_eff;
         int32_t* cur = cands;
         int32_t* nxt = cands + (size_t)maxnodes * b;
-        calu_select_kernel<<<(unsigned)p_eff, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, cur, 2 * b);
+        int32_t* ccur = ccnt;
+        int32_t* cnxt = ccnt + maxnodes;
+        calu_select_kernel<<<(unsigned)p_eff, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, want_all, live_all,
+                                                             0, cur, ccur, 2 * b);
         int64_t ncur = p_eff;
         int level = 1;
         while (ncur > 1) {
           const int64_t nmerge = ncur / 2;
-          // node i of this level reads lpos_all/rowidx_all[i*2b .. i*2b + 2b) (stride 2b even when bj < b)
-          calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(cur, bj, (int)(2 * nmerge), lpos_all,
-                                                                      rowidx_all, pos2row, col0, 2 * b);
+          // node i of this level reads lpos_all/rowidx_all[i*2b .. i*2b + 2b) (stride 2b even when bj < b);
+          // members = [left's candidates, right's candidates], dead (zero) rows after them
+          calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(cur, ccur, bj, (int)(2 * nmerge), lpos_all,
+                                                                      rowidx_all, live_all, pos2row, col0, 2 * b);
           CU_TRY(cudaGetLastError());
           std::vector<int64_t> mlo(nmerge, 0), mcnt(nmerge, 2 * bj);
           run_level(mlo, mcnt, false, col0, bj, panel, level, slot, sm);
@@ -1554,19 +1586,23 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
             node_members[panel].push_back({2 * bj, slot + (int)i});
           }
           slot += (int)nmerge;
-          calu_select_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, nxt, 2 * b);
-          if (ncur % 2)   // odd node promoted unmerged (tournament.py:197-198)
+          calu_select_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, want_all, live_all,
+                                                                1, nxt, cnxt, 2 * b);
+          if (ncur % 2) {   // odd node promoted unmerged (tournament.py:197-198)
             CU_TRY(cudaMemcpyAsync(nxt + nmerge * bj, cur + (ncur - 1) * bj, sizeof(int32_t) * bj,
                                    cudaMemcpyDeviceToDevice, sm));
+            CU_TRY(cudaMemcpyAsync(cnxt + nmerge, ccur + (ncur - 1), sizeof(int32_t), cudaMemcpyDeviceToDevice, sm));
+          }
           ncur = nmerge + (ncur % 2);
           std::swap(cur, nxt);
+          std::swap(ccur, cnxt);
           ++level;
         }
         charges[panel] = chg3;
         // new logical order [pivots, rest ascending]; move the pivot rows to slots col0..
         tbegin(PRRP_K_OTHER, sm);
-        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
-                                                st);
+        calu_reorder_kernel<<<1, 1024, 0, sm>>>(cur, ccur, nullptr, 0, bj, rows, col0, pos2row, scratch, mv, mc,
+                                                log2phys, st, panel);
         tend(sm);
       }
       if (w1_prev) CU_TRY(cudaStreamWaitEvent(sm, w1_prev, 0));
@@ -1664,16 +1700,16 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           const int64_t cpb = bj <= 64 ? TC_COLS : 4 * TC_COLS;
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
           if (bj <= 64)
-            trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1);
+            trsm_c_kernel<<<nblk, TC_T, 0, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1, nullptr, nullptr);
           else
             trsm_c2_kernel<<<nblk, TC_T, kTrsmC2Smem, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel,
-                                                            fro_inf, -1, -1);
+                                                            fro_inf, -1, -1, nullptr, nullptr);
         } else {
           nblk = (int)std::min<int64_t>(kMaxCand, (ncol + TTC - 1) / TTC);
           const size_t tdyn = (((size_t)bj * (bj + 1) / 2 + 1) / 2 * 2 + (size_t)bj * TTCP) * 8;
           switch ((bj + 31) / 32) {
-            case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
-            default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1); break;
+            case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1, nullptr, nullptr); break;
+            default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, sm>>>(B.Rbuf, rows, bj, Lg, ldl, B.cand, B.cand_flat, st, panel, fro_inf, -1, -1, nullptr, nullptr); break;
           }
         }
         calu_stats_kernel<<<1, 256, 0, sm>>>(B.cand, nblk, node_swaps + (size_t)panel * maxnodes, maxnodes,
@@ -1761,8 +1797,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       // last square block: logical order (all columns, on the side stream, which
       // has seen every earlier update and row move), then GEPP
       tbegin(PRRP_K_OTHER, sd);
-      calu_reorder_kernel<<<1, 1024, 0, sd>>>(nullptr, ident, 1, bj, rows, col0, pos2row, scratch, mv, mc, log2phys,
-                                              st);
+      calu_reorder_kernel<<<1, 1024, 0, sd>>>(nullptr, nullptr, ident, 1, bj, rows, col0, pos2row, scratch, mv, mc,
+                                              log2phys, st, panel);
       tend(sd);
       tbegin(PRRP_K_PERMUTE, sd);
       permute_cols(0, n, col0, mv, mc, perm, panel, sd);
@@ -1800,6 +1836,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   out.st = st;
   out.swaps_dev = swaps_dev;
   out.node_swaps = node_swaps;
+  out.node_rows = node_rows;
+  out.n = n;
   out.charges = std::move(charges);
   out.node_members = std::move(node_members);
   out.npanels = npanels;
@@ -1964,14 +2002,22 @@ int caluprrp_finish(const CaluOut& out, cudaStream_t s, int32_t* swap_counts, in
   racecheck_end();
   std::vector<int32_t> sw(npanels);
   CU_TRY(cudaMemcpy(sw.data(), swaps_dev, sizeof(int32_t) * npanels, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> nsw((size_t)npanels * maxnodes);
+  std::vector<int32_t> nsw((size_t)npanels * maxnodes), nrows((size_t)npanels * maxnodes);
   CU_TRY(cudaMemcpy(nsw.data(), node_swaps, sizeof(int32_t) * nsw.size(), cudaMemcpyDeviceToHost));
+  CU_TRY(cudaMemcpy(nrows.data(), out.node_rows, sizeof(int32_t) * nrows.size(), cudaMemcpyDeviceToHost));
   if (swap_counts) memcpy(swap_counts, sw.data(), sizeof(int32_t) * npanels);
   if (tchg3) {
+    // _tournament_charges (tournament.py:224-234): nodes of more than b members,
+    // (1 + swaps) x _charge_qr(members, b); member counts as the device saw them
+    // (a merge node shrinks when a child was rank deficient)
     for (int k = 0; k < npanels; ++k) {
       if (charges[k] < 0) { tchg3[k] = -1; continue; }
+      const int bk = (int)std::min<int64_t>(b, out.n - (int64_t)k * b);
       int64_t c3 = 0;
-      for (auto& mm : node_members[k]) c3 += (1 + nsw[(size_t)k * maxnodes + mm.second]) * qr_charge3(mm.first, b);
+      for (auto& mm : node_members[k]) {
+        const int64_t r = nrows[(size_t)k * maxnodes + mm.second];
+        if (r > bk) c3 += (1 + nsw[(size_t)k * maxnodes + mm.second]) * qr_charge3(r, bk);
+      }
       tchg3[k] = c3;
     }
   }
@@ -2536,12 +2582,12 @@ int prrp_multiplier_block(const double* R, int64_t ldr, int32_t b, int64_t p, do
       const bool c2 = b > 64 && use_trsm_c2();
       const int nblk = (int)std::min<int64_t>(kMaxCand, c2 ? (ncol + TC_COLS - 1) / TC_COLS : (ncol + TTC - 1) / TTC);
       const size_t tdyn = (((size_t)b * (b + 1) / 2 + 1) / 2 * 2 + (size_t)b * TTCP) * 8;
-      if (c2) trsm_c2_kernel<<<nblk, TC_T, kTrsmC2Smem, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1);
+      if (c2) trsm_c2_kernel<<<nblk, TC_T, kTrsmC2Smem, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1, nullptr, nullptr);
       else switch ((b + 31) / 32) {
-        case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
-        case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
-        case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
-        default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1); break;
+        case 1: trsm_w_kernel<1><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1, nullptr, nullptr); break;
+        case 2: trsm_w_kernel<2><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1, nullptr, nullptr); break;
+        case 3: trsm_w_kernel<3><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1, nullptr, nullptr); break;
+        default: trsm_w_kernel<4><<<nblk, TW_WARPS * 32, tdyn, s>>>(Rbuf, p, b, L, ldl, cand, candf, st, -1, fro0, -1, -1, nullptr, nullptr); break;
       }
       calu_stats_kernel<<<1, 256, 0, s>>>(cand, nblk, cand == nullptr ? nullptr : (const int32_t*)nullptr, 0,
                                           (int32_t*)fro0, 0, st);

@@ -39,19 +39,20 @@ template <int NR>
 __global__ void __launch_bounds__(TW_WARPS * 32) trsm_w_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                               double* L21, int64_t ldl, double* cand,
                                                               long long* cand_flat, DevState* st, int panel,
-                                                              const double* fro, int tl, int ti) {
+                                                              const double* fro, int tl, int ti,
+                                                              const int32_t* live, int32_t* want) {
   extern __shared__ __align__(16) double sm[];
   double* r11 = sm;                                    // packed upper, bsel(bsel+1)/2
   double* tile = sm + ((bsel * (bsel + 1) / 2 + 1) & ~1);   // bsel x TTCP
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
   __shared__ double rcp[PRRP_MAXH];
-  if (prrp_failed(st)) return;
+  if (prrp_failed(st) || (live && *live <= bsel)) return;
   load_r11(Rbuf, p, bsel, r11);
   __syncthreads();
   for (int i = threadIdx.x; i < bsel; i += blockDim.x) rcp[i] = __drcp_rn(r11[upk(i, i)]);
   if (blockIdx.x == 0 && threadIdx.x < 32)
-    r11_checks_warp([&](int k) { return r11[upk(k, k)]; }, bsel, *fro, st, panel, true, tl, ti);
+    r11_checks_warp([&](int k) { return r11[upk(k, k)]; }, bsel, *fro, st, panel, true, tl, ti, want);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t ncol = p - bsel;
   double worst = -1.0;
@@ -189,7 +190,7 @@ template <int NQ, int UP>
 __device__ __forceinline__ void trsm_c_body(double* us, double* dg, double* rc, double* red_d, long long* red_l,
                                             const double* __restrict__ Rbuf, int64_t p, int bsel, double* L21,
                                             int64_t ldl, double* cand, long long* cand_flat, DevState* st, int panel,
-                                            const double* fro, int tl, int ti) {
+                                            const double* fro, int tl, int ti, int32_t* want) {
   constexpr int BW = 8 * NQ;   // padded R11 width
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int nk = (bsel + 7) >> 3, bp = nk * 8;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void trsm_c_body(double* us, double* dg, double* rc, 
     rc[i] = __drcp_rn(dg[i]);
   }
   if (blockIdx.x == 0 && t < 32)
-    r11_checks_warp([&](int k) { return us[k * UP + k]; }, bsel, frov, st, panel, true, tl, ti);
+    r11_checks_warp([&](int k) { return us[k * UP + k]; }, bsel, frov, st, panel, true, tl, ti, want);
   TC_STAMP(5);
   __syncthreads();
   TC_STAMP(1);
@@ -261,13 +262,15 @@ __device__ __forceinline__ void trsm_c_body(double* us, double* dg, double* rc, 
 
 __global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                       double* L21, int64_t ldl, double* cand, long long* cand_flat,
-                                                      DevState* st, int panel, const double* fro, int tl, int ti) {
+                                                      DevState* st, int panel, const double* fro, int tl, int ti,
+                                                      const int32_t* live, int32_t* want) {
   __shared__ __align__(16) double us[64 * TC_UP];
   __shared__ __align__(16) double dg[64], rc[64];
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
-  if (prrp_failed(st)) return;
-  trsm_c_body<8, TC_UP>(us, dg, rc, red_d, red_l, Rbuf, p, bsel, L21, ldl, cand, cand_flat, st, panel, fro, tl, ti);
+  if (prrp_failed(st) || (live && *live <= bsel)) return;
+  trsm_c_body<8, TC_UP>(us, dg, rc, red_d, red_l, Rbuf, p, bsel, L21, ldl, cand, cand_flat, st, panel, fro, tl, ti,
+                        want);
 }
 
 // b in (64, 128]: 16 chunks per column, R11 (128 x TC_UP2) in dynamic shared memory
@@ -275,13 +278,14 @@ __global__ void __launch_bounds__(TC_T) trsm_c_kernel(const double* __restrict__
 constexpr size_t kTrsmC2Smem = (size_t)(128 * TC_UP2 + 2 * 128) * 8;
 __global__ void __launch_bounds__(TC_T) trsm_c2_kernel(const double* __restrict__ Rbuf, int64_t p, int bsel,
                                                        double* L21, int64_t ldl, double* cand, long long* cand_flat,
-                                                       DevState* st, int panel, const double* fro, int tl, int ti) {
+                                                       DevState* st, int panel, const double* fro, int tl, int ti,
+                                                       const int32_t* live, int32_t* want) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red_d[33];
   __shared__ long long red_l[33];
-  if (prrp_failed(st)) return;
+  if (prrp_failed(st) || (live && *live <= bsel)) return;
   trsm_c_body<16, TC_UP2>(dsm, dsm + 128 * TC_UP2, dsm + 128 * TC_UP2 + 128, red_d, red_l, Rbuf, p, bsel, L21, ldl,
-                          cand, cand_flat, st, panel, fro, tl, ti);
+                          cand, cand_flat, st, panel, fro, tl, ti, want);
 }
 
 // out[r][j] = sum_{k >= j} L21[r][gperm[k]] * L11[k][j]

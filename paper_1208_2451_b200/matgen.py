@@ -99,3 +99,23 @@ def gen_kahan_panel(p, b, theta, scale, seed):
     k = (k * rs[:, None]) * cd[None, :]
     r = (gen_randn_rect(b, p - b, seed) * scale) * rs[:, None]
     return np.hstack([k, r])
+
+
+def gen_deficient_block(n, seed, blocks, cols):
+    """randn(n, seed) with numerically rank-deficient row blocks in the first
+    `cols` columns: for each (r0, r1, rank) in `blocks`, row r0 + i of the
+    block becomes base row (i mod rank) scaled by 2^(i // rank), the
+    base rows being the block's own first `rank` rows.  Power-of-two scaling
+    is exact, so the block has exact rank `rank`; no two rows are equal
+    (equal columns tie exactly, and which copy wins is then decided by the
+    BLAS kernel's rounding, not by the algorithm), and a column-pivoted QR of
+    its transpose meets roundoff-level diagonals after `rank` steps -- a
+    CALU tournament node whose strong RRQR reports RankDeficient and passes
+    on fewer than b rows (tournament.py:131-137).  Elementwise only (no
+    BLAS), so the bits do not depend on the host."""
+    a = np.array(gen_randn(n, seed, order="C"))
+    for r0, r1, rank in blocks:
+        base = a[r0:r0 + rank, :cols].copy()
+        for i in range(r1 - r0):
+            a[r0 + i, :cols] = base[i % rank] * (2.0 ** (i // rank))
+    return np.asfortranarray(a)

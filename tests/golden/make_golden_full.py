@@ -189,6 +189,33 @@ def case_srrqr(name, p, b, tau, kahan=None):
     return meta, arrays
 
 
+def case_calu_deficient(name, n, b, P, blocks, tau=2.0):
+    """CALU_PRRP with rank-deficient tournament nodes (tournament.py:131-137):
+    the full factorization (or the reference's error) on a small matrix."""
+    a = pmg.gen_deficient_block(n, 11, blocks, b)
+    tree = prrp.binary_tree(P) if P > 0 else prrp.flat_tree()
+    meta = {"kind": "calu_deficient", "n": n, "b": b, "P": P, "tau": tau, "blocks": blocks, "seed": 11,
+            "input_sha": sha(a)}
+    arrays = {}
+    try:
+        f = prrp.caluprrp_factor(a, b, tau, tree)
+    except ArithmeticError as exc:
+        meta["error"] = {"type": type(exc).__name__, "index": getattr(exc, "index", None),
+                         "column": getattr(exc, "column", None), "panel": getattr(exc, "panel", None),
+                         "tree_node": list(exc.tree_node) if getattr(exc, "tree_node", None) else None}
+        return meta, arrays
+    arrays["perm"] = np.asarray(f.perm, dtype=np.int64)
+    arrays["l"] = f.l
+    arrays["u"] = f.u
+    meta["stats"] = stats_dict(f.stats)
+    perm0, trace = prrp.tournament_select(np.asfortranarray(a[:, :b]), b, tau, tree, "srrqr")
+    arrays["t0_perm"] = np.asarray(perm0, dtype=np.int64)
+    meta["t0_trace"] = [{"level": nd.level, "index": nd.index, "members": nd.members.tolist(),
+                         "selected": nd.selected.tolist(), "swap_count": int(nd.swap_count)} for nd in trace.nodes]
+    meta["rel_residual"] = rel_residual(a, f.perm, f.l, f.u)
+    return meta, arrays
+
+
 CASES = {
     "c2_b64": lambda: case_lu("c2_b64", "randn", 8192, 64),
     "c2_b128": lambda: case_lu("c2_b128", "randn", 8192, 128),
@@ -197,6 +224,19 @@ CASES = {
     "c4_prefix": lambda: case_calu_prefix("c4_prefix", "randn", 16384, 64, 8),
     "c5_prefix": lambda: case_calu_prefix("c5_prefix", "urand", 32768, 128, 4),
 }
+# rank-deficient tournament nodes: a leaf that passes fewer than b rows; two
+# deficient leaves whose merge passes its members through (<= b); the flat
+# tree; a panel whose whole tournament supplies fewer than b rows (error);
+# b = 64 / 128 nodes on the register engines
+CASES["calu_def_leaf160_b16_P4"] = lambda: case_calu_deficient("calu_def_leaf160_b16_P4", 160, 16, 4, [[0, 40, 5]])
+CASES["calu_def_pair160_b16_P4"] = lambda: case_calu_deficient("calu_def_pair160_b16_P4", 160, 16, 4,
+                                                               [[0, 40, 5], [40, 80, 6]])
+CASES["calu_def_flat160_b16"] = lambda: case_calu_deficient("calu_def_flat160_b16", 160, 16, 0, [[0, 32, 7]])
+CASES["calu_def_root96_b16_P4"] = lambda: case_calu_deficient("calu_def_root96_b16_P4", 96, 16, 4, [[0, 96, 9]])
+CASES["calu_def_leaf640_b64_P8"] = lambda: case_calu_deficient("calu_def_leaf640_b64_P8", 640, 64, 8,
+                                                               [[0, 80, 20], [160, 240, 30]])
+CASES["calu_def_leaf1024_b128_P4"] = lambda: case_calu_deficient("calu_def_leaf1024_b128_P4", 1024, 128, 4,
+                                                                 [[0, 256, 50], [256, 512, 60]])
 for _p in (4097, 6000, 8192, 12288, 16384):
     for _b in (64, 128):
         CASES["srrqr_p%d_b%d" % (_p, _b)] = (lambda p=_p, b=_b: case_srrqr("srrqr_p%d_b%d" % (p, b), p, b, 2.0))

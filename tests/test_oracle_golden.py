@@ -208,3 +208,74 @@ def orc_pairwise(x):
         s += x[i]
         i += 1
     return s
+
+
+# ------------------------------------------------------------ full-size / deficient-node fixtures
+def _full(name):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full", name)
+    return json.load(open(path + ".json")), dict(np.load(path + ".npz"))
+
+
+def _full_names(prefix):
+    import glob
+    import os
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full")
+    return sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(d, prefix + "*.json")))
+
+
+@pytest.mark.parametrize("name", _full_names("calu_def_"))
+def test_oracle_calu_rank_deficient_nodes(name):
+    """The oracle's tournament (tournament.py:118-152 restated) shrinks a
+    rank-deficient node's selection like the reference: same permutation,
+    factors, node trace and error on the deficient-node fixtures."""
+    from paper_1208_2451_b200 import matgen
+    meta, arr = _full(name)
+    a = matgen.gen_deficient_block(meta["n"], meta["seed"], meta["blocks"], meta["b"])
+    assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == meta["input_sha"]
+    shape, leaf = ("flat", 8) if meta["P"] == 0 else ("binary", meta["P"])
+    if "error" in meta:
+        with pytest.raises(ArithmeticError) as ei:
+            orc.calu_prrp(a, meta["b"], meta["tau"], shape, leaf)
+        assert type(ei.value).__name__.replace("Oracle", "") == meta["error"]["type"]
+        assert getattr(ei.value, "index", None) == meta["error"]["index"]
+        assert getattr(ei.value, "panel", None) == meta["error"]["panel"]
+        return
+    f = orc.calu_prrp(a, meta["b"], meta["tau"], shape, leaf)
+    assert np.array_equal(f.perm, arr["perm"])
+    _close(f.l, arr["l"], False)
+    _close(f.u, arr["u"], False)
+    perm, trace = orc.tournament(np.asfortranarray(a[:, :meta["b"]]), meta["b"], meta["tau"], shape, leaf)
+    assert np.array_equal(perm, arr["t0_perm"])
+    got = [(n.level, n.index, n.members.tolist(), n.selected.tolist()) for n in trace.nodes]
+    assert got == [(d["level"], d["index"], d["members"], d["selected"]) for d in meta["t0_trace"]]
+
+
+@pytest.mark.parametrize("name", _full_names("srrqr_"))
+def test_oracle_srrqr_large_p(name):
+    """strong_rrqr at p in 4097..16384 (the device engines' multi-CTA paths):
+    the oracle against the reference's permutation, swaps and R11."""
+    from paper_1208_2451_b200 import matgen
+    meta, arr = _full(name)
+    p, b = meta["p"], meta["b"]
+    if meta.get("kahan"):
+        at = matgen.gen_kahan_panel(p, b, meta["kahan"][0], meta["kahan"][1], meta["seed"])
+    else:
+        at = matgen.gen_randn_rect(p, b, meta["seed"]).T
+    res = orc.srrqr(np.asfortranarray(at), b, meta["tau"])
+    assert np.array_equal(res.qr.perm, arr["perm"])
+    assert res.swap_count == meta["swap_count"]
+    _close(res.qr.r[:, :b], arr["r11"], False)
+
+
+def test_full_size_generators_match_reference():
+    """The repo's generators reproduce the reference's matgen bits at the
+    BASELINE sizes (checksums recorded by make_golden_full.py)."""
+    from paper_1208_2451_b200 import matgen
+    meta, _ = _full("c3_foster")
+    a = matgen.gen_foster(meta["n"], 1.0, 1.0, 1.0)
+    assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == meta["input_sha"]
+    meta, _ = _full("c3_wilkinson")
+    a = matgen.gen_wilkinson(meta["n"])
+    assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == meta["input_sha"]
