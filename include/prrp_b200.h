@@ -221,6 +221,42 @@ int prrp_lu_residual(const double* A, int64_t lda, const double* LU, int64_t ldl
 int prrp_lu_solve(const double* LU, int64_t ldlu, int64_t n, const int64_t* perm, const double* B,
                   int64_t ldb, double* X, int64_t ldx, int32_t nrhs, prrp_err* err, void* stream);
 
+/* ---- Distributed CALU_PRRP, one process per GPU (
+ * PAPER.md:1739-1751 layout, 2885-2951 per-panel pattern).  Replaces
+ * prrp.caluprrp_factor (tournament.py:237-296) when the matrix is spread
+ * over `nranks` GPUs: column block-cyclic (process grid 1 x nranks, block b):
+ * global column block J lives on rank J mod nranks as local block
+ * J div nranks, all m rows (A_loc row-major m x n_loc, lda even).  The
+ * library does not communicate: per panel k the caller runs
+ *     owner (k mod nranks):  prrp_calu_dist_select(k)
+ *     everyone:              broadcast msg[k & 1][0 .. msg_bytes(k)) from the owner
+ *                            prrp_calu_dist_apply(k, 0)
+ * (the owner of panel k+1 may run apply(k, 1), select(k+1), apply(k, 2):
+ * look-ahead), then prrp_calu_dist_stats, a MAX all-reduce of the int64
+ * stats record over the ranks, and prrp_calu_dist_finish.  Every rank ends
+ * with the same perm (device, m) and its columns of the packed L\U; the
+ * results are bit-identical to prrp_caluprrp on one GPU. */
+int prrp_calu_dist_create(void** handle, double* A_loc, int64_t lda, int64_t m, int64_t n, int64_t n_loc,
+                          int32_t b, double tau, int32_t leaf_count, int32_t nranks, int32_t rank,
+                          int64_t* perm, prrp_err* err, void* stream);
+/* Device buffers: the two panel messages (parity k & 1), their capacity in
+ * bytes, and the int64 statistics record to be MAX-reduced (length). */
+int prrp_calu_dist_buffers(void* handle, void** msg0, void** msg1, int64_t* msg_capacity, void** stats,
+                           int64_t* stats_len);
+/* Bytes of panel k's message that must be broadcast (-1 on a bad panel). */
+int64_t prrp_calu_dist_msg_bytes(void* handle, int32_t panel);
+int prrp_calu_dist_select(void* handle, int32_t panel, prrp_err* err, void* stream);
+/* part: 0 = all, 1 = head (all but the trailing update beyond the next
+ * panel's block), 2 = tail (that update). */
+int prrp_calu_dist_apply(void* handle, int32_t panel, int32_t part, prrp_err* err, void* stream);
+int prrp_calu_dist_stats(void* handle, prrp_err* err, void* stream);
+/* reduced: the MAX-reduced statistics record (device; NULL = this rank's own).
+ * Outputs as prrp_caluprrp; the error is the owner's first failure (every
+ * rank reports the same). */
+int prrp_calu_dist_finish(void* handle, const int64_t* reduced, int32_t* swap_counts,
+                          int64_t* tournament_charge3, prrp_stats* stats, prrp_err* err, void* stream);
+void prrp_calu_dist_destroy(void* handle);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,15 @@ SIGNATURES = {
     "prrp_calu": ([_P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_gepp_select": ([_P, _I64, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
     "prrp_gepp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_create": ([_P, _P, _I64, _I64, _I64, _I64, _I32, _D, _I32, _I32, _I32, _P, _P, _P],
+                              ctypes.c_int),
+    "prrp_calu_dist_buffers": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_msg_bytes": ([_P, _I32], ctypes.c_int64),
+    "prrp_calu_dist_select": ([_P, _I32, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_apply": ([_P, _I32, _I32, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_stats": ([_P, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_finish": ([_P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_calu_dist_destroy": ([_P], None),
 }
 
 _lib = None

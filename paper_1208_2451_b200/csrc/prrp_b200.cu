@@ -829,14 +829,15 @@ void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const do
 }
 
 void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, const double* D, const int32_t* gperm,
-                       int64_t* perm, DevState* st, cudaStream_t s) {
+                       int64_t* perm, DevState* st, cudaStream_t s, int64_t bl = 1, int nr = 1, int rk = 0) {
+  if (n <= 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 4, (n + TC - 1) / TC);
   const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
-    case 1: blockrow_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
-    case 2: blockrow_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
-    case 3: blockrow_w_kernel<3><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
-    default: blockrow_w_kernel<4><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st); break;
+    case 1: blockrow_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk); break;
+    case 2: blockrow_w_kernel<2><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk); break;
+    case 3: blockrow_w_kernel<3><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk); break;
+    default: blockrow_w_kernel<4><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk); break;
   }
 }
 
@@ -2275,6 +2276,8 @@ int gepp_full_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, 
   if (omax) *omax = bits_to_double(hs.orig_max);
   return state_to_err(hs, err);
 }
+#include "calu_dist.cuh"
+
 }  // namespace
 
 // ======================================================================== ABI
@@ -2675,6 +2678,122 @@ int prrp_gepp(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, doubl
   } catch (const Fail& f) {
     return report(err, f);
   }
+}
+
+// ---------------------------------------------------------------- distributed CALU_PRRP (calu_dist.cuh)
+int prrp_calu_dist_create(void** handle, double* A_loc, int64_t lda, int64_t m, int64_t n, int64_t n_loc, int32_t b,
+                          double tau, int32_t leaf_count, int32_t nranks, int32_t rank, int64_t* perm, prrp_err* err,
+                          void* stream) {
+  clear_err(err);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!handle) fail(PRRP_ERR_ARG, "null handle");
+    if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
+    if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
+    if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
+    if (leaf_count < 0) fail(PRRP_ERR_ARG, "binary tree needs a leaf count >= 1 (0 selects the flat tree)");
+    if (b > PRRP_MAXH) fail(PRRP_ERR_UNSUPPORTED, "panel width > 128 is outside the device panel engine");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(PRRP_ERR_ARG, "bad rank / nranks");
+    const int64_t npan = (n + b - 1) / b;
+    int64_t want_loc = 0;
+    for (int64_t J = rank; J < npan; J += nranks) want_loc += std::min<int64_t>(b, n - J * b);
+    if (n_loc != want_loc) fail(PRRP_ERR_DIM, "n_loc does not match the column block-cyclic layout");
+    if (lda < std::max<int64_t>(n_loc, 1) || (lda & 1) || ((uintptr_t)A_loc % 16)) fail(PRRP_ERR_ARG, "lda must be even, >= n_loc, A 16-byte aligned");
+    caps();
+    std::unique_ptr<CaluDist> w(new CaluDist);
+    w->m = m; w->n = n; w->n_loc = n_loc; w->lda = lda; w->b = b; w->tau = tau; w->P = leaf_count;
+    w->nranks = nranks; w->rank = rank; w->npanels = (int)npan; w->A = A_loc; w->perm = perm;
+    calu_dist_alloc(*w, s);
+    calu_dist_structure(*w);
+    *handle = w.release();
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_calu_dist_buffers(void* handle, void** msg0, void** msg1, int64_t* msg_capacity, void** stats,
+                           int64_t* stats_len) {
+  CaluDist* w = static_cast<CaluDist*>(handle);
+  if (!w) return PRRP_ERR_ARG;
+  if (msg0) *msg0 = w->msgs[0];
+  if (msg1) *msg1 = w->msgs[1];
+  if (msg_capacity) *msg_capacity = (int64_t)w->msg_cap;
+  if (stats) *stats = w->red;
+  if (stats_len) *stats_len = (int64_t)w->red_len;
+  return PRRP_OK;
+}
+
+int64_t prrp_calu_dist_msg_bytes(void* handle, int32_t panel) {
+  CaluDist* w = static_cast<CaluDist*>(handle);
+  if (!w || panel < 0 || panel >= w->npanels) return -1;
+  const int64_t col0 = (int64_t)panel * w->b;
+  const int64_t rows = w->m - col0, bj = std::min<int64_t>(w->b, w->n - col0);
+  // the single-node order region is needed only when the panel has one node
+  if (rows > bj && w->p_eff(panel) > 1) return (int64_t)w->msg_bytes(panel);
+  if (rows <= bj) return (int64_t)w->off_full;
+  return (int64_t)w->msg_bytes(panel);
+}
+
+int prrp_calu_dist_select(void* handle, int32_t panel, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    CaluDist* w = static_cast<CaluDist*>(handle);
+    if (!w || panel < 0 || panel >= w->npanels) fail(PRRP_ERR_ARG, "bad handle or panel");
+    if (w->owner(panel) != w->rank) fail(PRRP_ERR_ARG, "select runs on the panel's owner only");
+    calu_dist_select(*w, panel, (cudaStream_t)stream);
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_calu_dist_apply(void* handle, int32_t panel, int32_t part, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    CaluDist* w = static_cast<CaluDist*>(handle);
+    if (!w || panel < 0 || panel >= w->npanels) fail(PRRP_ERR_ARG, "bad handle or panel");
+    if (part < 0 || part > 2) fail(PRRP_ERR_ARG, "part must be 0 (all), 1 (head) or 2 (tail)");
+    calu_dist_apply(*w, panel, part, (cudaStream_t)stream);
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_calu_dist_stats(void* handle, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    CaluDist* w = static_cast<CaluDist*>(handle);
+    if (!w) fail(PRRP_ERR_ARG, "bad handle");
+    const int nslots = w->npanels * w->maxnodes;
+    dist_stats_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(w->st, w->swaps_dev, w->npanels, w->node_swaps,
+                                                              w->node_rows, nslots, w->red);
+    CU_TRY(cudaGetLastError());
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_calu_dist_finish(void* handle, const int64_t* reduced, int32_t* swap_counts, int64_t* tournament_charge3,
+                          prrp_stats* stats, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    CaluDist* w = static_cast<CaluDist*>(handle);
+    if (!w) fail(PRRP_ERR_ARG, "bad handle");
+    return calu_dist_finish(*w, reduced ? reduced : w->red, swap_counts, tournament_charge3, stats, err,
+                            (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+void prrp_calu_dist_destroy(void* handle) {
+  CaluDist* w = static_cast<CaluDist*>(handle);
+  if (!w) return;
+  cudaDeviceSynchronize();
+  delete w;
 }
 
 }  // extern "C"

@@ -344,10 +344,15 @@ __global__ void __launch_bounds__(TW_WARPS * 32) compose_w_kernel(const double* 
 
 // Block-row finish (see blockrow_kernel): columns [0, col0) permuted by the
 // GEPP order, [col0, col0+b) from D, [col0+b, n) eliminated.
+// Columns are local indices c < n; their global index (which decides the L
+// part / diagonal block / trailing role) is g = ((c / bl) nr + rk) bl + c % bl
+// -- a column block-cyclic layout over nr ranks (rank rk, block bl); the
+// single-GPU driver passes nr = 1, rk = 0 (g = c).
 template <int NR>
 __global__ void __launch_bounds__(TW_WARPS * 32) blockrow_w_kernel(double* A, int64_t lda, int64_t col0, int b,
                                                                   int64_t n, const double* __restrict__ D,
-                                                                  const int32_t* gperm, int64_t* p, DevState* st) {
+                                                                  const int32_t* gperm, int64_t* p, DevState* st,
+                                                                  int64_t bl, int nr, int rk) {
   extern __shared__ __align__(16) double sm[];
   double* lc = sm;                       // lc[k*b + i] = L11[i][k] (column k contiguous)
   double* tile = sm + b * b;             // b x TCP
@@ -376,12 +381,14 @@ __global__ void __launch_bounds__(TW_WARPS * 32) blockrow_w_kernel(double* A, in
       const int i = e / TC, cc = e % TC;
       if (cc >= tc) continue;
       const int64_t j = c0 + cc;
-      tile[i * TCP + cc] = (j >= col0 && j < col0 + b) ? D[i * b + (j - col0)] : A[(col0 + s_gp[i]) * lda + j];
+      const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
+      tile[i * TCP + cc] = (g >= col0 && g < col0 + b) ? D[i * b + (g - col0)] : A[(col0 + s_gp[i]) * lda + j];
     }
     __syncthreads();
     for (int cc = warp; cc < tc; cc += TW_WARPS) {
       const int64_t j = c0 + cc;
-      if (j < col0 + b) continue;                      // L part / diagonal block: data movement only
+      const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
+      if (g < col0 + b) continue;                      // L part / diagonal block: data movement only
       double x[NR];
 #pragma unroll
       for (int u = 0; u < NR; ++u) {

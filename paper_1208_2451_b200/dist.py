@@ -1,291 +1,261 @@
-"""Distributed CALU_PRRP over N processes (one per GPU), torch.distributed.
+"""Distributed CALU_PRRP: one process per GPU, device-resident.
 
-SURVEY.md 8(e): LU_PRRP does not shard (replicas only); CALU_PRRP shards
-through its tournament tree.  This module distributes the trailing matrix by
-row blocks of b rows, cyclically over the ranks (the P_r x 1 case of the
-paper's 2-D block-cyclic layout), and follows the
-per-panel message pattern of Appendix D:
+Layout: a 2-D block-cyclic grid P_r x P_c with block
+size b; this implementation is the P_r = 1 column of that family: global
+column block J (b columns) lives on rank J mod P_c, every rank keeps all m
+rows of its blocks in HBM (row-major, m x n_loc).  LU_PRRP itself does not
+shard (its panel QRCP needs a global argmax every column step; SURVEY.md
+8(e): replicas only) -- CALU_PRRP does, through the tournament.
 
-  1. all-gather the b panel columns of the trailing rows (logical order)
-  2. tournament: leaf i (the reference's contiguous logical blocks,
-     tournament.py:64-88) is factored by rank i % N; the candidate sets
-     (b row ids per leaf) are all-gathered; the merges (2b x b nodes) are
-     recomputed identically on every rank, so the pivot choice is independent
-     of N (P stays fixed at the tree's leaf count)
-  3. L21 for the local non-pivot rows from the unpivoted QR of the pivot block
-     (the reflectors are fixed by the b pivot columns)
-  4. all-reduce (sum) of the pivot rows' trailing part A12 (owners contribute)
-  5. local Schur update, GEPP finish of the block row (identical on every
-     rank), compose of the local multipliers
-  6. statistics: max-all-reduce of the local maxima
+Per panel k (Appendix D), all device work in
+libprrp_b200.so (include/prrp_b200.h, prrp_calu_dist_*):
 
-Rows never move between ranks; the logical order is bookkeeping (identical
-on every rank).  The per-rank arithmetic is delegated to an ops object
-(`DeviceOps`: the B200 C ABI).  The result equals the single-process
-caluprrp_factor for every N.
+  owner (k mod P_c)   prrp_calu_dist_select: the tournament over the panel's
+                      rows (the reference's tree, tournament.py:155-217), the
+                      reorder, the final QR and L21, GEPP of the pivot block,
+                      packed into one device message
+  all ranks           broadcast of the message (NCCL via torch.distributed on
+                      device memory; host-staged for gloo), then
+                      prrp_calu_dist_apply: the same reorder, row moves, the
+                      block-row finish and the DMMA trailing update of the
+                      rank's own columns
+  end                 MAX all-reduce of the statistics record
+
+The owner of panel k + 1 runs apply(k) in two parts around its select(k+1)
+(look-ahead of depth one).  Every element of the result is bit-identical to
+the single-GPU prrp_caluprrp (same kernels, same k order per element).
 """
+import ctypes
 from dataclasses import dataclass
 from fractions import Fraction
 
 import numpy as np
 
-from .luprrp import BlockLUFactors, ElimStats, _qr_charge, _finish_charge
+from . import _lib
 from .errors import DimensionMismatch
+from .luprrp import BlockLUFactors, ElimStats, _validate, as_matrix, flop_counters
 
 
-def row_owner(i, b, world):
-    """Rank owning global row i: row blocks of b rows, cyclic over ranks."""
-    return (i // b) % world
+# ------------------------------------------------------------------ layout (host logic)
+def owned_blocks(n, b, world, rank):
+    """Global column blocks of `rank`: J = rank, rank + world, ..."""
+    npan = (n + b - 1) // b
+    return list(range(rank, npan, world))
 
 
-def leaf_partition(rows, b, leaf_count):
-    """tournament.py:76-88 (binary): contiguous, near-equal, first larger."""
-    p_eff = max(1, min(leaf_count, rows // (b + 1)))
-    base, extra = divmod(rows, p_eff)
-    out, start = [], 0
-    for i in range(p_eff):
-        size = base + (1 if i < extra else 0)
-        out.append((start, start + size))
-        start += size
+def local_columns(n, b, world, rank):
+    """Global column indices of rank's local columns, in local order."""
+    cols = [np.arange(J * b, min(n, (J + 1) * b)) for J in owned_blocks(n, b, world, rank)]
+    return np.concatenate(cols) if cols else np.zeros(0, dtype=np.int64)
+
+
+def panel_owner(k, world):
+    return k % world
+
+
+def global_column(c, b, world, rank):
+    """Global index of local column c (the map blockrow_w applies on the device)."""
+    return ((c // b) * world + rank) * b + c % b
+
+
+def scatter_columns(a, b, world, rank):
+    """Rank's local columns of the m x n matrix a (row-major copy, lda even)."""
+    cols = local_columns(a.shape[1], b, world, rank)
+    loc = np.ascontiguousarray(a[:, cols])
+    return loc, cols
+
+
+def assemble_columns(blocks, n, b):
+    """Inverse of scatter_columns: {rank: local m x n_loc} -> m x n."""
+    world = len(blocks)
+    m = next(iter(blocks.values())).shape[0]
+    out = np.empty((m, n))
+    for r, loc in blocks.items():
+        out[:, local_columns(n, b, world, r)] = loc
     return out
 
 
-def merge_schedule(nleaves):
-    """Binary merge levels with the odd node promoted (tournament.py:188-200):
-    list of levels, each a list of (left, right) index pairs or (idx,) for a
-    promoted node, over the previous level's candidate list."""
-    levels = []
-    n = nleaves
-    while n > 1:
-        lvl = [(i, i + 1) for i in range(0, n - 1, 2)]
-        if n % 2:
-            lvl.append((n - 1,))
-        levels.append(lvl)
-        n = len(lvl)
-    return levels
+# ------------------------------------------------------------------ transport
+class Transport:
+    """Collectives on device tensors through torch.distributed: NCCL runs on
+    the device buffers (stream-ordered, NVLink); gloo (CPU tests, or several
+    processes sharing one GPU) stages through host memory."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.on = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.nccl = self.on and dist.get_backend(group) == "nccl"
+
+    def broadcast(self, t, src):
+        if self.world == 1:
+            return
+        if self.nccl:
+            self.dist.broadcast(t, src=src, group=self.group)
+            return
+        h = t.cpu()
+        self.dist.broadcast(h, src=src, group=self.group)
+        t.copy_(h)
+
+    def all_reduce_max(self, t):
+        if self.world == 1:
+            return
+        if self.nccl:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+            return
+        h = t.cpu()
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+        t.copy_(h)
+
+    def all_gather_cpu(self, t):
+        if self.world == 1:
+            return [t]
+        out = [t.new_empty(t.shape) for _ in range(self.world)]
+        if self.nccl:
+            self.dist.all_gather(out, t, group=self.group)
+            return out
+        h = t.cpu()
+        outs = [h.new_empty(h.shape) for _ in range(self.world)]
+        self.dist.all_gather(outs, h, group=self.group)
+        return outs
 
 
+class _CudaView:
+    """Zero-copy torch view of a device buffer owned by the library."""
+
+    def __init__(self, ptr, nbytes, typestr="|u1", itemsize=1):
+        self.__cuda_array_interface__ = {"shape": (nbytes // itemsize,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _view(ptr, nbytes, dtype="u1"):
+    import torch
+    ts = {"u1": ("|u1", 1), "i8": ("<i8", 8)}[dtype]
+    return torch.as_tensor(_CudaView(ptr, nbytes, *ts), device="cuda")
+
+
+# ------------------------------------------------------------------ driver
 @dataclass
-class PanelPlan:
-    col0: int
-    bj: int
-    rows: int
-    width: int
-    leaves: list
+class DistFactors:
+    perm: object          # torch int64 [m] (device), identical on every rank
+    lu: object            # torch float64 [m, n_loc] view: this rank's columns of the packed L\U
+    cols: np.ndarray      # global column index of every local column
+    m: int
+    n: int
+    panel_width: int
+    stats: ElimStats
 
 
-def plan_panels(m, n, b, leaf_count):
-    col0, out = 0, []
-    while col0 < n:
-        bj = min(b, n - col0)
-        rows = m - col0
-        out.append(PanelPlan(col0, bj, rows, n - col0 - bj,
-                             leaf_partition(rows, bj, leaf_count) if rows > bj else []))
-        col0 += bj
-    return out
-
-
-class DeviceOps:
-    """Per-rank arithmetic on the local B200 through the C ABI."""
-
-    def __init__(self):
-        from . import pivoted_qr
-        self._pq = pivoted_qr
-
-    def srrqr(self, node_rows, want, tau):
-        """strong RRQR of the node rows' panel transpose -> (order, swaps, l_block)."""
-        res = self._pq.strong_rrqr(node_rows.T, want, tau)
-        return np.asarray(res.qr.perm), int(res.swap_count), res.l_block
-
-    def householder_qr(self, a):
-        f = self._pq.householder_qr(a)
-        return f.q, f.r
-
-    def multipliers(self, pivot_block, rows):
-        """(R11^-1 R12)^T for the given rows from the unpivoted QR of
-        [pivot_block; rows]^T (tournament.py:271-272)."""
-        import paper_1208_2451_b200 as prrp
-        a = np.vstack([pivot_block, rows]).T
-        _, r = self.householder_qr(a)
-        b = pivot_block.shape[0]
-        if rows.shape[0] == 0:
-            return np.zeros((0, b))
-        return prrp.multiplier_block(r, b)
-
-    def schur(self, c, l21, a12):
-        import paper_1208_2451_b200 as prrp
-        return prrp.rank_update(c, l21, a12)
-
-    def gepp(self, block_row):
-        import paper_1208_2451_b200 as prrp
-        return prrp.gepp_factor(block_row)
-
-    def matmul(self, a, b):
-        import paper_1208_2451_b200 as prrp
-        return prrp.matmul(a, b)
-
-
-def _allgather_obj(dist, group, obj):
-    out = [None] * dist.get_world_size(group)
-    dist.all_gather_object(out, obj, group=group)
-    return out
-
-
-def caluprrp_factor_dist(a, b, tau=2.0, leaf_count=8, group=None, ops=None):
-    """Row-distributed CALU_PRRP.  Every rank passes the same global matrix
-    `a` (each uses only the rows it owns); rank 0 returns BlockLUFactors, the
-    other ranks return None."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    ops = ops or DeviceOps()
-    a = np.asarray(a, dtype=np.float64)
-    m, n = a.shape
+def caluprrp_factor_dist_device(A_loc, m, n, b, tau=2.0, tree=None, group=None, lookahead=True):
+    """In-place distributed CALU_PRRP of the rank's local columns A_loc (a CUDA
+    float64 tensor, m x lda_loc, lda even, the first n_loc columns are the
+    rank's blocks in local order).  Collective over `group`."""
+    import torch
+    from .tournament import binary_tree
+    if tree is None:
+        tree = binary_tree(8)
+    leaf_count = int(tree.leaf_count) if tree.shape == "binary" else 0
+    tp = Transport(group)
+    world, rank = tp.world, tp.rank
     if m < n:
         raise DimensionMismatch("need at least as many rows as columns")
     if not 1 <= b <= n:
         raise ValueError(f"panel width {b} out of range [1, {n}]")
     if tau <= 1.0:
         raise ValueError("tau must exceed 1")
-    mine = np.array([i for i in range(m) if row_owner(i, b, world) == rank], dtype=np.intp)
-    work = {int(i): a[i].copy() for i in mine}          # local rows (full width)
-    lpart = {int(i): np.zeros(n) for i in mine}         # local L rows
-    order = list(range(m))                              # logical position -> global row
-    omax = max(_allgather_obj(dist, group, float(np.abs(a[mine]).max()) if len(mine) else 0.0))
-    inter, finish, pmm = omax, omax, 0.0
-    swaps_all, charged, executed = [], Fraction(0), Fraction(0)
+    n_loc = len(local_columns(n, b, world, rank))
+    lib = _lib.device_lib()
+    stream = _lib.stream_handle()
+    perm = torch.empty(m, dtype=torch.int64, device="cuda")
+    h = ctypes.c_void_p()
+    err = _lib.PrrpErr()
+    rc = lib.prrp_calu_dist_create(ctypes.byref(h), ctypes.c_void_p(A_loc.data_ptr()), A_loc.stride(0), m, n, n_loc,
+                                   b, float(tau), leaf_count, world, rank, ctypes.c_void_p(perm.data_ptr()),
+                                   ctypes.byref(err), stream)
+    _lib.raise_for(rc, err, "prrp_calu_dist_create")
+    try:
+        m0, m1, cap, sp, sl = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p(), ctypes.c_int64()
+        lib.prrp_calu_dist_buffers(h, ctypes.byref(m0), ctypes.byref(m1), ctypes.byref(cap), ctypes.byref(sp),
+                                   ctypes.byref(sl))
+        msgs = (_view(m0.value, cap.value), _view(m1.value, cap.value))
+        red = _view(sp.value, sl.value * 8, "i8")
+        npan = (n + b - 1) // b
 
-    for pl in plan_panels(m, n, b, leaf_count):
-        col0, bj, rows, width = pl.col0, pl.bj, pl.rows, pl.width
-        trailing = order[col0:]
-        # 1. all-gather the panel columns of the trailing rows
-        contrib = {g: work[g][col0:col0 + bj] for g in trailing if g in work}
-        panel_rows = {}
-        for part in _allgather_obj(dist, group, contrib):
-            panel_rows.update(part)
-        panel = np.array([panel_rows[g] for g in trailing])
-        charged += _qr_charge(rows, bj)
-        if rows > bj:
-            leaves = pl.leaves
-            if len(leaves) == 1:
-                sel, sw, l21_all = ops.srrqr(panel, bj, tau)
-                rel = list(sel)
-                swaps_all.append(sw)
-                executed += (1 + sw) * _qr_charge(rows, bj)
-                single = True
-            else:
-                # 2. leaves on their owner ranks, candidates all-gathered
-                local = {}
-                for li, (lo, hi) in enumerate(leaves):
-                    if li % world == rank:
-                        sel, sw, _ = ops.srrqr(panel[lo:hi], bj, tau)
-                        local[li] = (list(lo + np.asarray(sel[:bj])), sw, hi - lo)
-                allc = {}
-                for part in _allgather_obj(dist, group, local):
-                    allc.update(part)
-                cands = [allc[i][0] for i in range(len(leaves))]
-                nodes = [(allc[i][2], allc[i][1]) for i in range(len(leaves))]
-                for lvl in merge_schedule(len(cands)):
-                    nxt = []
-                    for pair in lvl:
-                        if len(pair) == 1:
-                            nxt.append(cands[pair[0]])
-                            continue
-                        idx = cands[pair[0]] + cands[pair[1]]
-                        sel, sw, _ = ops.srrqr(panel[idx], bj, tau)
-                        nxt.append([idx[j] for j in sel[:bj]])
-                        nodes.append((len(idx), sw))
-                    cands = nxt
-                piv = cands[0]
-                pset = set(piv)
-                rel = list(piv) + [i for i in range(rows) if i not in pset]
-                extra = sum(((1 + sw) * _qr_charge(r, bj) for r, sw in nodes if r > bj), Fraction(0))
-                charged += extra
-                executed += extra + _qr_charge(rows, bj)
-                swaps_all.append(sum(sw for _, sw in nodes))
-                single = False
-            new_trailing = [trailing[i] for i in rel]
-            order[col0:] = new_trailing
-            pivots = new_trailing[:bj]
-            rest_local = [g for g in new_trailing[bj:] if g in work]
-            # 3. multipliers of the local non-pivot rows
-            piv_block = np.array([panel_rows[g] for g in pivots])
-            if single:
-                # the single node's own l_block (tournament.py:263-266); row t <-> position bj + t
-                pos = {g: t for t, g in enumerate(new_trailing[bj:])}
-                l21 = np.array([l21_all[pos[g]] for g in rest_local]).reshape(len(rest_local), bj)
-            else:
-                rows_local = np.array([panel_rows[g] for g in rest_local]).reshape(len(rest_local), bj)
-                l21 = ops.multipliers(piv_block, rows_local)
-            lmax = float(np.abs(l21).max()) if l21.size else 0.0
-            pmm = max(pmm, max(_allgather_obj(dist, group, lmax)))
-            for t, g in enumerate(rest_local):
-                lpart[g][col0:col0 + bj] = l21[t]
-            # 4. pivot rows' trailing part to every rank (sum-reduce of owner contributions)
-            import torch
-            a12 = np.zeros((bj, width))
-            for q, g in enumerate(pivots):
-                if g in work:
-                    a12[q] = work[g][col0 + bj:]
-            t12 = torch.from_numpy(a12)
-            dist.all_reduce(t12, group=group)
-            a12 = t12.numpy()
-            # 5. local Schur update
-            if width and rest_local:
-                c = np.array([work[g][col0 + bj:] for g in rest_local])
-                upd = ops.schur(c, l21, a12)
-                for t, g in enumerate(rest_local):
-                    work[g][col0 + bj:] = upd[t]
-                umax = float(np.abs(upd).max()) if upd.size else 0.0
-            else:
-                umax = 0.0
-            if width:
-                inter = max(inter, max(_allgather_obj(dist, group, umax)))
-        else:
-            swaps_all.append(0)
-            pivots = order[col0:col0 + bj]
-            rest_local = []
-            a12 = np.zeros((bj, width))
-            piv_block = np.array([panel_rows[g] for g in pivots])
-            l21 = np.zeros((0, bj))
-        upd_c = Fraction(2 * bj * (rows - bj) * width)
-        charged += upd_c
-        executed += upd_c
-        # 6. GEPP finish of the block row (identical on every rank)
-        block_row = np.hstack([piv_block, a12])
-        gf = ops.gepp(block_row)
-        finish = max(finish, float(gf.intermediate_max))
-        gperm = list(gf.perm)
-        order[col0:col0 + bj] = [pivots[i] for i in gperm]
-        for q, g in enumerate(order[col0:col0 + bj]):
-            if g in work:
-                work[g][col0:] = gf.u[q]
-                lpart[g][col0:col0 + bj] = gf.l[q]
-        if rest_local and col0 + bj < m:
-            comp = ops.matmul(l21[:, gperm], gf.l)
-            for t, g in enumerate(rest_local):
-                lpart[g][col0:col0 + bj] = comp[t]
-            executed += Fraction(2 * (m - col0 - bj) * bj * bj)
-        elif col0 + bj < m:
-            executed += Fraction(2 * (m - col0 - bj) * bj * bj)
-        fin = _finish_charge(bj, n - col0)
-        charged += fin
-        executed += fin
+        def check(rc, what):
+            _lib.raise_for(rc, err, what)
 
-    # gather the factors on rank 0 in logical order
-    rows_out = {g: (lpart[g], work[g]) for g in work}
-    gathered = _allgather_obj(dist, group, rows_out)
-    if rank != 0:
-        return None
-    allrows = {}
-    for part in gathered:
-        allrows.update(part)
-    l = np.array([allrows[g][0] for g in order])
-    w = np.array([allrows[g][1] for g in order])
-    l = np.tril(l, -1)
+        if rank == panel_owner(0, world):
+            check(lib.prrp_calu_dist_select(h, 0, ctypes.byref(err), stream), "prrp_calu_dist_select")
+        for k in range(npan):
+            nb = lib.prrp_calu_dist_msg_bytes(h, k)
+            tp.broadcast(msgs[k & 1][:nb], panel_owner(k, world))
+            nxt = k + 1 < npan and rank == panel_owner(k + 1, world)
+            if nxt and lookahead:
+                check(lib.prrp_calu_dist_apply(h, k, 1, ctypes.byref(err), stream), "prrp_calu_dist_apply")
+                check(lib.prrp_calu_dist_select(h, k + 1, ctypes.byref(err), stream), "prrp_calu_dist_select")
+                check(lib.prrp_calu_dist_apply(h, k, 2, ctypes.byref(err), stream), "prrp_calu_dist_apply")
+            else:
+                check(lib.prrp_calu_dist_apply(h, k, 0, ctypes.byref(err), stream), "prrp_calu_dist_apply")
+                if nxt:
+                    check(lib.prrp_calu_dist_select(h, k + 1, ctypes.byref(err), stream), "prrp_calu_dist_select")
+        check(lib.prrp_calu_dist_stats(h, ctypes.byref(err), stream), "prrp_calu_dist_stats")
+        tp.all_reduce_max(red)
+        swaps = (ctypes.c_int32 * npan)()
+        chg3 = (ctypes.c_int64 * npan)()
+        st = _lib.PrrpStats()
+        rc = lib.prrp_calu_dist_finish(h, ctypes.c_void_p(red.data_ptr()), swaps, chg3, ctypes.byref(st),
+                                       ctypes.byref(err), stream)
+        _lib.raise_for(rc, err, "caluprrp_factor_dist")
+    finally:
+        lib.prrp_calu_dist_destroy(h)
+    extra = [None if c < 0 else Fraction(int(c), 3) for c in chg3]
+    charged, executed = flop_counters(m, n, b, list(swaps), tournament_extra=extra)
+    stats = ElimStats(original_max=st.original_max, intermediate_max=st.intermediate_max,
+                      finish_max=st.finish_max, swap_counts=list(map(int, swaps)),
+                      flops_charged=charged, flops_executed=executed,
+                      panel_multiplier_max=st.panel_multiplier_max)
+    return DistFactors(perm=perm, lu=A_loc[:, :n_loc], cols=local_columns(n, b, world, rank), m=m, n=n,
+                       panel_width=b, stats=stats)
+
+
+def caluprrp_factor_dist(a, b, tau=2.0, tree=None, group=None, lookahead=True):
+    """caluprrp_factor (tournament.py:237-296) over the ranks of `group`:
+    every rank passes the same host matrix (or None except on... every rank
+    needs its own columns, taken here from `a`); returns the full
+    BlockLUFactors on every rank (gathered).  For large matrices use
+    caluprrp_factor_dist_device with each rank's columns already resident."""
+    import torch
+    a = as_matrix(a)
+    _validate(a, b, tau)
+    m, n = a.shape
+    tp = Transport(group)
+    loc, cols = scatter_columns(a, b, tp.world, tp.rank)
+    lda = max(2, loc.shape[1] + (loc.shape[1] & 1))
+    A = torch.zeros((m, lda), dtype=torch.float64, device="cuda")
+    if loc.shape[1]:
+        A[:, :loc.shape[1]].copy_(torch.from_numpy(loc))
+    f = caluprrp_factor_dist_device(A, m, n, b, tau, tree, group, lookahead)
+    packed = gather_packed(f, tp)
+    l = np.tril(packed, -1)[:, :n]
     l[np.arange(n), np.arange(n)] = 1.0
-    u = np.triu(w[:n])
-    stats = ElimStats(original_max=omax, intermediate_max=inter, finish_max=finish, swap_counts=swaps_all,
-                      flops_charged=charged, flops_executed=executed, panel_multiplier_max=pmm)
-    return BlockLUFactors(perm=np.array(order, dtype=np.intp), l=np.asfortranarray(l), u=np.asfortranarray(u),
-                          panel_width=b, stats=stats)
+    u = np.triu(packed[:n, :])
+    return BlockLUFactors(perm=f.perm.cpu().numpy().astype(np.intp), l=np.asfortranarray(l),
+                          u=np.asfortranarray(u), panel_width=b, stats=f.stats)
+
+
+def gather_packed(f, tp):
+    """The packed m x n L\\U assembled from every rank's columns (host)."""
+    import torch
+    nmax = max(len(local_columns(f.n, f.panel_width, tp.world, r)) for r in range(tp.world))
+    pad = torch.zeros((f.m, max(nmax, 1)), dtype=torch.float64, device=f.lu.device)
+    if f.lu.shape[1]:
+        pad[:, :f.lu.shape[1]].copy_(f.lu)
+    parts = tp.all_gather_cpu(pad)
+    blocks = {}
+    for r, t in enumerate(parts):
+        nl = len(local_columns(f.n, f.panel_width, tp.world, r))
+        blocks[r] = t[:, :nl].cpu().numpy()
+    return assemble_columns(blocks, f.n, f.panel_width)
