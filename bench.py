@@ -1,25 +1,39 @@
 #!/usr/bin/env python
-"""LU_PRRP factorization throughput on B200 (BASELINE.json metric).
+"""CALU_PRRP / LU_PRRP factorization throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-One step = one full LU_PRRP factorization of BASELINE config 2 (randn(8192,
-seed 42), panel b=64, tau=2) with the matrix already resident in HBM (a
-fresh device copy is restored between steps, outside the timed region).
-value = (2n^3/3) / t_factor in GFLOP/s, device-timed with CUDA events.
-The 512 MiB input exceeds the 126 MB L2, so no extra flush is needed.
+Headline workload (north_star, BASELINE config 5): CALU_PRRP of U(-1,1)
+n = 32768 (seed 42, 8 GiB FP64), panel b = 128, tau = 2, binary tournament
+tree over P = 8 row blocks.  One step = one full factorization with the
+matrix resident in HBM (a fresh device copy is restored between steps,
+outside the timed region; the 8 GiB input exceeds the 126 MB L2, so no flush
+is needed).  value = (2n^3/3) / t_factor in GFLOP/s, device-timed with CUDA
+events on the launching stream.
 
-LU_PRRP does not shard (replicas only): under torchrun every
-rank factors its own replica; value = N * F / max-over-ranks time.
+  N = 1   the single-GPU driver (prrp_caluprrp: three-stream look-ahead,
+          graph-captured, replayed)
+  N > 1   under torchrun, one process per GPU: the distributed driver
+          (dist.py / prrp_calu_dist_*): column block-cyclic layout, the
+          panel owner's tournament broadcast over NCCL, every rank updating
+          its own columns; value = whole-job GFLOP/s over the max-over-ranks
+          time (strong scaling: the problem size is fixed)
+
+Secondary lines in `config` (N = 1): LU_PRRP on config 2 (randn 8192,
+b = 64 and 128), CALU_PRRP on config 4 (randn 16384, b = 64), and
+calu_factor (the GEPP tournament baseline, n = 8192).
 
 --impl reference times the reference algorithm's CPU implementation (the
 numpy restatement in oracle/, bit-identical to the reference package on the
-fixture host) on a bounded sample of the same workload: the first panels of
-the same factorization, GFLOP/s over those panels' share of 2n^3/3.
+fixture host) on a bounded sample of the same workload, with all host cores:
+the first panel of config 5 on the columns that panel's pivoting and update
+reach (the first 2b columns), GFLOP/s over that sample's algorithmic flops.
 """
 import argparse
+import ctypes
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -30,88 +44,112 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "LU_PRRP factorization GFLOP/s (2n^3/3)"
+METRIC = "CALU_PRRP factorization GFLOP/s (2n^3/3), BASELINE config 5"
 UNIT = "GFLOP/s"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--b", type=int, default=64)
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=128)
+    ap.add_argument("--P", type=int, default=8)
     ap.add_argument("--tau", type=float, default=2.0)
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-panels", type=int, default=2, help="panels in the bounded CPU sample")
+    ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--secondary-b", type=int, default=128, help="also report this panel width (0 = off)")
-    ap.add_argument("--calu-n", type=int, default=16384,
-                    help="also time CALU_PRRP (BASELINE config 4: randn(n), b=64, binary tree P=8); 0 = off")
-    ap.add_argument("--gcalu-n", type=int, default=8192, help="calu_factor (GEPP tournament) size (0 = off)")
-    ap.add_argument("--calu5-n", type=int, default=32768,
-                    help="also time CALU_PRRP (BASELINE config 5 on 1 GPU: U(-1,1), b=128, P=8); 0 = off")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-panels", type=int, default=1, help="panels in the bounded CPU sample")
     return ap.parse_args()
 
 
 def dist_info():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def lu_flops(n):
     return 2.0 * n ** 3 / 3.0
 
 
-def panel_share_flops(n, col0, bj):
-    s = n - col0
-    return 2.0 * (s ** 3 - (s - bj) ** 3) / 3.0
+def rect_lu_flops(m, w):
+    """Algorithmic flops of the LU of an m x w (m >= w) matrix: m w^2 - w^3/3."""
+    return m * w * w - w ** 3 / 3.0
 
 
-def config_dict(args, extra=None):
-    d = {"workload": f"LU_PRRP BASELINE config 2: randn(n={args.n}, seed {args.seed}), b={args.b}, tau={args.tau}",
-         "n": args.n, "b": args.b, "tau": args.tau, "matrix_bytes": args.n * args.n * 8,
-         "l2": "input 512 MiB > 126 MB L2 (no flush needed); fresh copy restored between steps",
-         "parallelism": "replicas" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single-gpu"}
-    if extra:
-        d.update(extra)
-    return d
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model
+
+
+def workload(args, ws):
+    return {"workload": f"CALU_PRRP BASELINE config 5: U(-1,1) n={args.n} (seed {args.seed}), b={args.b}, "
+                        f"tau={args.tau}, binary tournament tree P={args.P}",
+            "n": args.n, "b": args.b, "P": args.P, "tau": args.tau, "matrix_bytes": args.n * args.n * 8,
+            "l2": "input 8 GiB > 126 MB L2 (no flush needed); fresh device copy restored between steps",
+            "parallelism": (f"column block-cyclic over {ws} GPUs (process grid 1 x {ws}), panel owner's "
+                            "tournament broadcast over NCCL" if ws > 1 else "single GPU")}
 
 
 # ------------------------------------------------------------------ reference arm
+def cpu_sample(args, a_cols=None):
+    """The oracle on the first `cpu_panels` panels of config 5 restricted to the
+    columns they touch; returns (seconds, flops, description)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    from oracle import prrp_oracle as orc
+    from paper_1208_2451_b200 import matgen
+    k = max(1, args.cpu_panels)
+    w = (k + 1) * args.b
+    if a_cols is None:
+        a_cols = matgen.gen_urand_cols(args.n, args.seed, w)
+    t0 = time.perf_counter()
+    orc.calu_prrp(np.asfortranarray(a_cols[:, :w]), args.b, args.tau, "binary", args.P, panel_limit=k)
+    dt = time.perf_counter() - t0
+    flops = rect_lu_flops(args.n, w) - rect_lu_flops(args.n - k * args.b, w - k * args.b)
+    desc = (f"oracle.calu_prrp (numpy/OpenBLAS restatement of tournament.py:237-296) on the first {k} panel(s) "
+            f"of config 5 (n={args.n}, b={args.b}, P={args.P}) restricted to the first {w} columns (the columns "
+            f"those panels pivot and update; the rest of the matrix does not influence them): {dt:.1f} s; "
+            f"GFLOP/s over the sample's algorithmic flops m w^2 - w^3/3 (first {k} panels). The sample is "
+            f"tournament-dominated: the full factorization runs a larger share of BLAS-2 updates (SURVEY 8(d) "
+            f"extrapolates ~1.5 GFLOP/s for the whole run)")
+    return dt, flops, desc
+
+
+def cpu_descr():
+    return {"cores": os.cpu_count(), "cpu_model": cpu_info(),
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "openblas_coretype": os.environ.get("OPENBLAS_CORETYPE", "(unset: OpenBLAS DYNAMIC_ARCH auto-detect)")}
+
+
 def run_reference(args):
     ws, rank, _ = dist_info()
     if rank != 0:
         return
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-    from oracle import prrp_oracle as orc
-    a = orc.randn_matrix(args.n, args.seed)
-    panels = max(1, args.cpu_panels)
-    flops = sum(panel_share_flops(args.n, k * args.b, args.b) for k in range(panels))
+    from paper_1208_2451_b200 import matgen
+    a_cols = matgen.gen_urand_cols(args.n, args.seed, (max(1, args.cpu_panels) + 1) * args.b)
     times = []
+    desc, flops = "", 0.0
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        orc.lu_prrp(a, args.b, args.tau, panel_limit=panels)
-        dt = time.perf_counter() - t0
+        dt, flops, desc = cpu_sample(args, a_cols)
         if i >= args.warmup:
             times.append(dt)
     t = statistics.mean(times)
     value = flops / t / 1e9
-    cores = os.cpu_count()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference matgen recipe, seed 42)",
-            "impl": "reference",
-            "config": config_dict(args, {"sample": f"first {panels} panels of the factorization per step"}),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"oracle.lu_prrp (numpy/OpenBLAS restatement of luprrp.py:153-201), "
-                                       f"first {panels} of {args.n // args.b} panels of n={args.n}, b={args.b}; "
-                                       f"GFLOP/s over their share of 2n^3/3",
-                             "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")},
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference matgen conventions: PCG64 seed 42)",
+            "impl": "reference", "config": dict(workload(args, 1), sample=desc),
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "kind": "port", "sample": desc}, **cpu_descr()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -128,8 +166,6 @@ class ClockSampler:
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
 
     def start(self):
-        if os.environ.get("PRRP_BENCH_NOCLOCKS"):
-            return
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
@@ -164,26 +200,66 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def device_run(lib, _lib, torch, pristine, work, m, n, lda, b, tau, timed=True):
-    import ctypes
-    work.copy_(pristine)
-    perm = torch.empty(m, dtype=torch.int64, device=work.device)
-    npan = (n + b - 1) // b
-    swaps = (ctypes.c_int32 * npan)()
-    st = _lib.PrrpStats()
-    err = _lib.PrrpErr()
-    tm = _lib.PrrpTiming()
+def calu_call(lib, _lib, buf, n, b, tau, P, perm, timing=None):
+    npc = (n + b - 1) // b
+    sw = (ctypes.c_int32 * npc)()
+    chg = (ctypes.c_int64 * npc)()
+    st, err = _lib.PrrpStats(), _lib.PrrpErr()
+    if timing is None:
+        rc = lib.prrp_caluprrp(ctypes.c_void_p(buf.data_ptr()), buf.stride(0), n, n, b, float(tau), P,
+                               ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                               _lib.stream_handle())
+    else:
+        rc = lib.prrp_caluprrp_timed(ctypes.c_void_p(buf.data_ptr()), buf.stride(0), n, n, b, float(tau), P,
+                                     ctypes.c_void_p(perm.data_ptr()), sw, chg, ctypes.byref(st), ctypes.byref(err),
+                                     ctypes.byref(timing), _lib.stream_handle())
+    _lib.raise_for(rc, err, "prrp_caluprrp")
+    return st, list(sw)
+
+
+def timed(torch, fn):
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    rc = lib.prrp_luprrp_timed(ctypes.c_void_p(work.data_ptr()), lda, m, n, b, float(tau),
-                               ctypes.c_void_p(perm.data_ptr()), swaps, ctypes.byref(st), ctypes.byref(err),
-                               ctypes.byref(tm) if timed else None, _lib.stream_handle())
+    out = fn()
     e1.record()
     e1.synchronize()
-    _lib.raise_for(rc, err, "prrp_luprrp_timed")
-    return e0.elapsed_time(e1), tm, st
+    return e0.elapsed_time(e1), out
+
+
+def roofline_from_timing(tms, pk, what):
+    """Roofline of the dominant kernel (the DMMA Schur update) from per-launch
+    event spans: algorithmic flops 2 M N K summed over the launches / summed
+    launch time."""
+    from paper_1208_2451_b200 import _lib
+    si = _lib.KCLASSES.index("schur")
+    schur_ms = statistics.mean(t.ms[si] for t in tms)
+    launches = statistics.mean(t.launches[si] for t in tms)
+    flops = tms[0].schur_flops
+    achieved = flops / (schur_ms * 1e-3) / 1e12
+    breakdown = {k: round(statistics.mean(t.ms[i] for t in tms), 3) for i, k in enumerate(_lib.KCLASSES)}
+    return {"bound": "tensor", "kernel": "schur_wsc_kernel / schur_dmma_kernel (DMMA.8x8x4, TMA-fed)",
+            "achieved": achieved, "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk if pk else None,
+            "peak_source": "measured live: register-resident mma.sync.m8n8k4.f64 on all SMs, 1.5 s "
+                           "(prrp_b200_dmma_peak; MEASURED_PEAKS.json has no FP64 entry)",
+            "achieved_def": f"{what}: sum over launches of 2*M*N*K / summed Schur launch time (CUDA events on "
+                            "each launch's stream, direct enqueue)",
+            "schur_flops_per_step": flops, "schur_ms_per_step": schur_ms, "schur_launches_per_step": launches,
+            "step_breakdown_ms (summed spans, streams overlap)": breakdown}
+
+
+def attach_traffic(roof, name):
+    prof = os.path.join(ROOT, "profiles", name)
+    if os.path.exists(prof):
+        try:
+            ps = json.load(open(prof))
+            roof["traffic"] = ps.get("dram_bytes_per_launch")
+            roof["traffic_note"] = ps.get("note")
+        except Exception:
+            roof["traffic"] = None
+    else:
+        roof["traffic"] = None
+    return roof
 
 
 def run_device(args):
@@ -194,16 +270,10 @@ def run_device(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1208_2451_b200 import _lib, matgen
+    from paper_1208_2451_b200 import dist as pd
     import paper_1208_2451_b200 as prrp
     lib = _lib.device_lib()
-
-    n, b, tau = args.n, args.b, args.tau
-    a_host = matgen.gen_randn(n, args.seed, order="C")          # row-major == device layout
-    m = n
-    lda = n + (n & 1)
-    pristine = torch.empty((m, lda), dtype=torch.float64, device="cuda")
-    pristine[:, :n].copy_(torch.from_numpy(a_host))
-    work = torch.empty_like(pristine)
+    n, b, tau, P = args.n, args.b, args.tau, args.P
 
     def barrier():
         if ws > 1:
@@ -216,183 +286,210 @@ def run_device(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    pk = ctypes.c_double(0.0)
+    lib.prrp_b200_dmma_peak(1500.0, ctypes.byref(pk), ctypes.byref(_lib.PrrpErr()))
+    peak = pk.value
+
+    # ---- inputs resident in HBM
+    if ws == 1:
+        cols = np.arange(n)
+        a_loc = matgen.gen_urand(n, args.seed, order="C")
+    else:
+        cols = pd.local_columns(n, b, ws, rank)
+        a_loc = matgen.gen_urand_colset(n, args.seed, cols)
+    nl = len(cols)
+    lda = max(2, nl + (nl & 1))
+    pristine = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
+    pristine[:, :nl].copy_(torch.from_numpy(a_loc))
+    work = torch.empty_like(pristine)
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    tree = prrp.binary_tree(P)
+
+    def step():
+        if ws == 1:
+            return calu_call(lib, _lib, work, n, b, tau, P, perm)[0]
+        return pd.caluprrp_factor_dist_device(work, n, n, b, tau, tree).stats
+
     for _ in range(args.warmup):
-        device_run(lib, _lib, torch, pristine, work, m, n, lda, b, tau)
+        work.copy_(pristine)
+        barrier()
+        timed(torch, step)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    times, tms = [], []
+    times = []
     for _ in range(args.steps):
+        work.copy_(pristine)
         barrier()
-        # the timed steps run the plain entry point (no per-kernel timing spans)
-        ms, _, st = device_run(lib, _lib, torch, pristine, work, m, n, lda, b, tau, timed=False)
+        ms, st = timed(torch, step)
         times.append(max_over_ranks(ms))
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    # per-class breakdown and launch counts from separate instrumented runs
-    for _ in range(2):
-        _, tm, _ = device_run(lib, _lib, torch, pristine, work, m, n, lda, b, tau, timed=True)
-        tms.append(tm)
-    launches = args.steps * sum(tms[-1].launches)
     ms_step = statistics.mean(times)
-    value = ws * lu_flops(n) / (ms_step * 1e-3) / 1e9
-    if os.environ.get("PRRP_BENCH_STEPS"):
-        print("step ms:", [round(t, 2) for t in times], file=sys.stderr, flush=True)
+    value = lu_flops(n) / (ms_step * 1e-3) / 1e9
+    growth = (st.intermediate_max / st.original_max) if ws == 1 else st.growth_factor
+    launches = None
+    if ws == 1:
+        launches = int(lib.prrp_b200_graph_kernels()) * args.steps
 
-    # roofline of the dominant kernel (Schur update on the FP64 tensor pipe)
-    schur_ms = sum(t.ms[_lib.KCLASSES.index("schur")] for t in tms) / len(tms)
-    schur_launch = sum(t.launches[_lib.KCLASSES.index("schur")] for t in tms) / len(tms)
-    schur_flops = tms[0].schur_flops
-    import ctypes
-    pk = ctypes.c_double(0.0)
-    err = _lib.PrrpErr()
-    lib.prrp_b200_dmma_peak(1500.0, ctypes.byref(pk), ctypes.byref(err))
-    achieved = schur_flops / (schur_ms * 1e-3) / 1e12
-    traffic, traffic_note = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_schur_r01.json")
-    if os.path.exists(prof):
-        try:
-            ps = json.load(open(prof))
-            traffic = ps.get("dram_bytes_per_launch")
-            traffic_note = (f"dram read+write of {ps.get('reference_launch')} from {ps.get('report')}; "
-                            f"algorithmic bytes of that launch {ps.get('algorithmic_bytes_reference_launch')}")
-        except Exception:
-            traffic = None
-    breakdown = {k: round(sum(t.ms[i] for t in tms) / len(tms), 4) for i, k in enumerate(_lib.KCLASSES)}
-    roofline = {"bound": "tensor", "kernel": "schur_dmma_kernel (DMMA.8x8x4, TMA-fed)", "achieved": achieved,
-                "peak": pk.value, "unit": "TFLOP/s", "frac": achieved / pk.value if pk.value else None,
-                "traffic": traffic, "traffic_note": traffic_note,
-                "peak_source": "measured live: register-resident mma.sync.m8n8k4.f64 loop on all SMs, 1.5 s "
-                               "(MEASURED_PEAKS.json has no FP64 entry)",
-                "achieved_def": "sum over panels of 2*M*N*b / summed schur_dmma_kernel event time per step",
-                "launches_per_step": schur_launch, "schur_ms_per_step": schur_ms,
-                "step_breakdown_ms": breakdown}
-
-    extra = {}
-    # secondary panel width (b=128) on the same matrix
-    if args.secondary_b and args.secondary_b != b:
+    extra = {"step_ms": [round(t, 2) for t in times], "growth_factor": growth}
+    roofline = None
+    if ws == 1:
+        # per-class spans of the same factorization (direct enqueue, every launch timed)
+        tms = []
         for _ in range(2):
-            device_run(lib, _lib, torch, pristine, work, m, n, lda, args.secondary_b, tau)
-        t2 = []
-        for _ in range(max(2, args.steps // 2)):
-            barrier()
-            ms, _, _ = device_run(lib, _lib, torch, pristine, work, m, n, lda, args.secondary_b, tau, timed=False)
-            t2.append(max_over_ranks(ms))
-        ms2 = statistics.mean(t2)
-        extra["secondary"] = {"b": args.secondary_b, "ms_per_step": ms2,
-                              "value": ws * lu_flops(n) / (ms2 * 1e-3) / 1e9, "unit": UNIT}
+            work.copy_(pristine)
+            tm = _lib.PrrpTiming()
+            calu_call(lib, _lib, work, n, b, tau, P, perm, timing=tm)
+            tms.append(tm)
+        roofline = attach_traffic(roofline_from_timing(tms, peak, "config 5 CALU_PRRP"), "ncu_schur_c5_r02.json")
+        extra["timed_run_launches_per_step"] = int(sum(tms[-1].launches))
+    del pristine, work
+    torch.cuda.empty_cache()
 
-    def calu_line(cn, cb, gen, label, reps=2, gepp=False):
-        """CALU_PRRP (binary tree, P = 8) on a device-resident matrix; the first two
-        calls capture and upload the factorization's CUDA graph (untimed)."""
-        import ctypes
-        ca = (matgen.gen_urand if gen == "urand" else matgen.gen_randn)(cn, args.seed, order="C")
-        cld = cn + (cn & 1)
-        cprist = torch.empty((cn, cld), dtype=torch.float64, device="cuda")
-        cprist[:, :cn].copy_(torch.from_numpy(ca))
-        del ca
-        cwork = torch.empty_like(cprist)
-        cperm = torch.empty(cn, dtype=torch.int64, device="cuda")
-        npc = (cn + cb - 1) // cb
-        ct = []
-        for i in range(2 + reps):
-            cwork.copy_(cprist)
-            sw = (ctypes.c_int32 * npc)()
-            chg = (ctypes.c_int64 * npc)()
-            cst, cerr = _lib.PrrpStats(), _lib.PrrpErr()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            if gepp:   # calu_factor: the GEPP-tournament baseline (one stream, no graph)
-                rc = lib.prrp_calu(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, 8,
-                                   ctypes.c_void_p(cperm.data_ptr()), chg, ctypes.byref(cst), ctypes.byref(cerr),
-                                   _lib.stream_handle())
-            else:
-                rc = lib.prrp_caluprrp(ctypes.c_void_p(cwork.data_ptr()), cld, cn, cn, cb, float(tau), 8,
-                                       ctypes.c_void_p(cperm.data_ptr()), sw, chg, ctypes.byref(cst),
-                                       ctypes.byref(cerr), _lib.stream_handle())
-            e1.record()
-            e1.synchronize()
-            _lib.raise_for(rc, cerr, "prrp_caluprrp")
-            if i >= 2:
-                ct.append(e0.elapsed_time(e1))
-        cms = statistics.mean(ct)
-        del cprist, cwork, cperm
-        torch.cuda.empty_cache()
-        v = lu_flops(cn) / (cms * 1e-3) / 1e9
-        if gepp:
-            return {"workload": f"calu_factor (GEPP tournament) {label}({cn}, seed {args.seed}), b={cb}, binary "
-                                "tree P=8, 1 GPU", "ms_per_step": cms, "value": v, "unit": UNIT,
-                    "growth_factor": cst.intermediate_max / cst.original_max,
-                    "timing": f"CUDA events around prrp_calu, mean of {reps} steps after 2 untimed"}
-        return {"workload": f"CALU_PRRP {label}({cn}, seed {args.seed}), b={cb}, tau={tau}, binary tree P=8, 1 GPU",
-                "ms_per_step": cms, "value": v, "unit": UNIT,
-                "fp64_peak_fraction": (v / 1e3) / pk.value if pk.value else None,
-                "swaps": int(sum(sw)), "growth_factor": cst.intermediate_max / cst.original_max,
-                "timing": f"CUDA events around prrp_caluprrp, mean of {reps} steps after 2 untimed "
-                          "(graph capture + upload)"}
-
-    # BASELINE config 4: CALU_PRRP, randn(16384, seed 42), b = 64, binary tournament tree over P = 8
-    if args.calu_n and rank == 0:
-        extra["calu_config4"] = calu_line(args.calu_n, 64, "randn", "randn")
-    # BASELINE config 5 on one GPU: CALU_PRRP, U(-1,1) n = 32768 (8 GiB), b = 128, P = 8
-    if args.calu5_n and rank == 0:
-        extra["calu_config5"] = calu_line(args.calu5_n, 128, "urand", "urand")
-    # the reference's tournament-pivoted GEPP baseline (tournament.py:299-359), SURVEY 8(f)
-    if args.gcalu_n and rank == 0:
-        extra["calu_factor"] = calu_line(args.gcalu_n, 64, "randn", "randn", gepp=True)
-
-    # end to end through the public API: host input in pinned memory -> device -> factors on host
+    # ---- end to end through the public API (host buffers, H2D + D2H in the timed region)
     e2e = None
     if args.e2e_steps > 0:
-        pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        pinned.copy_(torch.from_numpy(a_host))
-        a_pin = pinned.numpy()
-        prrp.luprrp_factor(a_pin, b, tau)
-        et = []
-        for _ in range(args.e2e_steps):
-            barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            f = prrp.luprrp_factor(a_pin, b, tau)
-            et.append(max_over_ranks(time.perf_counter() - t0))
-        e_s = statistics.mean(et)
-        e2e = {"value": ws * lu_flops(n) / e_s / 1e9, "unit": UNIT, "seconds_per_step": e_s,
-               "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": 2 * n * n * 8 + m * 8,
-               "timing": "wall clock around prrp.luprrp_factor(numpy in pinned memory) -> BlockLUFactors "
-                         "(H2D, device factorization, device split of L/U, D2H of l, u, perm)"}
-        extra["growth_factor"] = f.stats.growth_factor
+        if ws == 1:
+            pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+            pinned.copy_(torch.from_numpy(a_loc))
+            a_pin = pinned.numpy()
+            et = []
+            for _ in range(args.e2e_steps):
+                t0 = time.perf_counter()
+                f = prrp.caluprrp_factor(a_pin, b, tau, tree)
+                et.append(time.perf_counter() - t0)
+            del f
+            e_s = statistics.mean(et)
+            e2e = {"value": lu_flops(n) / e_s / 1e9, "unit": UNIT, "seconds_per_step": e_s,
+                   "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": 2 * n * n * 8 + n * 8,
+                   "timing": "wall clock around prrp.caluprrp_factor(numpy array in pinned memory) -> "
+                             "BlockLUFactors (H2D, device factorization, device split, D2H of l, u, perm)"}
+            del pinned, a_pin
+        else:
+            pinned = torch.empty((n, nl), dtype=torch.float64, pin_memory=True)
+            pinned.copy_(torch.from_numpy(a_loc))
+            out = torch.empty((n, nl), dtype=torch.float64, pin_memory=True)
+            pout = torch.empty(n, dtype=torch.int64, pin_memory=True)
+            et = []
+            for _ in range(args.e2e_steps):
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                A = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
+                A[:, :nl].copy_(pinned, non_blocking=True)
+                f = pd.caluprrp_factor_dist_device(A, n, n, b, tau, tree)
+                out.copy_(f.lu[:, :nl], non_blocking=True)
+                pout.copy_(f.perm, non_blocking=True)
+                torch.cuda.synchronize()
+                et.append(max_over_ranks(time.perf_counter() - t0))
+                del A, f
+            e_s = statistics.mean(et)
+            e2e = {"value": lu_flops(n) / e_s / 1e9, "unit": UNIT, "seconds_per_step": e_s,
+                   "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8 + ws * n * 8,
+                   "timing": "wall clock (max over ranks): every rank's columns H2D from pinned memory, "
+                             "caluprrp_factor_dist_device, the packed local L\\U and perm D2H"}
 
+    # ---- bounded CPU sample (rank 0, N = 1)
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-            from oracle import prrp_oracle as orc
-            panels = max(1, args.cpu_panels)
-            a_f = np.asfortranarray(a_host)
-            t0 = time.perf_counter()
-            orc.lu_prrp(a_f, b, tau, panel_limit=panels)
-            dt = time.perf_counter() - t0
-            flops = sum(panel_share_flops(n, k * b, b) for k in range(panels))
-            cpu = {"value": flops / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"oracle.lu_prrp (numpy/OpenBLAS restatement of the reference), first {panels} "
-                             f"of {n // b} panels of n={n}, b={b} ({dt:.1f} s); GFLOP/s over their share of 2n^3/3"}
+            dt, flops, desc = cpu_sample(args, np.asfortranarray(a_loc[:, :(max(1, args.cpu_panels) + 1) * b]))
+            cpu = dict({"value": flops / dt / 1e9, "unit": UNIT, "kind": "port", "sample": desc}, **cpu_descr())
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    del a_loc
+
+    # ---- secondary workloads (N = 1)
+    if ws == 1 and not args.no_secondary:
+        extra["lu_prrp_config2"] = lu_prrp_lines(lib, _lib, torch, matgen, peak, args)
+        extra["calu_prrp_config4"] = calu_secondary(lib, _lib, torch, matgen, 16384, 64, "randn", args, peak)
+        extra["calu_factor_gepp_n8192"] = calu_secondary(lib, _lib, torch, matgen, 8192, 64, "randn", args, peak,
+                                                         gepp=True)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference matgen recipe: PCG64 seed 42, "
-                                                           "Box-Muller normals, row-major fill)",
-                "config": config_dict(args, extra), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk,
-                "fp64_peak_fraction": (value / ws / 1e3) / pk.value if pk.value else None}
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (U(-1,1) with the reference's matgen conventions: PCG64 seed 42, row-major fill)",
+                "config": dict(workload(args, ws), **extra), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "fp64_peak_fraction": (value / ws / 1e3) / peak if peak else None, "fp64_peak_tflops": peak}
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def lu_prrp_lines(lib, _lib, torch, matgen, peak, args):
+    """LU_PRRP on BASELINE config 2 (randn(8192, seed 42), tau = 2), b = 64 and 128."""
+    n = 8192
+    a = matgen.gen_randn(n, args.seed, order="C")
+    pristine = torch.from_numpy(a).cuda()
+    work = torch.empty_like(pristine)
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    out = {}
+    for b in (64, 128):
+        def run(tm=None):
+            work.copy_(pristine)
+            sw = (ctypes.c_int32 * ((n + b - 1) // b))()
+            st, err = _lib.PrrpStats(), _lib.PrrpErr()
+            fn = lambda: lib.prrp_luprrp_timed(ctypes.c_void_p(work.data_ptr()), n, n, n, b, float(args.tau),
+                                               ctypes.c_void_p(perm.data_ptr()), sw, ctypes.byref(st),
+                                               ctypes.byref(err), ctypes.byref(tm) if tm is not None else None,
+                                               _lib.stream_handle())
+            ms, rc = timed(torch, fn)
+            _lib.raise_for(rc, err, "prrp_luprrp")
+            return ms, st
+        for _ in range(3):
+            run()
+        ts = [run()[0] for _ in range(args.steps)]
+        tms = []
+        for _ in range(2):
+            tm = _lib.PrrpTiming()
+            run(tm)
+            tms.append(tm)
+        ms = statistics.mean(ts)
+        v = lu_flops(n) / (ms * 1e-3) / 1e9
+        out[f"b{b}"] = {"workload": f"LU_PRRP BASELINE config 2: randn(8192, seed {args.seed}), b={b}, tau=2",
+                        "ms_per_step": ms, "value": v, "unit": UNIT, "fp64_peak_fraction": v / 1e3 / peak,
+                        "step_ms": [round(t, 2) for t in ts],
+                        "roofline": attach_traffic(roofline_from_timing(tms, peak, f"config 2 LU_PRRP b={b}"),
+                                                   f"ncu_schur_c2b{b}_r02.json")}
+    del pristine, work
+    torch.cuda.empty_cache()
+    return out
+
+
+def calu_secondary(lib, _lib, torch, matgen, n, b, gen, args, peak, gepp=False):
+    a = (matgen.gen_urand if gen == "urand" else matgen.gen_randn)(n, args.seed, order="C")
+    pristine = torch.from_numpy(a).cuda()
+    del a
+    work = torch.empty_like(pristine)
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")
+    ts = []
+    for i in range(2 + max(2, args.steps // 2)):
+        work.copy_(pristine)
+        if gepp:
+            chg = (ctypes.c_int64 * ((n + b - 1) // b))()
+            st, err = _lib.PrrpStats(), _lib.PrrpErr()
+            ms, rc = timed(torch, lambda: lib.prrp_calu(ctypes.c_void_p(work.data_ptr()), n, n, n, b, 8,
+                                                        ctypes.c_void_p(perm.data_ptr()), chg, ctypes.byref(st),
+                                                        ctypes.byref(err), _lib.stream_handle()))
+            _lib.raise_for(rc, err, "prrp_calu")
+        else:
+            ms, (st, _) = timed(torch, lambda: calu_call(lib, _lib, work, n, b, args.tau, 8, perm))
+        if i >= 2:
+            ts.append(ms)
+    del pristine, work
+    torch.cuda.empty_cache()
+    ms = statistics.mean(ts)
+    v = lu_flops(n) / (ms * 1e-3) / 1e9
+    name = "calu_factor (GEPP tournament)" if gepp else "CALU_PRRP BASELINE config 4"
+    return {"workload": f"{name}: {gen}({n}, seed {args.seed}), b={b}, binary tree P=8, 1 GPU",
+            "ms_per_step": ms, "value": v, "unit": UNIT, "fp64_peak_fraction": v / 1e3 / peak,
+            "growth_factor": st.intermediate_max / st.original_max}
 
 
 def main():

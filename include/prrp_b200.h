@@ -133,6 +133,17 @@ int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, doubl
                   int32_t leaf_count, int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3,
                   prrp_stats* stats, prrp_err* err, void* stream);
 
+/* Kernel launches in the CUDA graph the calling thread's last prrp_caluprrp
+ * replayed (diagnostics / the bench's launch count; 0 before any call). */
+int64_t prrp_b200_graph_kernels(void);
+
+/* prrp_caluprrp through the direct (uncaptured) enqueue with every launch
+ * timed by CUDA events on its stream (per kernel class, as
+ * prrp_luprrp_timed); timing may be NULL. */
+int prrp_caluprrp_timed(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau,
+                        int32_t leaf_count, int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3,
+                        prrp_stats* stats, prrp_err* err, prrp_timing* timing, void* stream);
+
 /* Tournament-pivoted GEPP ("calu_factor") with a binary tree of
  * `leaf_count` leaves, 0 = flat tree — replaces prrp.calu_factor(a, b, tree)
  * (tournament.py:299-359): every tournament node selects by partial

@@ -1851,6 +1851,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
 // large factorization costs more than the GPU work at n = 16384).
 struct CaluPlan {
   double* A; int64_t lda, m, n; int b; double tau; int P; int64_t* perm; int dev;
+  int64_t kernel_nodes = 0;   // kernel launches in the captured graph (the bench's gpu_launches)
   cudaGraphExec_t exec = nullptr;
   std::vector<void*> bufs;
   CaluOut out;
@@ -1860,6 +1861,7 @@ struct CaluPlan {
     for (void* p : bufs) cudaFree(p);
   }
 };
+thread_local int64_t tl_last_graph_kernels = 0;
 std::vector<std::shared_ptr<CaluPlan>>& calu_plans() {
   static std::vector<std::shared_ptr<CaluPlan>> v;
   return v;
@@ -1894,7 +1896,8 @@ void racecheck_end() {}
 #endif
 
 int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
-                  int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s) {
+                  int32_t* swap_counts, int64_t* tchg3, prrp_stats* stats, prrp_err* err, cudaStream_t s,
+                  prrp_timing* timing = nullptr) {
   if (m < n) fail(PRRP_ERR_DIM, "need at least as many rows as columns");
   if (b < 1 || b > n) fail(PRRP_ERR_ARG, "panel width out of range");
   if (!(tau > 1.0)) fail(PRRP_ERR_ARG, "tau must exceed 1");
@@ -1905,14 +1908,22 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
   racecheck_begin(A, lda);
   const auto host_t0 = std::chrono::steady_clock::now();
   // PRRP_TRACE: record the timing spans (and write the trace file) for CALU too
-  if (getenv("PRRP_TRACE") || (getenv("PRRP_GRAPH") && atoi(getenv("PRRP_GRAPH")) == 0)) {
+  if (timing || getenv("PRRP_TRACE") || (getenv("PRRP_GRAPH") && atoi(getenv("PRRP_GRAPH")) == 0)) {
+    // direct enqueue; with `timing` (or PRRP_TRACE) every launch is bracketed
+    // by events on its stream and summed per kernel class
     Timer timer;
-    tl_timer = getenv("PRRP_TRACE") ? &timer : nullptr;
+    tl_timer = (timing || getenv("PRRP_TRACE")) ? &timer : nullptr;
+    tl_schur_flops = 0.0;
     struct Reset { ~Reset() { tl_timer = nullptr; } } reset_timer;
     Arena ar(s);
     CaluOut out;
     caluprrp_enqueue(A, lda, m, n, b, tau, P, perm, s, ar, out);
-    return caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, tl_timer);
+    const int rc = caluprrp_finish(out, s, swap_counts, tchg3, stats, err, host_t0, timing ? nullptr : tl_timer);
+    if (timing) {
+      timer.collect(timing);
+      timing->schur_flops = tl_schur_flops;
+    }
+    return rc;
   }
   int dev = 0;
   CU_TRY(cudaGetDevice(&dev));
@@ -1963,6 +1974,17 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     CU_TRY(cudaStreamEndCapture(cs, &g));
     if (const char* dot = getenv("PRRP_GRAPH_DOT"))   // diagnostics: the captured dependency graph
       cudaGraphDebugDotPrint(g, dot, cudaGraphDebugDotFlagsVerbose);
+    {
+      size_t nn = 0;
+      CU_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> gn(nn);
+      if (nn) CU_TRY(cudaGraphGetNodes(g, gn.data(), &nn));
+      for (auto nd : gn) {
+        cudaGraphNodeType ty;
+        CU_TRY(cudaGraphNodeGetType(nd, &ty));
+        np->kernel_nodes += ty == cudaGraphNodeTypeKernel;
+      }
+    }
     const cudaError_t ie = cudaGraphInstantiate(&np->exec, g, graph_instantiate_flags());
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) fail(PRRP_ERR_CUDA, "cudaGraphInstantiate failed");
@@ -1970,6 +1992,7 @@ int caluprrp_impl(double* A, int64_t lda, int64_t m, int64_t n, int b, double ta
     pl = plans.back().get();
   }
   pl->used = ++g_plan_clock;
+  tl_last_graph_kernels = pl->kernel_nodes;
   // the read-back runs outside the cache lock and reads the plan's buffers:
   // hold a reference so the plan cannot be evicted (freed) before it is done
   std::shared_ptr<CaluPlan> hold;
@@ -2358,6 +2381,21 @@ int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, doubl
   try {
     return caluprrp_impl(A, lda, m, n, b, tau, leaf_count, perm, swap_counts, tournament_charge3, stats, err,
                          (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int64_t prrp_b200_graph_kernels(void) { return tl_last_graph_kernels; }
+
+int prrp_caluprrp_timed(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau, int32_t leaf_count,
+                        int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3, prrp_stats* stats,
+                        prrp_err* err, prrp_timing* timing, void* stream) {
+  clear_err(err);
+  if (timing) memset(timing, 0, sizeof(*timing));
+  try {
+    return caluprrp_impl(A, lda, m, n, b, tau, leaf_count, perm, swap_counts, tournament_charge3, stats, err,
+                         (cudaStream_t)stream, timing);
   } catch (const Fail& f) {
     return report(err, f);
   }

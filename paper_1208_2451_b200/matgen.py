@@ -119,3 +119,17 @@ def gen_deficient_block(n, seed, blocks, cols):
         for i in range(r1 - r0):
             a[r0 + i, :cols] = base[i % rank] * (2.0 ** (i // rank))
     return np.asfortranarray(a)
+
+
+def gen_urand_colset(n, seed, cols, chunk_rows=1024):
+    """gen_urand(n, seed)[:, cols] (row-major m x len(cols)), streamed in row
+    chunks: the rank-local columns of config 5 without forming the n x n
+    matrix on any one host process."""
+    cols = np.asarray(cols, dtype=np.int64)
+    rng = _rng(seed)
+    out = np.empty((n, len(cols)))
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        blk = rng.random((r1 - r0) * n).reshape(r1 - r0, n)
+        out[r0:r1, :] = 2.0 * blk[:, cols] - 1.0
+    return out
