@@ -21,7 +21,8 @@
 // unused tail is dead (-1: a zero row, never selected); live_out = members.
 __global__ void calu_merge_inputs_kernel(const int32_t* cands, const int32_t* ccnt, int b, int nchild,
                                          int32_t* lpos_in, int64_t* rowidx, int32_t* live_out,
-                                         const int64_t* pos2row, int64_t col0, int stride) {
+                                         const int64_t* pos2row, int64_t col0, int stride, const DevState* st) {
+  if (prrp_failed(st)) return;     // the children may not have run: their outputs are not indices
   const int node = blockIdx.x;
   const int cl = ccnt[2 * node];
   const int cr = 2 * node + 1 < nchild ? ccnt[2 * node + 1] : 0;
@@ -41,7 +42,8 @@ __global__ void calu_merge_inputs_kernel(const int32_t* cands, const int32_t* cc
 // Leaves (lpos_in == nullptr): lpos(node, j) = leaf_lo[node] + j.
 __global__ void calu_select_kernel(const int32_t* const* perms, const int32_t* lpos_in, const int64_t* leaf_lo,
                                    int b, const int32_t* wants, const int32_t* lives, int merge, int32_t* cands_out,
-                                   int32_t* cnt_out, int stride) {
+                                   int32_t* cnt_out, int stride, const DevState* st) {
+  if (prrp_failed(st)) return;
   const int node = blockIdx.x;
   const int32_t* perm = perms[node];
   const int cnt = min(wants[node], b);
@@ -252,7 +254,8 @@ __global__ void calu_copy_r11_kernel(const double* Rsmall, int b, double* Rbuf, 
 
 // L21 (logical order, column-major ldl) -> physical slot order (column-major ldl2)
 __global__ void calu_scatter_l21_kernel(const double* Lsrc, int64_t ldl, const int32_t* log2phys, int64_t M, int b,
-                                        int64_t bslot, double* Ldst, int64_t ldd) {
+                                        int64_t bslot, double* Ldst, int64_t ldd, const DevState* st) {
+  if (prrp_failed(st)) return;     // the reorder that writes log2phys may have been skipped
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * b; e += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(e / M);
     const int64_t t = e % M;
@@ -299,7 +302,8 @@ __global__ void calu_leaf_lo_kernel(int64_t* leaf_lo, int64_t p_eff, int64_t bas
 // for t < ncol, k < b (32 rows per block through a padded shared tile)
 __global__ void __launch_bounds__(256) calu_gather_t_kernel(const double* A, int64_t lda, int64_t col0, int b,
                                                            int64_t ncol, const int64_t* rowof, double* out,
-                                                           int64_t ldo) {
+                                                           int64_t ldo, const DevState* st) {
+  if (prrp_failed(st)) return;
   extern __shared__ double tile[];   // b x 33
   const int64_t t0 = (int64_t)blockIdx.x * 32;
   const int nt = (int)min((int64_t)32, ncol - t0);
@@ -360,7 +364,8 @@ __global__ void __launch_bounds__(256) calu_form_negqt_kernel(const double* refl
 // rank-deficient node), block rows lo .. lo+len), dead rows after them
 __global__ void calu_flat_inputs_kernel(const int32_t* cands, const int32_t* ccnt, int b, int64_t lo, int len,
                                         int32_t* lpos_in, int64_t* rowidx, int32_t* live_out,
-                                        const int64_t* pos2row, int64_t col0) {
+                                        const int64_t* pos2row, int64_t col0, const DevState* st) {
+  if (prrp_failed(st)) return;
   const int c = ccnt[0];
   for (int t = threadIdx.x; t < b + len; t += blockDim.x) {
     int32_t lp = -1;

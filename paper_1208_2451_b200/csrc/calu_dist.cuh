@@ -330,15 +330,15 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       int32_t* nxt = w.cands + (size_t)b;
       int32_t* cnxt = w.ccnt + 1;
       calu_select_kernel<<<1, 128, 0, s>>>(w.perms_dev, nullptr, w.leaf_lo_dev, bj, w.want_all, w.live_all, 0, cur,
-                                           ccur, 2 * b);
+                                           ccur, 2 * b, w.st);
       int level = 1;
       for (int64_t lo = first; lo < rows; lo += bj, ++level) {
         const int64_t len = std::min<int64_t>(bj, rows - lo);
         calu_flat_inputs_kernel<<<1, 128, 0, s>>>(cur, ccur, bj, lo, (int)len, w.lpos_all, w.rowidx_all,
-                                                  w.live_all, w.pos2row, col0);
+                                                  w.live_all, w.pos2row, col0, w.st);
         run_level({0}, {bj + len}, false, level, slot++);
         calu_select_kernel<<<1, 128, 0, s>>>(w.perms_dev, w.lpos_all, nullptr, bj, w.want_all, w.live_all, 1, nxt,
-                                             cnxt, 2 * b);
+                                             cnxt, 2 * b, w.st);
         std::swap(cur, nxt);
         std::swap(ccur, cnxt);
       }
@@ -366,17 +366,17 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       int32_t* nxt = w.cands + (size_t)maxnodes * b;
       int32_t* cnxt = w.ccnt + maxnodes;
       calu_select_kernel<<<(unsigned)pe, 128, 0, s>>>(w.perms_dev, nullptr, w.leaf_lo_dev, bj, w.want_all,
-                                                      w.live_all, 0, cur, ccur, 2 * b);
+                                                      w.live_all, 0, cur, ccur, 2 * b, w.st);
       int64_t ncur = pe;
       int level = 1;
       while (ncur > 1) {
         const int64_t nm = ncur / 2;
         calu_merge_inputs_kernel<<<(unsigned)nm, 128, 0, s>>>(cur, ccur, bj, (int)(2 * nm), w.lpos_all,
-                                                              w.rowidx_all, w.live_all, w.pos2row, col0, 2 * b);
+                                                              w.rowidx_all, w.live_all, w.pos2row, col0, 2 * b, w.st);
         run_level(std::vector<int64_t>(nm, 0), std::vector<int64_t>(nm, 2 * bj), false, level, slot);
         slot += (int)nm;
         calu_select_kernel<<<(unsigned)nm, 128, 0, s>>>(w.perms_dev, w.lpos_all, nullptr, bj, w.want_all,
-                                                        w.live_all, 1, nxt, cnxt, 2 * b);
+                                                        w.live_all, 1, nxt, cnxt, 2 * b, w.st);
         if (ncur % 2) {
           CU_TRY(cudaMemcpyAsync(nxt + nm * bj, cur + (ncur - 1) * bj, sizeof(int32_t) * bj,
                                  cudaMemcpyDeviceToDevice, s));
@@ -425,7 +425,11 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       qa.st = st;
       qa.panel_id = k;
       iota32_kernel<<<1, 128, 0, s>>>(w.perm_small, bj);
-      if (bj == P1_H && ((uintptr_t)blk % 16 == 0) && (w.lda % 2 == 0) && !force_generic_panel()) {
+      if (team_eligible(bj, bj) && !force_generic_panel()) {
+        PanelArgs at = qa;
+        at.fro = w.nodes[0].B.fro;
+        launch_team(at, s);
+      } else if (bj == P1_H && ((uintptr_t)blk % 16 == 0) && (w.lda % 2 == 0) && !force_generic_panel()) {
         PanelCfg g1 = gq;
         g1.C = 1;
         g1.T = P1_T;
@@ -451,7 +455,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       if (calu_r12_gemm && bj >= r12_min_b && (bj % 2 == 0)) {
         calu_form_negqt_kernel<<<1, 256, (size_t)bj * (bj + 1) * 8, s>>>(w.refl, bj, w.Qneg);
         calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, s>>>(
-            Ash, w.lda, col0, bj, ncol, w.pos2row + col0 + bj, w.A21t, w.ld21t);
+            Ash, w.lda, col0, bj, ncol, w.pos2row + col0 + bj, w.A21t, w.ld21t, w.st);
         zero2d_kernel<<<(unsigned)std::min<int64_t>(4 * sms, (ncol * bj + 255) / 256), 256, 0, s>>>(
             w.B.Rbuf + bj, rows, bj, ncol);
         schur_update(w.B.Rbuf + bj, rows, w.Qneg, bj, w.A21t, w.ld21t, bj, ncol, bj, w.st_r12, s, 0, 0);
@@ -491,7 +495,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       CU_TRY(cudaGetLastError());
     }
     // L21 (logical order) -> physical slots, into the message (leading dimension ldl_k)
-    calu_scatter_l21_kernel<<<sms * 4, 256, 0, s>>>(w.Lg, w.ldl, w.log2phys, rows - bj, bj, bj, Lp, ldk);
+    calu_scatter_l21_kernel<<<sms * 4, 256, 0, s>>>(w.Lg, w.ldl, w.log2phys, rows - bj, bj, bj, Lp, ldk, w.st);
   } else {
     // last square block: logical order, then GEPP (every rank repeats the reorder)
     calu_reorder_kernel<<<1, 1024, 0, s>>>(nullptr, nullptr, w.ident, 1, bj, rows, col0, w.pos2row, w.scratch,

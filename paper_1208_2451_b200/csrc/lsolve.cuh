@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(1024, 1) panel_finalize_kernel(FinalizeArgs f)
   __shared__ int s_cnt[33];
   cg::cluster_group cl = cg::this_cluster();
   const PanelArgs& a = f.pa;
-  if (prrp_failed(a.st)) return;
+  __shared__ int s_failed;
+  if (cluster_failed(a.st, &s_failed)) return;
   const int c = (int)cl.block_rank(), C = (int)cl.num_blocks();
   const int t = threadIdx.x;
 

@@ -81,6 +81,23 @@ struct PanelArgs {
 // "this node passes its members through" (tournament.py:128-129: idx.shape[0] <= b)
 __device__ __forceinline__ bool node_passes(const PanelArgs& a) { return a.live && *a.live <= a.bsel; }
 
+// The run-state error flag read consistently by every CTA of a cluster: a
+// concurrent kernel (another tournament node, the look-ahead streams) may
+// set it between the CTAs' own reads, and a CTA that returned early would
+// leave the others waiting at a cluster barrier.  CTA 0 reads, one cluster
+// barrier, everyone follows; a failed cluster passes a second barrier so
+// CTA 0's flag stays readable until all have read it.  `flag` is a shared
+// int of the calling kernel.  Returns true when the kernel must return.
+__device__ __forceinline__ bool cluster_failed(const DevState* st, int* flag) {
+  cg::cluster_group cl = cg::this_cluster();
+  if (cl.num_blocks() == 1) return prrp_failed(st);
+  if (threadIdx.x == 0) *flag = prrp_failed(st);
+  cl.sync();
+  const int f = *cl.map_shared_rank(flag, 0);
+  if (f) cl.sync();
+  return f != 0;
+}
+
 struct Rec {
   double key;
   long long pos;
@@ -359,6 +376,7 @@ __device__ void engine_run(const PanelArgs& a, int mode, const int32_t* perm_in,
 __global__ void __launch_bounds__(1024, 1) panel_qrcp_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double dyn_smem[];
   __shared__ PanelShared S;
-  if (prrp_failed(a.st) || node_passes(a)) return;
+  __shared__ int s_failed;
+  if (node_passes(a) || cluster_failed(a.st, &s_failed)) return;
   engine_run(a, a.mode, a.perm, dyn_smem, S);
 }

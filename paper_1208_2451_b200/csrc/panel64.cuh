@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(P64_T, 1) panel_qrcp64_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double sdata[];      // P64_E x P64_T smem columns
   __shared__ P64Shared S;
   cg::cluster_group cl = cg::this_cluster();
-  if (prrp_failed(a.st) || node_passes(a)) return;
+  __shared__ int s_failed;
+  if (node_passes(a) || cluster_failed(a.st, &s_failed)) return;
   const int C = (int)cl.num_blocks();
   const int c = (int)cl.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;

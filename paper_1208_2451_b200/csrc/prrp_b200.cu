@@ -28,6 +28,7 @@
 #include "panel64.cuh"
 #include "panel1.cuh"
 #include "panel2.cuh"
+#include "panel_team.cuh"
 #include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
@@ -112,7 +113,9 @@ DeviceCaps& caps() {
     CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
                            (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel,
-                           (const void*)panel_qrcp2_kernel}) {
+                           (const void*)panel_qrcp2_kernel, (const void*)panel_team_kernel<4>,
+                           (const void*)panel_team_kernel<8>, (const void*)panel_team_kernel<12>,
+                           (const void*)panel_team_kernel<16>}) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       set_max_dyn((const void*)fn);
     }
@@ -375,6 +378,39 @@ void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Arg
   launch_clusters(kernel, g, 1, dyn, s, args...);
 }
 
+// The team engine (panel_team.cuh) for p <= team_max_p() columns: one column
+// per 8 threads, ceil(p / cols) CTAs in one cluster.  Opt-in
+// (PRRP_TEAM_MAXP=<largest p>): measured slower than the thread-per-column
+// engines in the CALU schedule (config 5: 1548 vs 1406 ms; config 4: 392 vs
+// 290 ms) -- ~3.9 us per pivot step at h = 128, p = 256 (ncu), the same as
+// panel2: the per-step chain of barriers and the serial reflector, not the
+// column arithmetic, bounds both.
+int64_t team_max_p() {
+  static const int64_t v = getenv("PRRP_TEAM_MAXP") ? atoll(getenv("PRRP_TEAM_MAXP")) : 0;
+  return v;
+}
+
+int team_cols(int h) {
+  const int nr = (h + 7) / 8;
+  return (nr <= 4 ? PTCfg<4>::T : nr <= 8 ? PTCfg<8>::T : PTCfg<16>::T) / PT_G;
+}
+
+bool team_eligible(int h, int64_t p) {
+  return h >= 1 && h <= PRRP_MAXH && p >= 1 &&
+         p <= std::min<int64_t>(team_max_p(), (int64_t)team_cols(h) * caps().max_cluster);
+}
+
+void launch_team(const PanelArgs& a, cudaStream_t s) {
+  PanelCfg g{};
+  const int cols = team_cols(a.h);
+  g.C = (int)((a.p + cols - 1) / cols);
+  const int nr = (a.h + 7) / 8;
+  if (nr <= 4) { g.T = PTCfg<4>::T; launch_cluster(panel_team_kernel<4>, g, kPTSmem, s, a); }
+  else if (nr <= 8) { g.T = PTCfg<8>::T; launch_cluster(panel_team_kernel<8>, g, kPTSmem, s, a); }
+  else if (nr <= 12) { g.T = PTCfg<12>::T; launch_cluster(panel_team_kernel<12>, g, kPTSmem, s, a); }
+  else { g.T = PTCfg<16>::T; launch_cluster(panel_team_kernel<16>, g, kPTSmem, s, a); }
+}
+
 // GEPP of a b x b block (register kernel for b <= 64, shared-memory kernel above)
 void launch_gepp(const double* src, int64_t ld, const int32_t* rowmap, int b, double* D, int32_t* piv,
                  int32_t* gperm, DevState* st, int panel, cudaStream_t s) {
@@ -494,7 +530,9 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
   const int64_t c1 = std::max<int64_t>((p + P1_MAXCOLS - 1) / P1_MAXCOLS,
                                        std::min<int64_t>(maxc, std::max<int64_t>(1, (p + cpc - 1) / cpc)));
   const bool aligned = ((uintptr_t)src % 16 == 0) && (ld % 2 == 0);
-  if (h == P1_H && c1 <= maxc && aligned && !force_generic_panel()) {
+  if (team_eligible(h, p) && !force_generic_panel()) {
+    launch_team(a, s);
+  } else if (h == P1_H && c1 <= maxc && aligned && !force_generic_panel()) {
     // thread-per-column register engine (h = 64)
     PanelCfg g1 = g;
     g1.C = (int)c1;
@@ -1506,18 +1544,18 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         int32_t* ccur = ccnt;
         int32_t* cnxt = ccnt + 1;
         calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, want_all, live_all, 0, cur, ccur,
-                                              2 * b);
+                                              2 * b, st);
         int level = 1;
         for (int64_t lo = first; lo < rows; lo += bj, ++level) {
           const int64_t len = std::min<int64_t>(bj, rows - lo);
           calu_flat_inputs_kernel<<<1, 128, 0, sm>>>(cur, ccur, bj, lo, (int)len, lpos_all, rowidx_all, live_all,
-                                                     pos2row, col0);
+                                                     pos2row, col0, st);
           run_level(std::vector<int64_t>{0}, std::vector<int64_t>{bj + len}, false, col0, bj, panel, level, slot, sm);
           chg3 += qr_charge3(bj + len, bj);
           node_members[panel].push_back({bj + len, slot});
           ++slot;
           calu_select_kernel<<<1, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, want_all, live_all, 1, nxt, cnxt,
-                                                2 * b);
+                                                2 * b, st);
           std::swap(cur, nxt);
           std::swap(ccur, cnxt);
         }
@@ -1570,7 +1608,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         int32_t* ccur = ccnt;
         int32_t* cnxt = ccnt + maxnodes;
         calu_select_kernel<<<(unsigned)p_eff, 128, 0, sm>>>(perms_dev, nullptr, leaf_lo_dev, bj, want_all, live_all,
-                                                             0, cur, ccur, 2 * b);
+                                                             0, cur, ccur, 2 * b, st);
         int64_t ncur = p_eff;
         int level = 1;
         while (ncur > 1) {
@@ -1578,7 +1616,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           // node i of this level reads lpos_all/rowidx_all[i*2b .. i*2b + 2b) (stride 2b even when bj < b);
           // members = [left's candidates, right's candidates], dead (zero) rows after them
           calu_merge_inputs_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(cur, ccur, bj, (int)(2 * nmerge), lpos_all,
-                                                                      rowidx_all, live_all, pos2row, col0, 2 * b);
+                                                                      rowidx_all, live_all, pos2row, col0, 2 * b, st);
           CU_TRY(cudaGetLastError());
           std::vector<int64_t> mlo(nmerge, 0), mcnt(nmerge, 2 * bj);
           run_level(mlo, mcnt, false, col0, bj, panel, level, slot, sm);
@@ -1588,7 +1626,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           }
           slot += (int)nmerge;
           calu_select_kernel<<<(unsigned)nmerge, 128, 0, sm>>>(perms_dev, lpos_all, nullptr, bj, want_all, live_all,
-                                                                1, nxt, cnxt, 2 * b);
+                                                                1, nxt, cnxt, 2 * b, st);
           if (ncur % 2) {   // odd node promoted unmerged (tournament.py:197-198)
             CU_TRY(cudaMemcpyAsync(nxt + nmerge * bj, cur + (ncur - 1) * bj, sizeof(int32_t) * bj,
                                    cudaMemcpyDeviceToDevice, sm));
@@ -1636,7 +1674,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         qa.panel_id = panel;
         tbegin(PRRP_K_FINALIZE, sm);
         iota32_kernel<<<1, 128, 0, sm>>>(perm_small, bj);
-        if (bj == P1_H && ((uintptr_t)blk % 16 == 0) && (lda % 2 == 0) && !force_generic_panel()) {
+        if (team_eligible(bj, bj) && !force_generic_panel()) {
+          PanelArgs at = qa;
+          at.fro = nodes[0].B.fro;
+          launch_team(at, sm);
+        } else if (bj == P1_H && ((uintptr_t)blk % 16 == 0) && (lda % 2 == 0) && !force_generic_panel()) {
           // the register engine in fixed-order mode, one CTA (p = b columns)
           PanelCfg g1 = gq;
           g1.C = 1;
@@ -1672,7 +1714,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           tend(sm);
           tbegin(PRRP_K_PERMUTE, sm);
           calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, sm>>>(
-              A, lda, col0, bj, ncol, pos2row + col0 + bj, A21t, ld21t);
+              A, lda, col0, bj, ncol, pos2row + col0 + bj, A21t, ld21t, st);
           zero2d_kernel<<<(unsigned)std::min<int64_t>(4 * sms, (ncol * bj + 255) / 256), 256, 0, sm>>>(
               B.Rbuf + bj, rows, bj, ncol);
           tend(sm);
@@ -1719,7 +1761,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaGetLastError());
       }
       // L21 (logical order) -> physical slots for the Schur update and the compose
-      calu_scatter_l21_kernel<<<sms * 4, 256, 0, sm>>>(Lg, ldl, log2phys, rows - bj, bj, bj, Lp, ldl);
+      calu_scatter_l21_kernel<<<sms * 4, 256, 0, sm>>>(Lg, ldl, log2phys, rows - bj, bj, bj, Lp, ldl, st);
       // the updates read the pivot rows (A12 before the GEPP finish) from a
       // copy, so the block row can be finished on the fin stream while the
       // trailing update is still running

@@ -294,7 +294,7 @@ def test_dist_calu_device_ops_single_rank(dev):
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         a = orc.randn_matrix(256, 11)
-        f = pd.caluprrp_factor_dist(a, 16, 2.0, 4)
+        f = pd.caluprrp_factor_dist(a, 16, 2.0, dev.binary_tree(4))
     finally:
         dist.destroy_process_group()
     ref = orc.calu_prrp(a, 16, 2.0, "binary", 4)
