@@ -268,6 +268,20 @@ int prrp_calu_dist_finish(void* handle, const int64_t* reduced, int32_t* swap_co
                           int64_t* tournament_charge3, prrp_stats* stats, prrp_err* err, void* stream);
 void prrp_calu_dist_destroy(void* handle);
 
+/* ---- Stability measurements (metrics.py:65-145) on device buffers.
+ * r = rhs - A x with the reference's compensated accumulation
+ * (residual_extended, metrics.py:75-92: Veltkamp two-product + Knuth
+ * two-sum per term, j ascending): bit-identical to the reference.  A is
+ * row-major m x n; x (n), rhs and r (m) are device vectors. */
+int prrp_residual_extended(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
+                           const double* rhs, double* r, prrp_err* err, void* stream);
+/* Absolute sums: colabs[j] = sum_i |A_ij| (||A||_1 = max), rowabs[i] =
+ * sum_j |A_ij| (||A||_inf), absax[i] = sum_j |A_ij| |x_j| (the componentwise
+ * denominator |A| |x|, metrics.py:109); any output may be NULL.  Summation
+ * order: per column / per warp (the reference uses numpy / BLAS orders). */
+int prrp_abs_sums(const double* A, int64_t lda, int64_t m, int64_t n, const double* x, double* colabs,
+                  double* rowabs, double* absax, prrp_err* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

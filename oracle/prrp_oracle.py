@@ -785,3 +785,35 @@ def panel_share_flops(n, col0, bj):
     s = n - col0 (telescopes to 2n^3/3 over all panels)."""
     s = n - col0
     return 2.0 * (s ** 3 - (s - bj) ** 3) / 3.0
+
+
+# ---------------------------------------------------------------- stability measurements (checker only)
+def _two_sum(a, b):                       # metrics.py:66-69
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _two_prod(a, b):                      # metrics.py:72-81 (Veltkamp split 2^27 + 1)
+    split = 134217729.0
+    p = a * b
+    ca = split * a
+    ah = ca - (ca - a)
+    al = a - ah
+    cb = split * b
+    bh = cb - (cb - b)
+    bl = b - bh
+    return p, ((ah * bh - p) + ah * bl + al * bh) + al * bl
+
+
+def residual_extended(a, x, rhs):
+    """rhs - A x, compensated (metrics.py:84-92)."""
+    a = fmat(a)
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
+    s = np.asarray(rhs, dtype=np.float64).reshape(-1).copy()
+    comp = np.zeros_like(s)
+    for j in range(a.shape[1]):
+        p, pe = _two_prod(a[:, j], -x[j])
+        s, se = _two_sum(s, p)
+        comp += pe + se
+    return s + comp

@@ -77,6 +77,8 @@ SIGNATURES = {
     "prrp_calu_dist_stats": ([_P, _P, _P], ctypes.c_int),
     "prrp_calu_dist_finish": ([_P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_calu_dist_destroy": ([_P], None),
+    "prrp_residual_extended": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_abs_sums": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
 }
 
 _lib = None

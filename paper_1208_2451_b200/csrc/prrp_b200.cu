@@ -2876,4 +2876,35 @@ void prrp_calu_dist_destroy(void* handle) {
   delete w;
 }
 
+// ---------------------------------------------------------------- stability measurements (verify.cuh)
+int prrp_residual_extended(const double* A, int64_t lda, int64_t m, int64_t n, const double* x, const double* rhs,
+                           double* r, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    if (m < 0 || n < 0 || lda < n) fail(PRRP_ERR_ARG, "bad shape");
+    if (m == 0) return PRRP_OK;
+    residual_ext_kernel<<<(unsigned)((m + RX_T - 1) / RX_T), RX_T, 0, (cudaStream_t)stream>>>(A, lda, m, n, x, rhs, r);
+    CU_TRY(cudaGetLastError());
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_abs_sums(const double* A, int64_t lda, int64_t m, int64_t n, const double* x, double* colabs,
+                  double* rowabs, double* absax, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    if (m < 0 || n < 0 || lda < n) fail(PRRP_ERR_ARG, "bad shape");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (colabs && n > 0) abs_colsum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A, lda, m, n, colabs);
+    if ((rowabs || absax) && m > 0)
+      abs_rowsum_kernel<<<(unsigned)((m * 32 + 255) / 256), 256, 0, s>>>(A, lda, m, n, x, rowabs, absax);
+    CU_TRY(cudaGetLastError());
+    return PRRP_OK;
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
 }  // extern "C"

@@ -138,3 +138,93 @@ __global__ void __launch_bounds__(LS_T) lu_solve_kernel(const double* __restrict
     __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// Stability measurements (metrics.py:65-145).
+//
+// residual_extended (metrics.py:75-92): r = rhs - A x accumulated in twice
+// working precision, exactly the reference's recipe per row i, j ascending:
+//   p, pe = two_prod(A[i,j], -x[j])   (Veltkamp split, 2^27 + 1)
+//   s, se = two_sum(s, p)             (Knuth)
+//   comp += pe + se;   r_i = s + comp
+// Every operation is rounded on its own (no FMA contraction), so the result
+// is bit-identical to the numpy elementwise evaluation.  One thread per row;
+// x staged through shared memory.
+// ---------------------------------------------------------------------------
+#define RX_T 128
+#define RX_XC 2048
+__device__ __forceinline__ void two_prod_rn(double a, double b, double& p, double& e) {
+  const double split = 134217729.0;
+  p = mul_rn(a, b);
+  const double ca = mul_rn(split, a);
+  const double ah = sub_rn(ca, sub_rn(ca, a));
+  const double al = sub_rn(a, ah);
+  const double cb = mul_rn(split, b);
+  const double bh = sub_rn(cb, sub_rn(cb, b));
+  const double bl = sub_rn(b, bh);
+  e = add_rn(add_rn(add_rn(sub_rn(mul_rn(ah, bh), p), mul_rn(ah, bl)), mul_rn(al, bh)), mul_rn(al, bl));
+}
+
+__device__ __forceinline__ void two_sum_rn(double a, double b, double& s, double& e) {
+  s = add_rn(a, b);
+  const double bb = sub_rn(s, a);
+  e = add_rn(sub_rn(a, sub_rn(s, bb)), sub_rn(b, bb));
+}
+
+__global__ void __launch_bounds__(RX_T) residual_ext_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
+                                                            int64_t n, const double* __restrict__ x,
+                                                            const double* __restrict__ rhs, double* __restrict__ r) {
+  __shared__ double xs[RX_XC];
+  const int64_t i = (int64_t)blockIdx.x * RX_T + threadIdx.x;
+  double s = i < m ? rhs[i] : 0.0, comp = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += RX_XC) {
+    const int nc = (int)min((int64_t)RX_XC, n - j0);
+    __syncthreads();
+    for (int c = threadIdx.x; c < nc; c += RX_T) xs[c] = -x[j0 + c];
+    __syncthreads();
+    if (i < m) {
+      const double* row = A + i * lda + j0;
+      for (int c = 0; c < nc; ++c) {
+        double p, pe, se;
+        two_prod_rn(row[c], xs[c], p, pe);
+        two_sum_rn(s, p, s, se);
+        comp = add_rn(comp, add_rn(pe, se));
+      }
+    }
+  }
+  if (i < m) r[i] = add_rn(s, comp);
+}
+
+// column sums of |A| (||A||_1 = max), one thread per column (coalesced rows)
+__global__ void abs_colsum_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                  double* __restrict__ colabs) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < m; ++i) s += fabs(A[i * lda + j]);
+  colabs[j] = s;
+}
+
+// row sums of |A| and of |A| |x| (||A||_inf, the componentwise denominator),
+// one warp per row
+__global__ void abs_rowsum_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                  const double* __restrict__ x, double* rowabs, double* absax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= m) return;
+  double s = 0.0, t = 0.0;
+  const double* row = A + i * lda;
+  for (int64_t j = lane; j < n; j += 32) {
+    const double a = fabs(row[j]);
+    s += a;
+    if (x) t = fma(a, fabs(x[j]), t);
+  }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  if (lane == 0) {
+    if (rowabs) rowabs[i] = s;
+    if (absax) absax[i] = t;
+  }
+}

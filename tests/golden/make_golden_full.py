@@ -216,6 +216,34 @@ def case_calu_deficient(name, n, b, P, blocks, tau=2.0):
     return meta, arrays
 
 
+def case_metrics(name, gen, n, b, alg):
+    """The measurement battery (metrics.py:56-228) of the reference on one
+    factorization: residual_extended bits at the reference's solution, eta,
+    w, the HPL triplet, iterative refinement and the inverse norms."""
+    from prrp import metrics
+    if gen == "randn":
+        a = matgen.gen_randn(n, 42)
+    elif gen == "wilkinson":
+        a = matgen.gen_wilkinson(n)
+    else:
+        a = matgen.gen_foster(n, c=1.0, h=1.0, k=1.0)
+    rhs = pmg.gen_randn_rect(n, 1, 5).reshape(-1)
+    f = prrp.luprrp_factor(a, b, 2.0) if alg == "luprrp" else prrp.gepp_factor(a)
+    x0 = np.asarray(f.solve(rhs)).reshape(-1)
+    r = metrics.residual_extended(a, x0, rhs)
+    xr, n_ir, w_before = metrics.iterative_refinement(f, a, rhs)
+    rep = metrics.full_report(a, f, rhs)
+    arrays = {"x0": x0, "r": r, "x_refined": np.asarray(xr)}
+    meta = {"kind": "metrics", "gen": gen, "n": n, "b": b, "alg": alg, "rhs_seed": 5, "input_sha": sha(a),
+            "eta": metrics.normwise_backward_error(a, x0, rhs), "w": metrics.componentwise_backward_error(a, x0, rhs),
+            "hpl": list(metrics.hpl_triplet(a, x0, rhs)), "n_ir": int(n_ir), "w_before": w_before,
+            "inverse_norms": list(metrics.triangular_inverse_norms(f.l, f.u)),
+            "report": [float(v) for v in (rep.g_w, rep.rel_fact_error, rep.eta, rep.w, *rep.hpl, rep.n_ir,
+                                          rep.norm_l1, rep.norm_linv1, rep.norm_u1, rep.norm_uinv1)],
+            "csv_row": metrics.report_csv_row(rep)}
+    return meta, arrays
+
+
 CASES = {
     "c2_b64": lambda: case_lu("c2_b64", "randn", 8192, 64),
     "c2_b128": lambda: case_lu("c2_b128", "randn", 8192, 128),
@@ -237,6 +265,9 @@ CASES["calu_def_leaf640_b64_P8"] = lambda: case_calu_deficient("calu_def_leaf640
                                                                [[0, 80, 20], [160, 240, 30]])
 CASES["calu_def_leaf1024_b128_P4"] = lambda: case_calu_deficient("calu_def_leaf1024_b128_P4", 1024, 128, 4,
                                                                  [[0, 256, 50], [256, 512, 60]])
+CASES["metrics_randn300_b32"] = lambda: case_metrics("metrics_randn300_b32", "randn", 300, 32, "luprrp")
+CASES["metrics_wilkinson55_gepp"] = lambda: case_metrics("metrics_wilkinson55_gepp", "wilkinson", 55, 8, "gepp")
+CASES["metrics_foster256_gepp"] = lambda: case_metrics("metrics_foster256_gepp", "foster", 256, 16, "gepp")
 for _p in (4097, 6000, 8192, 12288, 16384):
     for _b in (64, 128):
         CASES["srrqr_p%d_b%d" % (_p, _b)] = (lambda p=_p, b=_b: case_srrqr("srrqr_p%d_b%d" % (p, b), p, b, 2.0))

@@ -294,3 +294,53 @@ def test_caluprrp_error_fixtures(dev, golden):
             assert 0 <= exc.column < e["b"] * (ref["panel"] + 1), e["name"]
         else:
             assert exc.index == ref["index"], e["name"]
+
+
+# ------------------------------------------------------------ stability measurements
+@pytest.mark.parametrize("name", _names("metrics_"))
+def test_metrics_battery(dev, name):
+    """residual_extended bit for bit at the reference's solution (the
+    compensated recipe is fully specified, metrics.py:75-92); eta, w, the HPL
+    ratios, refinement and the inverse norms within 1e-10 (their sums follow
+    BLAS / numpy orders); full_report and its CSV row."""
+    from paper_1208_2451_b200 import matgen, metrics
+    meta, arr = _load(name)
+    n = meta["n"]
+    if meta["gen"] == "randn":
+        a = matgen.gen_randn(n, 42)
+    elif meta["gen"] == "wilkinson":
+        a = matgen.gen_wilkinson(n)
+    else:
+        a = matgen.gen_foster(n, 1.0, 1.0, 1.0)
+    rhs = matgen.gen_randn_rect(n, 1, meta["rhs_seed"]).reshape(-1)
+    x0 = arr["x0"]
+    r = metrics.residual_extended(a, x0, rhs)
+    assert np.array_equal(r, arr["r"]), name
+    assert metrics.normwise_backward_error(a, x0, rhs) == pytest.approx(meta["eta"], rel=TOL_G)
+    assert metrics.componentwise_backward_error(a, x0, rhs) == pytest.approx(meta["w"], rel=TOL_G)
+    assert metrics.hpl_triplet(a, x0, rhs) == pytest.approx(tuple(meta["hpl"]), rel=TOL_G)
+    f = dev.luprrp_factor(a, meta["b"], 2.0) if meta["alg"] == "luprrp" else dev.gepp_factor(a)
+    xs = f.solve(rhs)
+    xr, n_ir, w_before = metrics.iterative_refinement(f, a, rhs)
+    if meta["gen"] == "wilkinson":
+        # GEPP growth 2^(n-1): the direct solution carries O(1) relative error
+        # whatever the substitution order, so only the refinement's behaviour
+        # is comparable: it runs and improves w
+        assert n_ir >= 1 and metrics.componentwise_backward_error(a, xr, rhs) <= w_before
+    else:
+        assert np.abs(xs - x0).max() <= 1e-8 * max(np.abs(x0).max(), 1.0), name
+        assert n_ir == meta["n_ir"], name
+        assert np.abs(xr - arr["x_refined"]).max() <= 1e-8 * max(np.abs(arr["x_refined"]).max(), 1.0)
+    assert metrics.triangular_inverse_norms(f.l, f.u) == pytest.approx(tuple(meta["inverse_norms"]), rel=1e-9)
+    rep = metrics.full_report(a, f, rhs)
+    got = [rep.g_w, rep.rel_fact_error, rep.eta, rep.w, *rep.hpl, rep.n_ir, rep.norm_l1, rep.norm_linv1,
+           rep.norm_u1, rep.norm_uinv1]
+    assert got[0] == pytest.approx(meta["report"][0], rel=TOL_G)
+    if meta["gen"] != "wilkinson":
+        assert got[7] == meta["report"][7]             # n_ir
+        # eta, w, HPL at the device's direct solution: roundoff-level quantities of
+        # another (equally backward-stable) solution -- same order of magnitude
+        for gv, rv in zip(got[2:7], meta["report"][2:7]):
+            assert rv / 10 <= gv <= 10 * rv, (name, got[2:7], meta["report"][2:7])
+    assert got[8:] == pytest.approx(meta["report"][8:], rel=1e-9)
+    assert len(metrics.report_csv_row(rep).split(",")) == len(metrics.CSV_HEADER)

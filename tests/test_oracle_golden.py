@@ -279,3 +279,16 @@ def test_full_size_generators_match_reference():
     meta, _ = _full("c3_wilkinson")
     a = matgen.gen_wilkinson(meta["n"])
     assert hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest() == meta["input_sha"]
+
+
+@pytest.mark.parametrize("name", _full_names("metrics_"))
+def test_oracle_residual_extended(name):
+    """The oracle's compensated residual (metrics.py:84-92) reproduces the
+    reference's bits at the reference's solution."""
+    from paper_1208_2451_b200 import matgen
+    meta, arr = _full(name)
+    n = meta["n"]
+    a = {"randn": lambda: matgen.gen_randn(n, 42), "wilkinson": lambda: matgen.gen_wilkinson(n),
+         "foster": lambda: matgen.gen_foster(n, 1.0, 1.0, 1.0)}[meta["gen"]]()
+    rhs = matgen.gen_randn_rect(n, 1, meta["rhs_seed"]).reshape(-1)
+    assert np.array_equal(orc.residual_extended(a, arr["x0"], rhs), arr["r"])
