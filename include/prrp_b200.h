@@ -282,6 +282,12 @@ int prrp_residual_extended(const double* A, int64_t lda, int64_t m, int64_t n, c
 int prrp_abs_sums(const double* A, int64_t lda, int64_t m, int64_t n, const double* x, double* colabs,
                   double* rowabs, double* absax, prrp_err* err, void* stream);
 
+/* prrp_gepp whose running maximum covers only the entries each step
+ * updates (max over steps k of max|A[k+1:, k+1:]| after step k): the
+ * block variants' finish statistic (block_variants.py:170-186). */
+int prrp_gepp_steps(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* steps_max,
+                    double* original_max, prrp_err* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

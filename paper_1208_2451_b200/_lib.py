@@ -68,6 +68,7 @@ SIGNATURES = {
     "prrp_calu": ([_P, _I64, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_gepp_select": ([_P, _I64, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
     "prrp_gepp": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "prrp_gepp_steps": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_calu_dist_create": ([_P, _P, _I64, _I64, _I64, _I64, _I32, _D, _I32, _I32, _I32, _P, _P, _P],
                               ctypes.c_int),
     "prrp_calu_dist_buffers": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),

@@ -2316,16 +2316,20 @@ int gepp_select_impl(const double* a, int64_t lda, int64_t r, int cols, int64_t*
 }
 
 // gepp_factor of any shape (gepp.py:39-65): unblocked, two launches per step.
+// steps_only: the running maximum covers the updated entries only (the
+// block variants' observe_finish after every step, block_variants.py:170-186),
+// not seeded with the original maximum (gepp_factor's running_max).
 int gepp_full_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* imax, double* omax,
-                   prrp_err* err, cudaStream_t s) {
+                   prrp_err* err, cudaStream_t s, bool steps_only = false) {
   if (m < 1 || n < 1) fail(PRRP_ERR_DIM, "gepp needs a non-empty matrix");
   if (lda < n) fail(PRRP_ERR_ARG, "lda < n");
   caps();
   const int sms = caps().sms;
   Arena ar(s);
   DevState* st = new_state(ar, s);
+  DevState* st0 = steps_only ? new_state(ar, s) : st;
   iota_kernel<<<sms, 256, 0, s>>>(perm, m);
-  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st);
+  maxabs_kernel<<<sms * 4, 256, 0, s>>>(A, lda, m, n, st0);
   const int64_t steps = std::min(m, n);
   for (int64_t k = 0; k < steps; ++k) {
     gf_pivot_kernel<<<1, 1024, 0, s>>>(A, lda, m, n, k, perm, st);
@@ -2335,10 +2339,12 @@ int gepp_full_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, 
     }
   }
   CU_TRY(cudaGetLastError());
-  DevState hs;
+  DevState hs, hs0;
   read_state(st, hs, s);
+  if (steps_only) read_state(st0, hs0, s);
+  else hs0 = hs;
   if (imax) *imax = bits_to_double(hs.inter_max);
-  if (omax) *omax = bits_to_double(hs.orig_max);
+  if (omax) *omax = bits_to_double(hs0.orig_max);
   return state_to_err(hs, err);
 }
 #include "calu_dist.cuh"
@@ -2755,6 +2761,16 @@ int prrp_gepp(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, doubl
   clear_err(err);
   try {
     return gepp_full_impl(A, lda, m, n, perm, intermediate_max, original_max, err, (cudaStream_t)stream);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
+
+int prrp_gepp_steps(double* A, int64_t lda, int64_t m, int64_t n, int64_t* perm, double* steps_max,
+                    double* original_max, prrp_err* err, void* stream) {
+  clear_err(err);
+  try {
+    return gepp_full_impl(A, lda, m, n, perm, steps_max, original_max, err, (cudaStream_t)stream, true);
   } catch (const Fail& f) {
     return report(err, f);
   }

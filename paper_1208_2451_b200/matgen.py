@@ -133,3 +133,37 @@ def gen_urand_colset(n, seed, cols, chunk_rows=1024):
         blk = rng.random((r1 - r0) * n).reshape(r1 - r0, n)
         out[r0:r1, :] = 2.0 * blk[:, cols] - 1.0
     return out
+
+
+def gen_wright(n, h=0.3):
+    """matgen.gen_wright (matgen.py:133-143): multiple-shooting matrix of a
+    two-point boundary-value problem -- identity, the 2 x 2 blocks
+    -[[1 - h/6, h], [h, 1 - h/6]] below the block diagonal, an identity
+    block in the top-right corner."""
+    if n % 2 or n < 4:
+        raise ValueError("n must be even and >= 4")
+    a = np.eye(n, order="F")
+    blk = -np.array([[1.0 - h / 6.0, h], [h, 1.0 - h / 6.0]])
+    for r in range(2, n, 2):
+        a[r:r + 2, r - 2:r] = blk
+    a[:2, n - 2:] = np.eye(2)
+    return a
+
+
+def gen_generalized_wilkinson(n, r=2, seed=0):
+    """matgen.gen_generalized_wilkinson without fixed u, v (matgen.py:82-110):
+    uniform n x r factors, the strict upper part of -u v^T scaled row by row
+    below 1 in magnitude (factor max|row| (1 + 1/n)), transposed, unit
+    diagonal, last column of ones."""
+    if n < 2 or r < 1:
+        raise ValueError("need n >= 2 and r >= 1")
+    rng = _rng(seed)
+    u = rng.random((n, r))
+    v = rng.random((n, r))
+    t = -np.triu(u @ v.T)
+    for k in range(1, n):
+        t[k - 1, k:] /= np.abs(t[k - 1, k:]).max() * (1.0 + 1.0 / n)
+    t = t - np.diag(np.diag(t))
+    a = t.T + np.eye(n)
+    a[:n - 1, n - 1] = 1.0
+    return np.asfortranarray(a)

@@ -205,8 +205,16 @@ def case_calu_deficient(name, n, b, P, blocks, tau=2.0):
                          "tree_node": list(exc.tree_node) if getattr(exc, "tree_node", None) else None}
         return meta, arrays
     arrays["perm"] = np.asarray(f.perm, dtype=np.int64)
-    arrays["l"] = f.l
-    arrays["u"] = f.u
+    if n <= 256:
+        arrays["l"] = f.l
+        arrays["u"] = f.u
+    else:                                   # compact: sums, diagonal, sample rows
+        rows = [0, 1, b, n // 2, n - 1]
+        arrays.update(l_rowsum=f.l.sum(axis=1), l_colsum=f.l.sum(axis=0), u_rowsum=f.u.sum(axis=1),
+                      u_colsum=f.u.sum(axis=0), u_diag=np.diag(f.u).copy(), l_rows=f.l[rows], u_rows=f.u[rows])
+        meta["sample_rows"] = rows
+        meta["l_max"] = float(np.abs(f.l).max())
+        meta["u_max"] = float(np.abs(f.u).max())
     meta["stats"] = stats_dict(f.stats)
     perm0, trace = prrp.tournament_select(np.asfortranarray(a[:, :b]), b, tau, tree, "srrqr")
     arrays["t0_perm"] = np.asarray(perm0, dtype=np.int64)
@@ -244,6 +252,62 @@ def case_metrics(name, gen, n, b, alg):
     return meta, arrays
 
 
+def case_block_variant(name, kind, n, b, p=None, tau=2.0):
+    """block_parallel_luprrp / block_pairwise_luprrp (block_variants.py:231-244):
+    the event log, the final upper factor, the statistics, and the replay."""
+    from prrp import block_variants as bv
+    a = matgen.gen_randn(n, 42)
+    f = bv.block_parallel_luprrp(a, b, tau, p) if kind == "parallel" else bv.block_pairwise_luprrp(a, b, tau)
+    arrays = {"perm": np.asarray(f.perm, dtype=np.int64)}
+    rows = [0, 1, b, n // 2, n - 1]
+    if n <= 256:
+        arrays["u"] = f.u
+    else:
+        arrays.update(u_rowsum=f.u.sum(axis=1), u_colsum=f.u.sum(axis=0), u_rows=f.u[rows])
+    rep = bv.replay_events(f.events, a)
+    evs = []
+    for i, ev in enumerate(f.events):
+        if isinstance(ev, bv.RowPermEvent):
+            moved = np.nonzero(ev.perm != np.arange(ev.perm.shape[0]))[0]
+            if moved.size == 2 and ev.perm[moved[0]] == moved[1]:
+                evs.append({"type": "perm", "swap": [int(moved[0]), int(moved[1])]})
+            else:
+                arrays[f"ev{i}/perm"] = np.asarray(ev.perm, dtype=np.int64)
+                evs.append({"type": "perm"})
+        else:
+            arrays[f"ev{i}/elim"] = np.asarray(ev.elim_rows, dtype=np.int64)
+            arrays[f"ev{i}/piv"] = np.asarray(ev.pivot_rows, dtype=np.int64)
+            arrays[f"ev{i}/d"] = np.asarray(ev.d)
+            evs.append({"type": "elim", "zero": [ev.zero_col0, ev.zero_col1], "update_col0": ev.update_col0})
+    meta = {"kind": "block_" + kind, "n": n, "b": b, "p": p, "tau": tau, "seed": 42, "input_sha": sha(a),
+            "events": evs, "stats": stats_dict(f.stats), "leaf_counts": list(map(int, f.leaf_counts)),
+            "max_multiplier": f.max_multiplier, "sample_rows": rows, "u_max": float(np.abs(f.u).max()),
+            "replay_max_diff": float(np.abs(rep - f.u).max())}
+    return meta, arrays
+
+
+def case_harness(name):
+    """cli.run_single rows (CSV schema v1, cli.py:124-175) for every algorithm
+    on one small matrix, and the text format of a matrix."""
+    from prrp import cli
+    a = matgen.gen_randn(96, 42)
+    rows = {}
+    for alg in cli.ALGORITHMS:
+        rows[alg] = {k: (v if isinstance(v, (str, int)) else float(v)) for k, v in
+                     cli.run_single(alg, a, b=16, p=4, tau=2.0, seed=42, family="randn").items()}
+    txt = prrp.matcore.matrix_to_text(a[:5, :7])
+    gens = {"wright:20": sha(matgen.generate(matgen.parse_spec("wright:20"))),
+            "wright:64:h=0.7": sha(matgen.generate(matgen.parse_spec("wright:64:h=0.7"))),
+            "genwilk:50:r=3": sha(matgen.generate(matgen.parse_spec("genwilk:50:r=3", seed=7))),
+            "foster:40:k=1/3": sha(matgen.generate(matgen.parse_spec("foster:40:k=1/3"))),
+            "wilkinson:33": sha(matgen.generate(matgen.parse_spec("wilkinson:33"))),
+            "randn:30": sha(matgen.generate(matgen.parse_spec("randn:30", seed=5)))}
+    meta = {"kind": "harness", "n": 96, "b": 16, "p": 4, "seed": 42, "rows": rows, "text_5x7": txt,
+            "csv_header": list(cli.CSV_HEADER), "csv_version": cli.CSV_VERSION, "generator_sha": gens,
+            "generator_seeds": {"genwilk:50:r=3": 7, "randn:30": 5}}
+    return meta, {}
+
+
 CASES = {
     "c2_b64": lambda: case_lu("c2_b64", "randn", 8192, 64),
     "c2_b128": lambda: case_lu("c2_b128", "randn", 8192, 128),
@@ -266,6 +330,12 @@ CASES["calu_def_leaf640_b64_P8"] = lambda: case_calu_deficient("calu_def_leaf640
 CASES["calu_def_leaf1024_b128_P4"] = lambda: case_calu_deficient("calu_def_leaf1024_b128_P4", 1024, 128, 4,
                                                                  [[0, 256, 50], [256, 512, 60]])
 CASES["metrics_randn300_b32"] = lambda: case_metrics("metrics_randn300_b32", "randn", 300, 32, "luprrp")
+CASES["block_parallel256_b16_p4"] = lambda: case_block_variant("block_parallel256_b16_p4", "parallel", 256, 16, 4)
+CASES["block_parallel512_b64_p8"] = lambda: case_block_variant("block_parallel512_b64_p8", "parallel", 512, 64, 8)
+CASES["block_pairwise200_b16"] = lambda: case_block_variant("block_pairwise200_b16", "pairwise", 200, 16)
+CASES["block_pairwise384_b32_tau11"] = lambda: case_block_variant("block_pairwise384_b32_tau11", "pairwise", 384, 32,
+                                                                   tau=1.1)
+CASES["harness_rows_n96"] = lambda: case_harness("harness_rows_n96")
 CASES["metrics_wilkinson55_gepp"] = lambda: case_metrics("metrics_wilkinson55_gepp", "wilkinson", 55, 8, "gepp")
 CASES["metrics_foster256_gepp"] = lambda: case_metrics("metrics_foster256_gepp", "foster", 256, 16, "gepp")
 for _p in (4097, 6000, 8192, 12288, 16384):

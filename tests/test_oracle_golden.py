@@ -292,3 +292,24 @@ def test_oracle_residual_extended(name):
          "foster": lambda: matgen.gen_foster(n, 1.0, 1.0, 1.0)}[meta["gen"]]()
     rhs = matgen.gen_randn_rect(n, 1, meta["rhs_seed"]).reshape(-1)
     assert np.array_equal(orc.residual_extended(a, arr["x0"], rhs), arr["r"])
+
+
+def test_harness_formats_and_generators():
+    """The matrix text format (matcore.py:189-225) byte for byte, generator
+    specs (matgen.py:378-413) and the harness families' bits against the
+    reference's, CSV schema v1 (cli.py:29-33)."""
+    import io
+    from paper_1208_2451_b200 import harness
+    meta, _ = _full("harness_rows_n96")
+    from paper_1208_2451_b200 import matgen
+    a = matgen.gen_randn(meta["n"], meta["seed"])
+    assert harness.matrix_to_text(a[:5, :7]) == meta["text_5x7"]
+    assert np.array_equal(harness.read_matrix(io.StringIO(meta["text_5x7"])), a[:5, :7])
+    for spec, want in meta["generator_sha"].items():
+        g = harness.generate(harness.parse_spec(spec, seed=meta["generator_seeds"].get(spec, 0)))
+        assert hashlib.sha256(np.ascontiguousarray(g).tobytes()).hexdigest() == want, spec
+    assert list(harness.CSV_HEADER) == meta["csv_header"] and harness.CSV_VERSION == meta["csv_version"]
+    with pytest.raises(ValueError):
+        harness.read_matrix(io.StringIO("2 2\n1 2\n3\n"))
+    with pytest.raises(ValueError):
+        harness.parse_spec("randn")
