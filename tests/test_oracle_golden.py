@@ -244,8 +244,12 @@ def test_oracle_calu_rank_deficient_nodes(name):
         return
     f = orc.calu_prrp(a, meta["b"], meta["tau"], shape, leaf)
     assert np.array_equal(f.perm, arr["perm"])
-    _close(f.l, arr["l"], False)
-    _close(f.u, arr["u"], False)
+    if "l" in arr:
+        _close(f.l, arr["l"], False)
+        _close(f.u, arr["u"], False)
+    else:
+        _close(f.l[meta["sample_rows"]], arr["l_rows"], False)
+        _close(f.u[meta["sample_rows"]], arr["u_rows"], False)
     perm, trace = orc.tournament(np.asfortranarray(a[:, :meta["b"]]), meta["b"], meta["tau"], shape, leaf)
     assert np.array_equal(perm, arr["t0_perm"])
     got = [(n.level, n.index, n.members.tolist(), n.selected.tolist()) for n in trace.nodes]
