@@ -376,3 +376,27 @@ __global__ void calu_flat_inputs_kernel(const int32_t* cands, const int32_t* ccn
   }
   if (threadIdx.x == 0) live_out[0] = c + len;
 }
+
+// The unpivoted QR of the permuted panel (tournament.py:271) comes from the
+// tournament's ROOT node when that node ran its QRCP: the root's first b
+// pivot columns are the winners in selection order -- the columns of A11^T
+// -- and a Householder reflector depends only on its own pivot column, so the
+// root's leading R block and its first b logged reflectors are exactly the
+// QR of A11^T (after swap-loop interchanges the root's R and log were
+// recomputed from scratch in the final order).  Copies them, and sets
+// final_live = 0 so the separate final-QR launch returns at once; a root
+// that passed its members through (live <= b) leaves final_live large and
+// that launch runs.
+__global__ void calu_root_qr_kernel(const int32_t* root_live, int b, const double* root_R, int64_t root_p,
+                                    const double* root_refl, double* Rsmall, double* refl, int32_t* final_live,
+                                    const DevState* st) {
+  if (prrp_failed(st)) return;
+  const bool ran = *root_live > b;
+  if (threadIdx.x == 0) *final_live = ran ? 0 : INT_MAX;
+  if (!ran) return;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e / b, q = e - i * b;
+    Rsmall[e] = root_R[(int64_t)i * root_p + q];
+  }
+  for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) refl[e] = root_refl[e];
+}

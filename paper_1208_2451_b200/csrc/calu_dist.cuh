@@ -49,6 +49,7 @@ struct CaluDist {
   double* Qneg = nullptr;
   double* A21t = nullptr;
   int32_t* perm_small = nullptr;
+  int32_t* final_live = nullptr;
   PanelBuffers B{};
   std::vector<NodeBufs> nodes;
   int32_t *cands = nullptr, *ccnt = nullptr, *want_all = nullptr, *live_all = nullptr;
@@ -194,6 +195,7 @@ void calu_dist_alloc(CaluDist& w, cudaStream_t s) {
   w.Rsmall = ar.get<double>((size_t)b * b);
   w.refl = ar.get<double>((size_t)b * (b + 1));
   w.perm_small = ar.get<int32_t>(b);
+  w.final_live = ar.get<int32_t>(1);
   w.Qneg = ar.get<double>((size_t)b * b);
   w.ld21t = ((m + 7) / 8) * 8;
   w.A21t = ar.get<double>((size_t)b * w.ld21t);
@@ -212,6 +214,7 @@ void calu_dist_alloc(CaluDist& w, cudaStream_t s) {
     nb.B.cand_flat = ar.get<long long>(kMaxCand);
     nb.B.moved = ar.get<int32_t>(2 * pnode);
     nb.B.fro = ar.get<double>(1);
+    nb.B.refl = ar.get<double>((size_t)b * (b + 1));   // reflector log: the root's is the final QR (calu_root_qr_kernel)
     nb.ldl = ((pnode + 7) / 8) * 8;
     nb.L21 = ar.get<double>((size_t)b * nb.ldl);
     nb.lpos_in = w.lpos_all + (size_t)i * 2 * b;
@@ -322,6 +325,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
     };
     int32_t* cur = w.cands;
     int32_t* ccur = w.ccnt;
+    int64_t root_p = 0;     // columns of the root node's QRCP (the final QR reuses it)
     if (pe > 1 && w.P == 0) {
       const int64_t first = std::min<int64_t>(rows, 2 * bj);
       calu_leaf_lo_kernel<<<1, 64, 0, s>>>(w.leaf_lo_dev, 1, rows, 0);
@@ -336,6 +340,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
         const int64_t len = std::min<int64_t>(bj, rows - lo);
         calu_flat_inputs_kernel<<<1, 128, 0, s>>>(cur, ccur, bj, lo, (int)len, w.lpos_all, w.rowidx_all,
                                                   w.live_all, w.pos2row, col0, w.st);
+        root_p = bj + len;
         run_level({0}, {bj + len}, false, level, slot++);
         calu_select_kernel<<<1, 128, 0, s>>>(w.perms_dev, w.lpos_all, nullptr, bj, w.want_all, w.live_all, 1, nxt,
                                              cnxt, 2 * b, w.st);
@@ -373,6 +378,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
         const int64_t nm = ncur / 2;
         calu_merge_inputs_kernel<<<(unsigned)nm, 128, 0, s>>>(cur, ccur, bj, (int)(2 * nm), w.lpos_all,
                                                               w.rowidx_all, w.live_all, w.pos2row, col0, 2 * b, w.st);
+        root_p = 2 * bj;
         run_level(std::vector<int64_t>(nm, 0), std::vector<int64_t>(nm, 2 * bj), false, level, slot);
         slot += (int)nm;
         calu_select_kernel<<<(unsigned)nm, 128, 0, s>>>(w.perms_dev, w.lpos_all, nullptr, bj, w.want_all,
@@ -425,6 +431,11 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       qa.st = st;
       qa.panel_id = k;
       iota32_kernel<<<1, 128, 0, s>>>(w.perm_small, bj);
+      if (reuse_root_qr()) {
+        calu_root_qr_kernel<<<1, 256, 0, s>>>(w.live_all, bj, w.nodes[0].B.Rbuf, root_p, w.nodes[0].B.refl,
+                                              w.Rsmall, w.refl, w.final_live, w.st);
+        qa.live = w.final_live;
+      }
       if (team_eligible(bj, bj) && !force_generic_panel()) {
         PanelArgs at = qa;
         at.fro = w.nodes[0].B.fro;

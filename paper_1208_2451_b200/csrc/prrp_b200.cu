@@ -395,6 +395,13 @@ int team_cols(int h) {
   return (nr <= 4 ? PTCfg<4>::T : nr <= 8 ? PTCfg<8>::T : PTCfg<16>::T) / PT_G;
 }
 
+// The CALU final QR reuses the tournament root's QRCP (calu_root_qr_kernel);
+// PRRP_ROOT_QR=0 runs the separate QR of A11^T every panel instead.
+bool reuse_root_qr() {
+  static const bool v = !(getenv("PRRP_ROOT_QR") && atoi(getenv("PRRP_ROOT_QR")) == 0);
+  return v;
+}
+
 bool team_eligible(int h, int64_t p) {
   return h >= 1 && h <= PRRP_MAXH && p >= 1 &&
          p <= std::min<int64_t>(team_max_p(), (int64_t)team_cols(h) * caps().max_cluster);
@@ -1347,6 +1354,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   // by row form is the faster one, 289 vs 303 ms at n = 16384)
   static const bool calu_r12_gemm = !getenv("PRRP_CALU_R12_GEMM") || atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
   double* Qneg = ar.get<double>((size_t)b * b);
+  int32_t* final_live = ar.get<int32_t>(1);
   const int64_t ld21t = ((m + 7) / 8) * 8;
   double* A21t = ar.get<double>((size_t)b * ld21t);
   DevState* st_r12 = new_state(ar, s);   // the product's |C| must not enter the growth statistics
@@ -1366,6 +1374,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
     nb.B.cand_flat = ar.get<long long>(kMaxCand);
     nb.B.moved = ar.get<int32_t>(2 * pnode);
     nb.B.fro = ar.get<double>(1);
+    nb.B.refl = ar.get<double>((size_t)b * (b + 1));   // reflector log: the root's is the final QR (calu_root_qr_kernel)
     nb.ldl = ((pnode + 7) / 8) * 8;
     nb.L21 = ar.get<double>((size_t)b * nb.ldl);
     nb.lpos_in = lpos_all + (size_t)i * 2 * b;
@@ -1528,6 +1537,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       const int64_t first = std::min<int64_t>(rows, 2 * bj);
       const int64_t p_eff = flat ? 1 + (rows - first + bj - 1) / bj
                                  : std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
+      int64_t root_p = 0;   // columns of the root node's QRCP (the final QR reuses it)
       if (p_eff > 1 && flat) {
         // flat tree: the first block as a leaf, then one merge node per block
         // on [candidates, block rows] (members in that order, tournament.py:206)
@@ -1548,6 +1558,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         int level = 1;
         for (int64_t lo = first; lo < rows; lo += bj, ++level) {
           const int64_t len = std::min<int64_t>(bj, rows - lo);
+          root_p = bj + len;
           calu_flat_inputs_kernel<<<1, 128, 0, sm>>>(cur, ccur, bj, lo, (int)len, lpos_all, rowidx_all, live_all,
                                                      pos2row, col0, st);
           run_level(std::vector<int64_t>{0}, std::vector<int64_t>{bj + len}, false, col0, bj, panel, level, slot, sm);
@@ -1619,6 +1630,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                                                                       rowidx_all, live_all, pos2row, col0, 2 * b, st);
           CU_TRY(cudaGetLastError());
           std::vector<int64_t> mlo(nmerge, 0), mcnt(nmerge, 2 * bj);
+          root_p = 2 * bj;
           run_level(mlo, mcnt, false, col0, bj, panel, level, slot, sm);
           for (int64_t i = 0; i < nmerge; ++i) {
             chg3 += qr_charge3(2 * bj, bj);
@@ -1674,6 +1686,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         qa.panel_id = panel;
         tbegin(PRRP_K_FINALIZE, sm);
         iota32_kernel<<<1, 128, 0, sm>>>(perm_small, bj);
+        if (reuse_root_qr()) {
+          calu_root_qr_kernel<<<1, 256, 0, sm>>>(live_all, bj, nodes[0].B.Rbuf, root_p, nodes[0].B.refl, Rsmall, refl,
+                                                 final_live, st);
+          qa.live = final_live;   // the engine below runs only when the root passed its members through
+        }
         if (team_eligible(bj, bj) && !force_generic_panel()) {
           PanelArgs at = qa;
           at.fro = nodes[0].B.fro;
