@@ -266,8 +266,16 @@ def run_device(args):
     import torch
     ws, rank, local = dist_info()
     torch.cuda.set_device(local)
-    if ws > 1:
+    # PRRP_BENCH_DIST=1: the distributed driver even at N = 1 (exercises the
+    # NCCL path on one GPU; the N = 1 headline uses the single-GPU driver)
+    use_dist = ws > 1 or os.environ.get("PRRP_BENCH_DIST") == "1"
+    if use_dist:
         import torch.distributed as dist
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1208_2451_b200 import _lib, matgen
     from paper_1208_2451_b200 import dist as pd
@@ -291,7 +299,7 @@ def run_device(args):
     peak = pk.value
 
     # ---- inputs resident in HBM
-    if ws == 1:
+    if not use_dist:
         cols = np.arange(n)
         a_loc = matgen.gen_urand(n, args.seed, order="C")
     else:
@@ -306,7 +314,7 @@ def run_device(args):
     tree = prrp.binary_tree(P)
 
     def step():
-        if ws == 1:
+        if not use_dist:
             return calu_call(lib, _lib, work, n, b, tau, P, perm)[0]
         return pd.caluprrp_factor_dist_device(work, n, n, b, tau, tree).stats
 
@@ -329,14 +337,14 @@ def run_device(args):
     clk = clocks.stop()
     ms_step = statistics.mean(times)
     value = lu_flops(n) / (ms_step * 1e-3) / 1e9
-    growth = (st.intermediate_max / st.original_max) if ws == 1 else st.growth_factor
+    growth = (st.intermediate_max / st.original_max) if not use_dist else st.growth_factor
     launches = None
-    if ws == 1:
+    if not use_dist:
         launches = int(lib.prrp_b200_graph_kernels()) * args.steps
 
     extra = {"step_ms": [round(t, 2) for t in times], "growth_factor": growth}
     roofline = None
-    if ws == 1:
+    if not use_dist:
         # per-class spans of the same factorization (direct enqueue, every launch timed)
         tms = []
         for _ in range(2):
@@ -352,7 +360,7 @@ def run_device(args):
     # ---- end to end through the public API (host buffers, H2D + D2H in the timed region)
     e2e = None
     if args.e2e_steps > 0:
-        if ws == 1:
+        if not use_dist:
             pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
             pinned.copy_(torch.from_numpy(a_loc))
             a_pin = pinned.numpy()
@@ -394,7 +402,7 @@ def run_device(args):
 
     # ---- bounded CPU sample (rank 0, N = 1)
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and not use_dist and not args.no_cpu:
         try:
             dt, flops, desc = cpu_sample(args, np.asfortranarray(a_loc[:, :(max(1, args.cpu_panels) + 1) * b]))
             cpu = dict({"value": flops / dt / 1e9, "unit": UNIT, "kind": "port", "sample": desc}, **cpu_descr())
@@ -403,7 +411,7 @@ def run_device(args):
     del a_loc
 
     # ---- secondary workloads (N = 1)
-    if ws == 1 and not args.no_secondary:
+    if not use_dist and not args.no_secondary:
         extra["lu_prrp_config2"] = lu_prrp_lines(lib, _lib, torch, matgen, peak, args)
         extra["calu_prrp_config4"] = calu_secondary(lib, _lib, torch, matgen, 16384, 64, "randn", args, peak)
         extra["calu_factor_gepp_n8192"] = calu_secondary(lib, _lib, torch, matgen, 8192, 64, "randn", args, peak,
@@ -416,9 +424,10 @@ def run_device(args):
                 "data": "synthetic (U(-1,1) with the reference's matgen conventions: PCG64 seed 42, row-major fill)",
                 "config": dict(workload(args, ws), **extra), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "driver": "distributed (prrp_calu_dist_*, NCCL)" if use_dist else "single-GPU graph (prrp_caluprrp)",
                 "fp64_peak_fraction": (value / ws / 1e3) / peak if peak else None, "fp64_peak_tflops": peak}
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
 
 

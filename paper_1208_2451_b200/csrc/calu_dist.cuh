@@ -520,6 +520,13 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
   CU_TRY(cudaGetLastError());
 }
 
+// CTAs of the owner's look-ahead tail update (PRRP_DIST_TAIL_FREE SMs left
+// for its tournament, default 8; 0 = every SM)
+int dist_tail_ctas() {
+  static const int free_sms = getenv("PRRP_DIST_TAIL_FREE") ? atoi(getenv("PRRP_DIST_TAIL_FREE")) : 8;
+  return free_sms > 0 ? std::max(1, caps().sms - free_sms) : 0;
+}
+
 // Every rank, after the message of panel k arrived in msgs[k & 1].
 // part 0: everything; 1 (head): all but the trailing update beyond the next
 // panel's block; 2 (tail): that remaining update.  The owner of panel k + 1
@@ -588,9 +595,11 @@ void calu_dist_apply(CaluDist& w, int k, int part, cudaStream_t s) {
   }
   if (part == 2 && rows > bj && wt > wh) {
     const int64_t wh2 = next_mine ? std::min<int64_t>(wt, b) : 0;
+    // the owner of panel k+1 runs its tournament concurrently (dist.py's side
+    // stream): leave it a few SMs, as the single-GPU schedule's deferred update does
     if (wt > wh2)
       schur_update(w.A + (col0 + bj) * w.lda + t0 + wh2, w.lda, Lp, ldk, w.a12 + wh2, w.lda12, rows - bj, wt - wh2,
-                   bj, st, s);
+                   bj, st, s, dist_tail_ctas());
   }
   CU_TRY(cudaGetLastError());
 }

@@ -189,14 +189,21 @@ def caluprrp_factor_dist_device(A_loc, m, n, b, tau=2.0, tree=None, group=None, 
 
         if rank == panel_owner(0, world):
             check(lib.prrp_calu_dist_select(h, 0, ctypes.byref(err), stream), "prrp_calu_dist_select")
+        # look-ahead: the owner of panel k+1 runs its tournament on a high-priority
+        # side stream, concurrently with the rest of panel k's trailing update
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream(priority=-1) if lookahead else None
+        side_h = _lib.stream_handle(side) if side is not None else None
         for k in range(npan):
             nb = lib.prrp_calu_dist_msg_bytes(h, k)
             tp.broadcast(msgs[k & 1][:nb], panel_owner(k, world))
             nxt = k + 1 < npan and rank == panel_owner(k + 1, world)
             if nxt and lookahead:
                 check(lib.prrp_calu_dist_apply(h, k, 1, ctypes.byref(err), stream), "prrp_calu_dist_apply")
-                check(lib.prrp_calu_dist_select(h, k + 1, ctypes.byref(err), stream), "prrp_calu_dist_select")
+                side.wait_stream(main)
+                check(lib.prrp_calu_dist_select(h, k + 1, ctypes.byref(err), side_h), "prrp_calu_dist_select")
                 check(lib.prrp_calu_dist_apply(h, k, 2, ctypes.byref(err), stream), "prrp_calu_dist_apply")
+                main.wait_stream(side)           # the next message leaves after the selection
             else:
                 check(lib.prrp_calu_dist_apply(h, k, 0, ctypes.byref(err), stream), "prrp_calu_dist_apply")
                 if nxt:
