@@ -137,6 +137,16 @@ int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, doubl
  * replayed (diagnostics / the bench's launch count; 0 before any call). */
 int64_t prrp_b200_graph_kernels(void);
 
+/* Diagnostics: average device time (ms) of the panel QRCP engine alone
+ * (qr_column_pivoting, pivoted_qr.py:74-87) on an h x p transposed panel
+ * whose columns are the rows of `a` (device, row-major, lda), `reps`
+ * launches between CUDA events.  nwc / cpt > 0 force a latency-engine shape
+ * (compute warps per CTA, columns per 8-thread team), 0 = the default
+ * choice; nwc < 0 runs the thread-per-column engines (h = 64 or 128).
+ * ctas_out = cluster size used. */
+int prrp_b200_qrcp_time(const double* a, int64_t lda, int32_t h, int64_t p, int32_t nwc, int32_t cpt, int32_t reps,
+                        double* ms_out, int32_t* ctas_out, prrp_err* err);
+
 /* prrp_caluprrp through the direct (uncaptured) enqueue with every launch
  * timed by CUDA events on its stream (per kernel class, as
  * prrp_luprrp_timed); timing may be NULL. */

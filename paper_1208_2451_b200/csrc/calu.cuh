@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256) calu_apply_refl_kernel(const double* A, i
 
 // copy R11 (b x b, row stride pb) of a small QR into the leading block of Rbuf (stride p)
 __global__ void calu_copy_r11_kernel(const double* Rsmall, int b, double* Rbuf, int64_t p) {
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < b * b; e += gridDim.x * blockDim.x) {
     const int i = e / b, q = e % b;
     Rbuf[(int64_t)i * p + q] = Rsmall[(int64_t)i * b + q];
   }
@@ -319,42 +319,57 @@ __global__ void __launch_bounds__(256) calu_gather_t_kernel(const double* A, int
 }
 
 // L = -Q^T (column-major b x b) of a logged unpivoted QR, Q^T = H_{b-1} ... H_0:
-// the identity's columns are transformed by the reflectors in log order, two
-// threads per column (rows [0, 64) and [64, 128) in registers, partial dots
-// combined with one shuffle).  Reflector log: refl[k*(b+1) + i] = v_i
-// (zero for i < k), refl[k*(b+1) + b] = beta (0: step skipped).
-__global__ void __launch_bounds__(256) calu_form_negqt_kernel(const double* refl, int b, double* L) {
+// the identity's columns are transformed by the reflectors in log order.  A
+// team of 8 threads owns a column (thread q keeps rows 8u + q, 16 values for
+// b = 128), 16 columns per 128-thread CTA, ceil(b / 16) CTAs, so a reflector
+// step is 2 x 16 FMAs and three shuffles per thread instead of a 128-row
+// pass (the two-threads-per-column single-CTA form took 0.28 ms per panel
+// on the CALU critical path).
+// Reflector log: refl[k*(b+1) + i] = v_i (zero for i < k),
+// refl[k*(b+1) + b] = beta (0: step skipped).
+__global__ void __launch_bounds__(128) calu_form_negqt_kernel(const double* refl, int b, double* L) {
   extern __shared__ __align__(16) double rf[];   // b x (b + 1)
   for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) rf[e] = refl[e];
   __syncthreads();
-  const int j = threadIdx.x >> 1, hh = threadIdx.x & 1;
+  const int j = blockIdx.x * 16 + (threadIdx.x >> 3), q = threadIdx.x & 7;
   const bool on = j < b;
-  double m[64];
+  double m[PRRP_MAXH / 8];
 #pragma unroll
-  for (int u = 0; u < 64; ++u) m[u] = (on && hh * 64 + u == j) ? 1.0 : 0.0;
+  for (int u = 0; u < PRRP_MAXH / 8; ++u) m[u] = (on && 8 * u + q == j) ? 1.0 : 0.0;
+  const int nu = (b + 7) >> 3;
   for (int k = 0; k < b; ++k) {
     const double* v = rf + k * (b + 1);
     const double beta = v[b];
-    if (beta == 0.0) continue;
-    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    if (beta == 0.0) continue;                    // uniform
+    const int u0 = k >> 3;                        // v is zero above row k
+    double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-    for (int u = 0; u < 64; ++u) {
-      const int i = hh * 64 + u;
-      if (i < b) d[u & 3] = fma(v[i], m[u], d[u & 3]);
+    for (int u = 0; u < PRRP_MAXH / 8; ++u) {
+      if (u >= u0 && u < nu) {
+        const int i = 8 * u + q;
+        const double vi = i < b ? v[i] : 0.0;
+        if (u & 1) d1 = fma(vi, m[u], d1);
+        else d0 = fma(vi, m[u], d0);
+      }
     }
-    double dot = (d[0] + d[1]) + (d[2] + d[3]);
+    double dot = d0 + d1;
     dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+    dot += __shfl_xor_sync(0xffffffffu, dot, 4);
     const double w = beta * dot;
 #pragma unroll
-    for (int u = 0; u < 64; ++u) {
-      const int i = hh * 64 + u;
-      if (i < b) m[u] = fma(-v[i], w, m[u]);
+    for (int u = 0; u < PRRP_MAXH / 8; ++u) {
+      if (u >= u0 && u < nu) {
+        const int i = 8 * u + q;
+        const double vi = i < b ? v[i] : 0.0;
+        m[u] = fma(-vi, w, m[u]);
+      }
     }
   }
   if (on) {
 #pragma unroll
-    for (int u = 0; u < 64; ++u) {
-      const int i = hh * 64 + u;
+    for (int u = 0; u < PRRP_MAXH / 8; ++u) {
+      const int i = 8 * u + q;
       if (i < b) L[i + (int64_t)j * b] = -m[u];
     }
   }
@@ -392,11 +407,12 @@ __global__ void calu_root_qr_kernel(const int32_t* root_live, int b, const doubl
                                     const DevState* st) {
   if (prrp_failed(st)) return;
   const bool ran = *root_live > b;
-  if (threadIdx.x == 0) *final_live = ran ? 0 : INT_MAX;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *final_live = ran ? 0 : INT_MAX;
   if (!ran) return;
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int e = t0; e < b * b; e += nt) {
     const int i = e / b, q = e - i * b;
     Rsmall[e] = root_R[(int64_t)i * root_p + q];
   }
-  for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) refl[e] = root_refl[e];
+  for (int e = t0; e < b * (b + 1); e += nt) refl[e] = root_refl[e];
 }

@@ -275,6 +275,11 @@ void calu_dist_alloc(CaluDist& w, cudaStream_t s) {
 // GEPP of the pivot block; the message is complete when this returns (stream
 // ordered).
 void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
+  // the same engine per node as the single-GPU driver (caluprrp_enqueue)
+  struct LatScope {
+    ~LatScope() { tl_lat_cmax = -1; }
+  } lat_scope;
+  tl_lat_cmax = calu_chain_bound(w.m, w.n, w.b, k, w.P == 0) ? 16 : 0;
   w.msg = w.msgs[k & 1];
   const int b = w.b;
   const int64_t m = w.m, n = w.n, col0 = (int64_t)k * b;
@@ -310,9 +315,12 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
         nbuf.live = leaves ? nullptr : w.live_all + i;
         nbuf.want = w.want_all + i;
         nbuf.node_rows = w.node_rows + (size_t)k * maxnodes;
+        const int cmax_level = tl_lat_cmax;             // same engine shapes as caluprrp_enqueue
+        if (leaves && tl_lat_cmax > 0) tl_lat_cmax = std::min(tl_lat_cmax, calu_leaf_cmax());
         strong_rrqr_panel(Ash + col0, w.lda, bj, cnt[i], bj, w.tau, k, w.nodes[i].L21, w.nodes[i].ldl, nbuf, st,
                           w.node_swaps + (size_t)k * maxnodes, nullptr, nullptr, nullptr, false, ns, ridx, slot0 + i,
                           level, i);
+        tl_lat_cmax = cmax_level;
       }
       for (int i = 0; i < nn; ++i) {
         cudaEvent_t jn;
@@ -352,8 +360,13 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       PanelBuffers Bk = w.B;
       Bk.moved = w.moved;
       Bk.moved_cnt = w.mcnt;
-      strong_rrqr_panel(Ash + col0, w.lda, bj, rows, bj, w.tau, k, w.Lg, w.ldl, Bk, st, w.swaps_dev, nullptr,
-                        nullptr, nullptr, false, s, w.pos2row + col0);
+      {
+        const int keep = tl_lat_cmax;                   // the single node is the LU_PRRP panel (see caluprrp_enqueue)
+        tl_lat_cmax = -1;
+        strong_rrqr_panel(Ash + col0, w.lda, bj, rows, bj, w.tau, k, w.Lg, w.ldl, Bk, st, w.swaps_dev, nullptr,
+                          nullptr, nullptr, false, s, w.pos2row + col0);
+        tl_lat_cmax = keep;
+      }
       CU_TRY(cudaMemcpyAsync(full, w.B.perm, sizeof(int32_t) * rows, cudaMemcpyDeviceToDevice, s));
       w.root_mode = 1;
     } else {
@@ -432,7 +445,7 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       qa.panel_id = k;
       iota32_kernel<<<1, 128, 0, s>>>(w.perm_small, bj);
       if (reuse_root_qr()) {
-        calu_root_qr_kernel<<<1, 256, 0, s>>>(w.live_all, bj, w.nodes[0].B.Rbuf, root_p, w.nodes[0].B.refl,
+        calu_root_qr_kernel<<<16, 256, 0, s>>>(w.live_all, bj, w.nodes[0].B.Rbuf, root_p, w.nodes[0].B.refl,
                                               w.Rsmall, w.refl, w.final_live, w.st);
         qa.live = w.final_live;
       }
@@ -459,12 +472,12 @@ void calu_dist_select(CaluDist& w, int k, cudaStream_t s) {
       } else {
         launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, s, qa);
       }
-      calu_copy_r11_kernel<<<1, 256, 0, s>>>(w.Rsmall, bj, w.B.Rbuf, rows);
+      calu_copy_r11_kernel<<<16, 256, 0, s>>>(w.Rsmall, bj, w.B.Rbuf, rows);
       static const bool calu_r12_gemm = !getenv("PRRP_CALU_R12_GEMM") || atoi(getenv("PRRP_CALU_R12_GEMM")) != 0;
       static const int r12_min_b = getenv("PRRP_CALU_R12_MIN_B") ? atoi(getenv("PRRP_CALU_R12_MIN_B")) : 65;
       const int64_t ncol = rows - bj;
       if (calu_r12_gemm && bj >= r12_min_b && (bj % 2 == 0)) {
-        calu_form_negqt_kernel<<<1, 256, (size_t)bj * (bj + 1) * 8, s>>>(w.refl, bj, w.Qneg);
+        calu_form_negqt_kernel<<<(bj + 15) / 16, 128, (size_t)bj * (bj + 1) * 8, s>>>(w.refl, bj, w.Qneg);
         calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, s>>>(
             Ash, w.lda, col0, bj, ncol, w.pos2row + col0 + bj, w.A21t, w.ld21t, w.st);
         zero2d_kernel<<<(unsigned)std::min<int64_t>(4 * sms, (ncol * bj + 255) / 256), 256, 0, s>>>(

@@ -28,7 +28,7 @@
 #include "panel64.cuh"
 #include "panel1.cuh"
 #include "panel2.cuh"
-#include "panel_team.cuh"
+#include "panel_lat.cuh"
 #include "tri64.cuh"
 #include "rowops.cuh"
 #include "schur.cuh"
@@ -113,9 +113,13 @@ DeviceCaps& caps() {
     CU_TRY(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     for (const void* fn : {(const void*)panel_qrcp_kernel, (const void*)panel_finalize_kernel,
                            (const void*)panel_qrcp64_kernel, (const void*)panel_qrcp1_kernel,
-                           (const void*)panel_qrcp2_kernel, (const void*)panel_team_kernel<4>,
-                           (const void*)panel_team_kernel<8>, (const void*)panel_team_kernel<12>,
-                           (const void*)panel_team_kernel<16>}) {
+                           (const void*)panel_qrcp2_kernel,
+#define LAT_FN(NR, CPT, NWC) (const void*)panel_lat_kernel<NR, CPT, NWC, true>
+#define LAT_FNS(NR) LAT_FN(NR, 1, 7), LAT_FN(NR, 2, 7), LAT_FN(NR, 4, 7), LAT_FN(NR, 1, 15), LAT_FN(NR, 2, 15)
+                           LAT_FNS(4), LAT_FNS(8), LAT_FNS(16), LAT_FN(4, 4, 15), LAT_FN(8, 4, 15)
+#undef LAT_FNS
+#undef LAT_FN
+                          }) {
       CU_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       set_max_dyn((const void*)fn);
     }
@@ -145,6 +149,7 @@ DeviceCaps& caps() {
                                 (int)sizeof(SchurWSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWCSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWCSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_wsc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -378,21 +383,60 @@ void launch_cluster(K kernel, const PanelCfg& g, size_t dyn, cudaStream_t s, Arg
   launch_clusters(kernel, g, 1, dyn, s, args...);
 }
 
-// The team engine (panel_team.cuh) for p <= team_max_p() columns: one column
-// per 8 threads, ceil(p / cols) CTAs in one cluster.  Opt-in
-// (PRRP_TEAM_MAXP=<largest p>): measured slower than the thread-per-column
-// engines in the CALU schedule (config 5: 1548 vs 1406 ms; config 4: 392 vs
-// 290 ms) -- ~3.9 us per pivot step at h = 128, p = 256 (ncu), the same as
-// panel2: the per-step chain of barriers and the serial reflector, not the
-// column arithmetic, bounds both.
-int64_t team_max_p() {
-  static const int64_t v = getenv("PRRP_TEAM_MAXP") ? atoll(getenv("PRRP_TEAM_MAXP")) : 0;
+// The latency engine (panel_lat.cuh): a team of 8 threads per column, CPT
+// columns per team, NWC compute warps (4 NWC teams) + one control warp per
+// CTA, ceil(p / (4 NWC CPT)) CTAs in one cluster.
+// PRRP_LAT=0 disables it (the thread-per-column engines run instead);
+// PRRP_LAT_MAXP caps the panel height it takes; PRRP_LAT_NWC / PRRP_LAT_CPT
+// force a shape (A/B measurements, tools/lat_sweep.py).
+int lat_nr(int h) { return h <= 32 ? 4 : h <= 64 ? 8 : 16; }
+bool lat_has(int nr, int nwc, int cpt) {
+  if (nwc == 7) return cpt == 1 || cpt == 2 || cpt == 4;
+  if (nwc == 15) return cpt == 1 || cpt == 2 || (cpt == 4 && nr <= 8);
+  return false;
+}
+int64_t lat_max_p() {
+  static const int64_t v = getenv("PRRP_LAT_MAXP") ? atoll(getenv("PRRP_LAT_MAXP")) : (int64_t)1 << 40;
+  static const bool on = !(getenv("PRRP_LAT") && atoi(getenv("PRRP_LAT")) == 0);
+  return on ? v : 0;
+}
+struct LatShape { int nwc = 0, cpt = 0, C = 0; };
+int lat_ctas(int64_t p, int nwc, int cpt) { return (int)std::max<int64_t>(1, (p + 4 * nwc * cpt - 1) / (4 * nwc * cpt)); }
+// Largest cluster the latency engine may use in the calls of this thread
+// (0: engine off).  A cluster needs that many free SMs in ONE GPC, which a
+// persistent trailing update beside it does not leave, so the CALU schedule
+// sets it per panel (see caluprrp_enqueue); PRRP_LAT_CMAX sets the default.
+int lat_default_cmax() {
+  static const int v = getenv("PRRP_LAT_CMAX") ? atoi(getenv("PRRP_LAT_CMAX")) : 16;
   return v;
 }
-
-int team_cols(int h) {
-  const int nr = (h + 7) / 8;
-  return (nr <= 4 ? PTCfg<4>::T : nr <= 8 ? PTCfg<8>::T : PTCfg<16>::T) / PT_G;
+thread_local int tl_lat_cmax = -1;   // -1: the default
+// shape for an h x p panel (nwc = 0: not eligible); force_* > 0 pin a choice.
+// Preference = measured order (tools/lat_sweep.py): few warps
+// per scheduler and one column per team first.
+LatShape lat_shape(int h, int64_t p, int force_nwc = 0, int force_cpt = 0, int cmax = -1) {
+  static const int env_nwc = getenv("PRRP_LAT_NWC") ? atoi(getenv("PRRP_LAT_NWC")) : 0;
+  static const int env_cpt = getenv("PRRP_LAT_CPT") ? atoi(getenv("PRRP_LAT_CPT")) : 0;
+  if (!force_nwc) force_nwc = env_nwc;
+  if (!force_cpt) force_cpt = env_cpt;
+  if (cmax < 0) cmax = tl_lat_cmax >= 0 ? tl_lat_cmax : lat_default_cmax();
+  const int nr = lat_nr(h);
+  const int maxc = std::min(caps().max_cluster, cmax);
+  LatShape best;
+  // whole 8-row blocks only (h = 32, 64, 128: every tournament node and panel
+  // of the BASELINE configs); other widths run the generic engine
+  if (h != 8 * nr) return best;
+  static const int pref[5][2] = {{7, 1}, {15, 1}, {7, 2}, {15, 2}, {7, 4}};
+  for (const auto& pc : pref) {
+    const int nwc = pc[0], cpt = pc[1];
+    if (force_nwc && nwc != force_nwc) continue;
+    if (force_cpt && cpt != force_cpt) continue;
+    if (!lat_has(nr, nwc, cpt)) continue;
+    const int C = lat_ctas(p, nwc, cpt);
+    if (C > maxc) continue;
+    return LatShape{nwc, cpt, C};
+  }
+  return best;
 }
 
 // The CALU final QR reuses the tournament root's QRCP (calu_root_qr_kernel);
@@ -403,19 +447,41 @@ bool reuse_root_qr() {
 }
 
 bool team_eligible(int h, int64_t p) {
-  return h >= 1 && h <= PRRP_MAXH && p >= 1 &&
-         p <= std::min<int64_t>(team_max_p(), (int64_t)team_cols(h) * caps().max_cluster);
+  if (!(h >= 1 && h <= PRRP_MAXH && p >= 1 && p <= lat_max_p())) return false;
+  return lat_shape(h, p).nwc != 0;
 }
 
-void launch_team(const PanelArgs& a, cudaStream_t s) {
+template <int NR, int CPT, int NWC>
+void launch_lat_as(const PanelArgs& a, PanelCfg g, cudaStream_t s) {
+  const size_t dyn = lat_smem<NR, NWC>();
+  g.T = 32 * (NWC + 1);
+  launch_cluster(panel_lat_kernel<NR, CPT, NWC, true>, g, dyn, s, a);   // h == 8 NR (lat_shape)
+}
+
+template <int NR>
+void launch_lat_nr(const PanelArgs& a, const PanelCfg& g, const LatShape& sh, cudaStream_t s) {
+  if (sh.nwc == 7) {
+    if (sh.cpt == 1) launch_lat_as<NR, 1, 7>(a, g, s);
+    else if (sh.cpt == 2) launch_lat_as<NR, 2, 7>(a, g, s);
+    else launch_lat_as<NR, 4, 7>(a, g, s);
+  } else {
+    if (sh.cpt == 1) launch_lat_as<NR, 1, 15>(a, g, s);
+    else if (sh.cpt == 2) launch_lat_as<NR, 2, 15>(a, g, s);
+    else if constexpr (NR <= 8) launch_lat_as<NR, 4, 15>(a, g, s);
+  }
+}
+
+void launch_team(const PanelArgs& a0, cudaStream_t s, int force_nwc = 0, int force_cpt = 0, int cmax = -1) {
+  const LatShape sh = lat_shape(a0.h, a0.p, force_nwc, force_cpt, cmax);
+  if (!sh.nwc) fail(PRRP_ERR_UNSUPPORTED, "no latency-engine shape for this panel");
   PanelCfg g{};
-  const int cols = team_cols(a.h);
-  g.C = (int)((a.p + cols - 1) / cols);
-  const int nr = (a.h + 7) / 8;
-  if (nr <= 4) { g.T = PTCfg<4>::T; launch_cluster(panel_team_kernel<4>, g, kPTSmem, s, a); }
-  else if (nr <= 8) { g.T = PTCfg<8>::T; launch_cluster(panel_team_kernel<8>, g, kPTSmem, s, a); }
-  else if (nr <= 12) { g.T = PTCfg<12>::T; launch_cluster(panel_team_kernel<12>, g, kPTSmem, s, a); }
-  else { g.T = PTCfg<16>::T; launch_cluster(panel_team_kernel<16>, g, kPTSmem, s, a); }
+  g.C = sh.C;
+  PanelArgs a = a0;
+  a.per = (a.p + sh.C - 1) / sh.C;
+  const int nr = lat_nr(a.h);
+  if (nr == 4) launch_lat_nr<4>(a, g, sh, s);
+  else if (nr == 8) launch_lat_nr<8>(a, g, sh, s);
+  else launch_lat_nr<16>(a, g, sh, s);
 }
 
 // GEPP of a b x b block (register kernel for b <= 64, shared-memory kernel above)
@@ -652,6 +718,12 @@ void launch_finalize(const PanelArgs& a, const PanelBuffers& B, int bsel, int64_
 }
 
 thread_local int tl_force_ws = -1;   // diagnostics: per-call kernel choice (PRRP_WS_W1 / PRRP_WS_W2)
+// > 0: the persistent K > 64 trailing update is launched as clusters of this
+// many CTAs (the kernel itself does not use cluster features).  A cluster is
+// placed inside one GPC, so with one cluster fewer than the GPU has GPCs a
+// whole GPC stays free for the tournament's own clusters beside the update
+// (caluprrp_enqueue, chain-bound panels).
+thread_local int tl_schur_cluster = 0;
 // CALU_PRRP enqueue: the warp-specialised kernel prefetches C (see DESIGN.md 4:
 // with the C read in the epilogue the graph-replayed CALU schedule gave
 // run-to-run different results; with the prefetch it is bit-stable)
@@ -709,7 +781,21 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
       else if (wsc_warps == 16)
         schur_wsc_kernel<16><<<grid, 17 * 32, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K,
                                                                          st);
-      else
+      else if (tl_schur_cluster > 1 && (int)grid >= tl_schur_cluster) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((grid / (unsigned)tl_schur_cluster) * (unsigned)tl_schur_cluster);
+        cfg.blockDim = dim3(SW_THREADS);
+        cfg.dynamicSmemBytes = sizeof(SchurWCSmem);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)tl_schur_cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CU_TRY(cudaLaunchKernelEx(&cfg, schur_wsc_kernel<8>, mapL, mapB, mapC, C, ldc, (int)M, (int)N, K, st));
+      } else
         schur_wsc_kernel<8><<<grid, SW_THREADS, sizeof(SchurWCSmem), s>>>(mapL, mapB, mapC, C, ldc, (int)M, (int)N, K,
                                                                           st);
     } else if (late_c && !tl_schur_prefetch_c)
@@ -860,10 +946,13 @@ DevState* new_state(Arena& ar, cudaStream_t s) {
   return st;
 }
 
+// > 0: CTA cap of the compose / block-row kernels (they run beside the next
+// panel's tournament in the CALU schedule and must not take its SMs)
+thread_local int tl_fin_ctas = 0;
 void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const double* D, const int32_t* gperm,
                       double* out, int64_t ldo, DevState* st, cudaStream_t s) {
   if (M <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 4, (M + TC - 1) / TC);
+  const unsigned grid = (unsigned)std::min<int64_t>(tl_fin_ctas > 0 ? tl_fin_ctas : caps().sms * 4, (M + TC - 1) / TC);
   const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
     case 1: compose_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(L21, ldl, M, b, D, gperm, out, ldo, st); break;
@@ -876,7 +965,7 @@ void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const do
 void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, const double* D, const int32_t* gperm,
                        int64_t* perm, DevState* st, cudaStream_t s, int64_t bl = 1, int nr = 1, int rk = 0) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(caps().sms * 4, (n + TC - 1) / TC);
+  const unsigned grid = (unsigned)std::min<int64_t>(tl_fin_ctas > 0 ? tl_fin_ctas : caps().sms * 4, (n + TC - 1) / TC);
   const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
     case 1: blockrow_w_kernel<1><<<grid, TW_WARPS * 32, dyn, s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk); break;
@@ -1310,6 +1399,24 @@ struct CaluOut {
 
 // Enqueue one CALU_PRRP factorization on stream s (capturable: no host
 // synchronisation, no pageable copies); buffers from `ar`.
+// "Panel pnl of an m x n CALU_PRRP with block b is chain-bound": its trailing
+// update is estimated shorter than PRRP_CALU_CB_MS (25 TFLOP/s), so the
+// tournament chain, not the update, bounds the panel (see caluprrp_enqueue).
+// The single-GPU and the distributed driver use the same rule, so every node
+// runs on the same engine in both (bit-identical results).
+int calu_leaf_cmax() {
+  static const int v = getenv("PRRP_CALU_LEAF_CMAX") ? atoi(getenv("PRRP_CALU_LEAF_CMAX")) : 8;
+  return v;
+}
+bool calu_chain_bound(int64_t m, int64_t n, int b, int pnl, bool flat) {
+  static const double cb_ms = getenv("PRRP_CALU_CB_MS") ? atof(getenv("PRRP_CALU_CB_MS")) : 2.0;
+  if (!(b > 64 && !flat && caps().max_cluster >= 16 && lat_default_cmax() > 0)) return false;
+  const int64_t c0 = (int64_t)pnl * b;
+  if (c0 + b >= n) return true;
+  const double fl = 2.0 * b * (double)(m - c0 - b) * (double)(n - c0 - b);
+  return fl / 25e12 * 1e3 < cb_ms;
+}
+
 void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
                       cudaStream_t s, Arena& ar, CaluOut& out) {
   static const bool calu_late_c = getenv("PRRP_CALU_LATE_C") && atoi(getenv("PRRP_CALU_LATE_C")) != 0;
@@ -1440,9 +1547,14 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       nbuf.live = leaves ? nullptr : live_all + i;
       nbuf.want = want_all + i;
       nbuf.node_rows = node_rows + (size_t)panel * maxnodes;
+      // the leaves of a level run side by side: clusters of at most
+      // calu_leaf_cmax() CTAs, so that all of them are resident at once
+      const int cmax_level = tl_lat_cmax;
+      if (leaves && tl_lat_cmax > 0) tl_lat_cmax = std::min(tl_lat_cmax, calu_leaf_cmax());
       strong_rrqr_panel(A + col0, lda, bj, cnt[i], bj, tau, panel, nodes[i].L21, nodes[i].ldl, nbuf, st,
                         node_swaps + (size_t)panel * maxnodes, nullptr, nullptr, nullptr, false, ns, ridx,
                         slot0 + i, level, i, qe);
+      tl_lat_cmax = cmax_level;
     }
     // join
     for (int i = 0; i < nn; ++i) {
@@ -1512,12 +1624,29 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
     CU_TRY(cudaEventRecord(e, sm));
     flush_side(e);
   };
+  // Two regimes.  While a panel's trailing update (W2) outlasts the
+  // tournament chain the update is the bottleneck: it runs on all but 8 SMs
+  // and the tournament's small nodes run as single CTAs on the rest.  Once
+  // the chain is the bottleneck (estimated W2 time below PRRP_CALU_CB_MS),
+  // W2 is launched as PRRP_CALU_W2_CLUSTERS clusters of 16 CTAs -- clusters
+  // are placed inside one GPC, so one GPC stays free -- and the tournament
+  // nodes run on the latency engine with clusters of up to 16 CTAs there;
+  // (PRRP_CALU_CB_FIN caps the compose / block-row kernels of the fin stream;
+  // measured slower -- the next-but-one panel waits for them -- so off.)
+  static const int w2_clusters = getenv("PRRP_CALU_W2_CLUSTERS") ? atoi(getenv("PRRP_CALU_W2_CLUSTERS")) : 7;
+  static const int cb_fin_ctas = getenv("PRRP_CALU_CB_FIN") ? atoi(getenv("PRRP_CALU_CB_FIN")) : 0;
+  auto chain_bound = [&](int pnl) { return calu_chain_bound(m, n, b, pnl, flat); };
+  struct LatScope {      // the thread's latency-engine setting is restored on every exit path
+    ~LatScope() { tl_lat_cmax = -1; tl_fin_ctas = 0; tl_schur_cluster = 0; }
+  } lat_scope;
   int panel = 0;
   for (int64_t col0 = 0; col0 < n; col0 += b, ++panel) {
     const int bj = (int)std::min<int64_t>(b, n - col0);
     const int64_t rows = m - col0;
     const int64_t width = n - col0 - bj;
     const int par = panel & 1;
+    tl_lat_cmax = chain_bound(panel) ? 16 : 0;
+    tl_fin_ctas = chain_bound(panel + 1) ? cb_fin_ctas : 0;
     double* blk = A + col0 * lda + col0;
     double* Lg = Llogb[par];
     double* Lp = Lphysb[par];
@@ -1577,9 +1706,16 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                                                 log2phys, st, panel);
         tend(sm);
       } else if (p_eff == 1) {
-        // single node: the selector's own full order and l_block (tournament.py:168-177)
-        strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Lg, ldl, Bk, st, swaps_dev, nullptr, nullptr,
-                          nullptr, false, sm, pos2row + col0);
+        // single node: the selector's own full order and l_block (tournament.py:168-177);
+        // it IS the LU_PRRP panel, so it runs with LU_PRRP's engine setting
+        // (bitwise equal factors, test_caluprrp_single_leaf_equals_luprrp)
+        {
+          const int keep = tl_lat_cmax;
+          tl_lat_cmax = -1;
+          strong_rrqr_panel(A + col0, lda, bj, rows, bj, tau, panel, Lg, ldl, Bk, st, swaps_dev, nullptr, nullptr,
+                            nullptr, false, sm, pos2row + col0);
+          tl_lat_cmax = keep;
+        }
         flush_after_main();
         tbegin(PRRP_K_OTHER, sm);
         calu_reorder_kernel<<<1, 1024, 0, sm>>>(nullptr, nullptr, Bk.perm, 1, bj, rows, col0, pos2row, scratch, mv,
@@ -1687,7 +1823,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         tbegin(PRRP_K_FINALIZE, sm);
         iota32_kernel<<<1, 128, 0, sm>>>(perm_small, bj);
         if (reuse_root_qr()) {
-          calu_root_qr_kernel<<<1, 256, 0, sm>>>(live_all, bj, nodes[0].B.Rbuf, root_p, nodes[0].B.refl, Rsmall, refl,
+          calu_root_qr_kernel<<<16, 256, 0, sm>>>(live_all, bj, nodes[0].B.Rbuf, root_p, nodes[0].B.refl, Rsmall, refl,
                                                  final_live, st);
           qa.live = final_live;   // the engine below runs only when the root passed its members through
         }
@@ -1717,7 +1853,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         } else {
           launch_cluster(panel_qrcp_kernel, gq, gq.dyn_engine, sm, qa);
         }
-        calu_copy_r11_kernel<<<1, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
+        calu_copy_r11_kernel<<<16, 256, 0, sm>>>(Rsmall, bj, B.Rbuf, rows);
         static const int r12_min_b = getenv("PRRP_CALU_R12_MIN_B") ? atoi(getenv("PRRP_CALU_R12_MIN_B")) : 65;
         if (calu_r12_gemm && bj >= r12_min_b && (bj % 2 == 0)) {
           // R12 = Q^T A21^T on the DMMA pipe: Q from the reflector log, A21's
@@ -1727,7 +1863,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
           const int64_t ncol = rows - bj;
           tend(sm);
           tbegin(PRRP_K_OTHER, sm);
-          calu_form_negqt_kernel<<<1, 256, (size_t)bj * (bj + 1) * 8, sm>>>(refl, bj, Qneg);
+          calu_form_negqt_kernel<<<(bj + 15) / 16, 128, (size_t)bj * (bj + 1) * 8, sm>>>(refl, bj, Qneg);
           tend(sm);
           tbegin(PRRP_K_PERMUTE, sm);
           calu_gather_t_kernel<<<(unsigned)((ncol + 31) / 32), 256, (size_t)bj * 33 * 8, sm>>>(
@@ -1841,8 +1977,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         {
           static const int fw2 = getenv("PRRP_WS_W2") ? atoi(getenv("PRRP_WS_W2")) : -1;
           tl_force_ws = fw2;
+          const bool cb = chain_bound(panel + 1);   // it runs beside panel + 1's merge levels
+          tl_schur_cluster = cb ? 16 : 0;
           schur_update(A + (col0 + bj) * lda + cw0 + w1, lda, Lp, ldl, a12 + wn + w1, lda12, rows - bj,
-                       n - cw0 - w1, bj, st, sd, calu_wide_ctas, calu_wide_q, w2_stream);
+                       n - cw0 - w1, bj, st, sd, cb ? 16 * w2_clusters : calu_wide_ctas, calu_wide_q, w2_stream);
+          tl_schur_cluster = 0;
           tl_force_ws = -1;
         }
         side_done = ss.ev(evi++);
@@ -2452,6 +2591,81 @@ int prrp_caluprrp(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, doubl
 }
 
 int64_t prrp_b200_graph_kernels(void) { return tl_last_graph_kernels; }
+
+// Diagnostics: average device time of the panel QRCP engine alone on an
+// h x p transposed panel (rows of `a`), `reps` launches between CUDA events.
+// nwc/cpt > 0 force a latency-engine shape; nwc < 0 runs the thread-per-
+// column engines (h = 64 or 128 only).
+int prrp_b200_qrcp_time(const double* a, int64_t lda, int32_t h, int64_t p, int32_t nwc, int32_t cpt, int32_t reps,
+                        double* ms_out, int32_t* ctas_out, prrp_err* err) {
+  clear_err(err);
+  try {
+    cudaStream_t s = 0;
+    if (h < 1 || h > PRRP_MAXH || p < 1 || reps < 1) fail(PRRP_ERR_ARG, "bad probe arguments");
+    caps();
+    Arena ar(s);
+    DevState* st = new_state(ar, s);
+    PanelArgs pa{};
+    pa.src = a;
+    pa.ld = lda;
+    pa.h = h;
+    pa.p = p;
+    pa.bsel = h;
+    pa.steps = (int)std::min<int64_t>(h, p);
+    pa.mode = 0;
+    pa.perm = ar.get<int32_t>(p);
+    pa.Rbuf = ar.get<double>((size_t)h * p);
+    pa.ovf = ar.get<double>(ovf_elems(h, p, h));
+    pa.st = st;
+    pa.fro = &st->fro;
+    pa.tree_level = pa.tree_index = -1;
+    pa.fused_ak = 1;
+    cudaEvent_t e0, e1;
+    CU_TRY(cudaEventCreate(&e0));
+    CU_TRY(cudaEventCreate(&e1));
+    int ctas = 0;
+    for (int r = -1; r < reps; ++r) {
+      if (r == 0) CU_TRY(cudaEventRecord(e0, s));
+      if (nwc >= 0) {
+        const LatShape sh = lat_shape(h, p, nwc, cpt, 16);
+        if (!sh.nwc) fail(PRRP_ERR_UNSUPPORTED, "no such latency-engine shape");
+        ctas = sh.C;
+        launch_team(pa, s, nwc, cpt, 16);
+      } else if (h == P1_H) {
+        PanelCfg g1{};
+        g1.C = (int)std::max<int64_t>(1, (p + 255) / 256);
+        g1.T = P1_T;
+        PanelArgs a1 = pa;
+        a1.per = (p + g1.C - 1) / g1.C;
+        ctas = g1.C;
+        launch_cluster(panel_qrcp1_kernel, g1, a1.per > P1_T ? (size_t)P1_H * P1_T * 8 : 0, s, a1);
+      } else if (h == P2_H) {
+        PanelCfg g2{};
+        g2.C = (int)std::max<int64_t>(1, (p + P2_T - 1) / P2_T);
+        g2.T = P2_T;
+        PanelArgs a2 = pa;
+        a2.per = (p + g2.C - 1) / g2.C;
+        ctas = g2.C;
+        launch_cluster(panel_qrcp2_kernel, g2, (size_t)(P2_H - P2_W) * P2_T * 8, s, a2);
+      } else {
+        fail(PRRP_ERR_UNSUPPORTED, "thread-per-column engines need h = 64 or 128");
+      }
+    }
+    CU_TRY(cudaEventRecord(e1, s));
+    CU_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms_out) *ms_out = (double)ms / reps;
+    if (ctas_out) *ctas_out = ctas;
+    DevState hs;
+    read_state(st, hs, s);
+    return state_to_err(hs, err);
+  } catch (const Fail& f) {
+    return report(err, f);
+  }
+}
 
 int prrp_caluprrp_timed(double* A, int64_t lda, int64_t m, int64_t n, int32_t b, double tau, int32_t leaf_count,
                         int64_t* perm, int32_t* swap_counts, int64_t* tournament_charge3, prrp_stats* stats,
