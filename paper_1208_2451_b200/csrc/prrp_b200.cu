@@ -1611,19 +1611,32 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   // on all but 8 SMs, beside the rest of the tournament chain
   // (PRRP_CALU_DEFER=0: enqueue at once).
   static const int calu_defer = getenv("PRRP_CALU_DEFER") ? atoi(getenv("PRRP_CALU_DEFER")) : 1;
-  std::function<void()> pending_side;
+  std::function<void()> pending_side, pending_fin;
   auto flush_side = [&](cudaEvent_t after) {
+    if (pending_fin) {
+      if (after) CU_TRY(cudaStreamWaitEvent(sf, after, 0));
+      pending_fin();
+      pending_fin = nullptr;
+    }
     if (!pending_side) return;
     if (after) CU_TRY(cudaStreamWaitEvent(sd, after, 0));
     pending_side();
     pending_side = nullptr;
   };
   auto flush_after_main = [&]() {
-    if (!pending_side) return;
+    if (!pending_side && !pending_fin) return;
     cudaEvent_t e = ss.ev(evi++);
     CU_TRY(cudaEventRecord(e, sm));
     flush_side(e);
   };
+  // Update-bound panels: the leaf level of panel k+1 is the one part of the
+  // chain the trailing update cannot overlap (its clusters need the whole
+  // GPU).  PRRP_CALU_SB_SERIAL keeps other work away from it: bit 0 makes
+  // main wait for W1(k) before the leaves, bit 1 enqueues panel k's
+  // fin-stream work (GEPP, compose, block row) after them like W2(k).  Both
+  // were measured SLOWER at config 5 (1315 and 1447 ms against 1291: the
+  // deferred work then competes with the chain for the 8 spare SMs), so off.
+  static const int sb_serial = getenv("PRRP_CALU_SB_SERIAL") ? atoi(getenv("PRRP_CALU_SB_SERIAL")) : 0;
   // Two regimes.  While a panel's trailing update (W2) outlasts the
   // tournament chain the update is the bottleneck: it runs on all but 8 SMs
   // and the tournament's small nodes run as single CTAs on the rest.  Once
@@ -1663,6 +1676,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaStreamWaitEvent(sm, side_ev[panel - 2], 0));
         CU_TRY(cudaStreamWaitEvent(sm, fin_ev[panel - 2], 0));
       }
+      if ((sb_serial & 1) && calu_defer && b > 64 && !chain_bound(panel) && w1_prev) CU_TRY(cudaStreamWaitEvent(sm, w1_prev, 0));
       const int64_t first = std::min<int64_t>(rows, 2 * bj);
       const int64_t p_eff = flat ? 1 + (rows - first + bj - 1) / bj
                                  : std::max<int64_t>(1, std::min<int64_t>(P, rows / (bj + 1)));
@@ -1927,17 +1941,30 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                      bj, st, sm, calu_narrow_ctas, calu_wide_q);
       cudaEvent_t ev_narrow = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_narrow, sm));
-      // fin: L-part row moves + row order, GEPP, compose
-      CU_TRY(cudaStreamWaitEvent(sf, ev_narrow, 0));
-      tbegin(PRRP_K_PERMUTE, sf);
-      permute_cols(0, col0, col0, mv, mc, perm, panel, sf);
-      tend(sf);
-      tbegin(PRRP_K_GEPP, sf);
-      launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sf);
-      tend(sf);
-      tbegin(PRRP_K_COMPOSE, sf);
-      launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf);
-      tend(sf);
+      // fin: L-part row moves + row order, GEPP, compose, then (after every
+      // row move of this panel and the pivot-row copy; side's permute also
+      // orders it after the previous trailing update) the block row
+      fin_ev[panel] = ss.ev(evi++);
+      cudaEvent_t fin_done = fin_ev[panel];
+      cudaEvent_t ev_copy = ss.ev(evi++);
+      pending_fin = [=]() {
+        CU_TRY(cudaStreamWaitEvent(sf, ev_narrow, 0));
+        tbegin(PRRP_K_PERMUTE, sf);
+        permute_cols(0, col0, col0, mv, mc, perm, panel, sf);
+        tend(sf);
+        tbegin(PRRP_K_GEPP, sf);
+        launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sf);
+        tend(sf);
+        tbegin(PRRP_K_COMPOSE, sf);
+        launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf);
+        tend(sf);
+        CU_TRY(cudaStreamWaitEvent(sf, ev_copy, 0));
+        tbegin(PRRP_K_BLOCKROW, sf);
+        launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sf);
+        tend(sf);
+        CU_TRY(cudaGetLastError());
+        CU_TRY(cudaEventRecord(fin_done, sf));
+      };
       // side: trailing row moves + copy of their pivot-row part, trailing
       // update (next narrow region first)
       CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
@@ -1948,17 +1975,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         CU_TRY(cudaMemcpy2DAsync(a12 + wn, (size_t)lda12 * 8, A + col0 * lda + cw0, (size_t)lda * 8,
                                  (size_t)(n - cw0) * 8, (size_t)bj, cudaMemcpyDeviceToDevice, sd));
       tend(sd);
-      cudaEvent_t ev_copy = ss.ev(evi++);
       CU_TRY(cudaEventRecord(ev_copy, sd));
-      // fin: the block row (after every row move of this panel and the copy;
-      // side's permute also orders it after the previous trailing update)
-      CU_TRY(cudaStreamWaitEvent(sf, ev_copy, 0));
-      tbegin(PRRP_K_BLOCKROW, sf);
-      launch_blockrow_w(A, lda, col0, bj, n, Dk, gpk, perm, st, sf);
-      tend(sf);
-      CU_TRY(cudaGetLastError());
-      fin_ev[panel] = ss.ev(evi++);
-      CU_TRY(cudaEventRecord(fin_ev[panel], sf));
+      if (!((sb_serial & 2) && calu_defer && b > 64 && !chain_bound(panel + 1))) {
+        pending_fin();
+        pending_fin = nullptr;
+      }
       const int64_t w1 = std::min<int64_t>(n - cw0, b);
       if (w1 > 0)
       {
