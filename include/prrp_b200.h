@@ -143,9 +143,12 @@ int64_t prrp_b200_graph_kernels(void);
  * launches between CUDA events.  nwc / cpt > 0 force a latency-engine shape
  * (compute warps per CTA, columns per 8-thread team), 0 = the default
  * choice; nwc < 0 runs the thread-per-column engines (h = 64 or 128).
- * ctas_out = cluster size used. */
+ * ctas_out = cluster size used.  R_out (device, column-major h x p: R by
+ * position) and perm_out (device, p column indices) optionally return the
+ * last launch's result (both or neither), so every engine shape can be
+ * checked against the oracle. */
 int prrp_b200_qrcp_time(const double* a, int64_t lda, int32_t h, int64_t p, int32_t nwc, int32_t cpt, int32_t reps,
-                        double* ms_out, int32_t* ctas_out, prrp_err* err);
+                        double* ms_out, int32_t* ctas_out, double* R_out, int64_t* perm_out, prrp_err* err);
 
 /* prrp_caluprrp through the direct (uncaptured) enqueue with every launch
  * timed by CUDA events on its stream (per kernel class, as

@@ -56,7 +56,7 @@ SIGNATURES = {
     "prrp_b200_dmma_peak": ([_D, _P, _P], ctypes.c_int),
     "prrp_caluprrp": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_b200_graph_kernels": ([], ctypes.c_int64),
-    "prrp_b200_qrcp_time": ([_P, _I64, _I32, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "prrp_b200_qrcp_time": ([_P, _I64, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_caluprrp_timed": ([_P, _I64, _I64, _I64, _I32, _D, _I32, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_strong_rrqr": ([_P, _I64, _I32, _I64, _I32, _D, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "prrp_householder_qr": ([_P, _I64, _I32, _I64, _P, _P, _P, _P], ctypes.c_int),

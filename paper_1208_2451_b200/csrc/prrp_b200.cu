@@ -1600,7 +1600,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                           int64_t* pp, int pnl, cudaStream_t q) {
     if (c_hi <= c_lo && !pp) return;
     const int64_t nc = std::max<int64_t>(c_hi - c_lo, 1);
-    const unsigned grid = (unsigned)std::min<int64_t>((nc + 31) / 32, 2 * sms);
+    static const int perm_ctas = getenv("PRRP_CALU_PERM_CTAS") ? atoi(getenv("PRRP_CALU_PERM_CTAS")) : 0;
+    const unsigned grid = (unsigned)std::min<int64_t>((nc + 31) / 32, perm_ctas > 0 ? perm_ctas : 2 * sms);
     permute_cols_kernel<<<grid, 256, 0, q>>>(A, lda, row0, c_lo, std::max(c_lo, c_hi), mv, mc, pp, st, pnl);
     CU_TRY(cudaGetLastError());
   };
@@ -1985,8 +1986,9 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       {
         static const int fw1 = getenv("PRRP_WS_W1") ? atoi(getenv("PRRP_WS_W1")) : -1;
         tl_force_ws = fw1;
+        static const int w1_ctas = getenv("PRRP_CALU_W1_CTAS") ? atoi(getenv("PRRP_CALU_W1_CTAS")) : 0;
         schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, a12 + wn, lda12, rows - bj, w1, bj, st, sd,
-                     calu_wide_ctas, calu_wide_q);
+                     w1_ctas > 0 ? w1_ctas : calu_wide_ctas, calu_wide_q);
         tl_force_ws = -1;
       }
       w1_prev = ss.ev(evi++);
@@ -2618,7 +2620,7 @@ int64_t prrp_b200_graph_kernels(void) { return tl_last_graph_kernels; }
 // nwc/cpt > 0 force a latency-engine shape; nwc < 0 runs the thread-per-
 // column engines (h = 64 or 128 only).
 int prrp_b200_qrcp_time(const double* a, int64_t lda, int32_t h, int64_t p, int32_t nwc, int32_t cpt, int32_t reps,
-                        double* ms_out, int32_t* ctas_out, prrp_err* err) {
+                        double* ms_out, int32_t* ctas_out, double* R_out, int64_t* perm_out, prrp_err* err) {
   clear_err(err);
   try {
     cudaStream_t s = 0;
@@ -2680,6 +2682,10 @@ int prrp_b200_qrcp_time(const double* a, int64_t lda, int32_t h, int64_t p, int3
     cudaEventDestroy(e1);
     if (ms_out) *ms_out = (double)ms / reps;
     if (ctas_out) *ctas_out = ctas;
+    if (R_out && perm_out) {
+      r_out_kernel<<<caps().sms, 256, 0, s>>>(pa.Rbuf, h, p, pa.perm, R_out, perm_out);
+      CU_TRY(cudaGetLastError());
+    }
     DevState hs;
     read_state(st, hs, s);
     return state_to_err(hs, err);
@@ -2777,7 +2783,8 @@ int prrp_householder_qr(const double* a, int64_t lda, int32_t h, int64_t p, doub
     pa.cap_pad = g.cap_pad;
     pa.ovpad = g.ovpad;
     pa.st = st;
-    launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
+    if (team_eligible(h, p) && !force_generic_panel()) launch_team(pa, s);
+    else launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
     int64_t* dummy_perm = ar.get<int64_t>(p);
     r_out_kernel<<<caps().sms, 256, 0, s>>>(Rbuf, h, p, permb, R, dummy_perm);
     form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(refl, h, steps, Q);
@@ -2827,7 +2834,8 @@ int prrp_qrcp(const double* a, int64_t lda, int32_t h, int64_t p, double* R, dou
     pa.st = st;
     pa.fro = &st->fro;
     pa.tree_level = pa.tree_index = -1;
-    launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
+    if (team_eligible(h, p) && !force_generic_panel()) launch_team(pa, s);
+    else launch_cluster(panel_qrcp_kernel, g, g.dyn_engine, s, pa);
     r_out_kernel<<<caps().sms, 256, 0, s>>>(Rbuf, h, p, permb, R, perm);
     form_q_kernel<<<1, 256, (size_t)h * h * 8, s>>>(refl, h, steps, Q);
     CU_TRY(cudaGetLastError());

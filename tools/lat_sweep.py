@@ -23,7 +23,7 @@ def main():
             ms, ct = ctypes.c_double(), ctypes.c_int32()
             err = _lib.PrrpErr()
             rc = lib.prrp_b200_qrcp_time(ctypes.c_void_p(a.data_ptr()), h, h, p, nwc, cpt, 5, ctypes.byref(ms),
-                                         ctypes.byref(ct), ctypes.byref(err))
+                                         ctypes.byref(ct), None, None, ctypes.byref(err))
             if rc != 0:
                 out.append(f"({nwc},{cpt}): -")
                 continue
