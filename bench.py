@@ -43,6 +43,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# before any CUDA context exists (see paper_1208_2451_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "CALU_PRRP factorization GFLOP/s (2n^3/3), BASELINE config 5"
 UNIT = "GFLOP/s"
