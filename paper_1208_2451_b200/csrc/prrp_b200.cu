@@ -661,7 +661,13 @@ void strong_rrqr_panel(const double* src, int64_t ld, int h, int64_t p, int bsel
       return;
     }
     if (bsel <= 64 || use_trsm_c2()) {
-      const int64_t cpb = TC_COLS;
+      // b > 64: a CTA stages the 133 KB R11 before it solves anything, and the
+      // eight leaves of a tournament level launch their solves together (992
+      // CTAs at 4096-row leaves).  PRRP_TRSM_GROUPS = g gives a CTA g column
+      // groups on tall panels; measured no different at config 5 (1293-1299
+      // ms for g = 1, 2, 4, 8), so 1.
+      static const int tg = getenv("PRRP_TRSM_GROUPS") ? atoi(getenv("PRRP_TRSM_GROUPS")) : 1;
+      const int64_t cpb = (bsel > 64 && ncol >= 1024) ? (int64_t)std::max(1, tg) * TC_COLS : TC_COLS;
       const int nbv = (int)std::min<int64_t>(kMaxCand, (ncol + cpb - 1) / cpb);
       if (bsel <= 64)
         trsm_c_kernel<<<nbv, TC_T, 0, s>>>(B.Rbuf, p, bsel, L21, ldl, B.cand, B.cand_flat, st, panel, a.fro, tl, ti,
@@ -1987,8 +1993,9 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         static const int fw1 = getenv("PRRP_WS_W1") ? atoi(getenv("PRRP_WS_W1")) : -1;
         tl_force_ws = fw1;
         static const int w1_ctas = getenv("PRRP_CALU_W1_CTAS") ? atoi(getenv("PRRP_CALU_W1_CTAS")) : 0;
+        // PRRP_CALU_W1_CTAS < 0: the classic one-tile-per-CTA kernel (short CTAs)
         schur_update(A + (col0 + bj) * lda + cw0, lda, Lp, ldl, a12 + wn, lda12, rows - bj, w1, bj, st, sd,
-                     w1_ctas > 0 ? w1_ctas : calu_wide_ctas, calu_wide_q);
+                     w1_ctas > 0 ? w1_ctas : (w1_ctas < 0 ? 0 : calu_wide_ctas), w1_ctas < 0 ? 0 : calu_wide_q);
         tl_force_ws = -1;
       }
       w1_prev = ss.ev(evi++);

@@ -24,9 +24,9 @@ def main():
     a = matgen.gen_urand(n, 42, order="C") if args.urand else matgen.gen_randn(n, 42, order="C")
     lda = n + (n & 1)
     buf = torch.empty((n, lda), dtype=torch.float64, device="cuda")
+    perm = torch.empty(n, dtype=torch.int64, device="cuda")   # one buffer: rep 0 direct, rep 1 capture, then replays
     for r in range(args.reps):
         buf[:, :n].copy_(torch.from_numpy(a))
-        perm = torch.empty(n, dtype=torch.int64, device="cuda")
         npan = (n + b - 1) // b
         sw = (ctypes.c_int32 * npan)()
         chg = (ctypes.c_int64 * npan)()
