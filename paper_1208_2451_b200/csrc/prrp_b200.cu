@@ -143,6 +143,7 @@ DeviceCaps& caps() {
       set_max_dyn((const void*)fn);
     CU_TRY(cudaFuncSetAttribute(schur_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SchurPSmem)));
+    CU_TRY(cudaFuncSetAttribute(schur_persist_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(SchurWSmem)));
     CU_TRY(cudaFuncSetAttribute(schur_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -819,6 +820,21 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     const int vec_ok = ((uintptr_t)C % 16 == 0) && (ldc % 2 == 0);
     const int64_t tiles = ((M + SCH_BM - 1) / SCH_BM) * ((N + SCH_BN - 1) / SCH_BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, max_ctas);
+    if (tl_schur_cluster > 1 && (int)grid >= tl_schur_cluster) {   // GPC-sized clusters (see tl_schur_cluster)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((grid / (unsigned)tl_schur_cluster) * (unsigned)tl_schur_cluster);
+      cfg.blockDim = dim3(SCH_THREADS);
+      cfg.dynamicSmemBytes = sizeof(SchurPSmem);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)tl_schur_cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CU_TRY(cudaLaunchKernelEx(&cfg, schur_persist_kernel, mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st));
+    } else
     schur_persist_kernel<<<grid, SCH_THREADS, sizeof(SchurPSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok,
                                                                         st);
   } else if (tma_ok) {
@@ -1415,12 +1431,16 @@ int calu_leaf_cmax() {
   return v;
 }
 bool calu_chain_bound(int64_t m, int64_t n, int b, int pnl, bool flat) {
+  // thresholds ~ the chain time of a panel: ~2 ms at b = 128, ~0.8 ms at b = 64
   static const double cb_ms = getenv("PRRP_CALU_CB_MS") ? atof(getenv("PRRP_CALU_CB_MS")) : 2.0;
-  if (!(b > 64 && !flat && caps().max_cluster >= 16 && lat_default_cmax() > 0)) return false;
+  static const double cb_ms64 = getenv("PRRP_CALU_CB_MS64") ? atof(getenv("PRRP_CALU_CB_MS64")) : 0.6;
+  const double thr = b > 64 ? cb_ms : cb_ms64;
+  if (!(thr > 0.0 && (b == 64 || b == 128 || b == 32) && !flat && caps().max_cluster >= 16 && lat_default_cmax() > 0))
+    return false;
   const int64_t c0 = (int64_t)pnl * b;
   if (c0 + b >= n) return true;
   const double fl = 2.0 * b * (double)(m - c0 - b) * (double)(n - c0 - b);
-  return fl / 25e12 * 1e3 < cb_ms;
+  return fl / (b > 64 ? 25e12 : 18e12) * 1e3 < thr;
 }
 
 void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
