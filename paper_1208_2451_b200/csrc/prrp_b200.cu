@@ -89,6 +89,7 @@ struct DeviceCaps {
   std::atomic<unsigned> sched_next{0};
   int sms = 0;
   int max_cluster = 8;
+  int schur_clusters16 = 8;    // 16-CTA clusters of the persistent trailing update the GPU holds at once (~ its GPCs)
 };
 
 // opt in to all the dynamic shared memory the kernel's static footprint leaves
@@ -173,6 +174,27 @@ DeviceCaps& caps() {
         c.max_cluster = cs;
         break;
       }
+      cudaGetLastError();
+    }
+    {
+      // how many 16-CTA clusters of the trailing update fit at once (one per
+      // GPC with >= 16 SMs): the chain-bound CALU regime launches one fewer,
+      // so that a GPC stays free for the tournament's clusters
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16 * 64);
+      cfg.blockDim = dim3(SW_THREADS);
+      cfg.dynamicSmemBytes = sizeof(SchurWCSmem);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (c.max_cluster >= 16 &&
+          cudaOccupancyMaxActiveClusters(&ncl, (void*)schur_wsc_kernel<8>, &cfg) == cudaSuccess && ncl > 0)
+        c.schur_clusters16 = ncl;
       cudaGetLastError();
     }
     // the per-call workspaces come from the stream-ordered pool: keep freed
@@ -1435,7 +1457,8 @@ bool calu_chain_bound(int64_t m, int64_t n, int b, int pnl, bool flat) {
   static const double cb_ms = getenv("PRRP_CALU_CB_MS") ? atof(getenv("PRRP_CALU_CB_MS")) : 2.0;
   static const double cb_ms64 = getenv("PRRP_CALU_CB_MS64") ? atof(getenv("PRRP_CALU_CB_MS64")) : 0.6;
   const double thr = b > 64 ? cb_ms : cb_ms64;
-  if (!(thr > 0.0 && (b == 64 || b == 128 || b == 32) && !flat && caps().max_cluster >= 16 && lat_default_cmax() > 0))
+  if (!(thr > 0.0 && (b == 64 || b == 128 || b == 32) && !flat && caps().max_cluster >= 16 &&
+        caps().schur_clusters16 >= 2 && lat_default_cmax() > 0))
     return false;
   const int64_t c0 = (int64_t)pnl * b;
   if (c0 + b >= n) return true;
@@ -1673,7 +1696,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   // nodes run on the latency engine with clusters of up to 16 CTAs there;
   // (PRRP_CALU_CB_FIN caps the compose / block-row kernels of the fin stream;
   // measured slower -- the next-but-one panel waits for them -- so off.)
-  static const int w2_clusters = getenv("PRRP_CALU_W2_CLUSTERS") ? atoi(getenv("PRRP_CALU_W2_CLUSTERS")) : 7;
+  static const int w2_clusters = getenv("PRRP_CALU_W2_CLUSTERS") ? atoi(getenv("PRRP_CALU_W2_CLUSTERS"))
+                                                                 : std::max(1, caps().schur_clusters16 - 1);
   static const int cb_fin_ctas = getenv("PRRP_CALU_CB_FIN") ? atoi(getenv("PRRP_CALU_CB_FIN")) : 0;
   auto chain_bound = [&](int pnl) { return calu_chain_bound(m, n, b, pnl, flat); };
   struct LatScope {      // the thread's latency-engine setting is restored on every exit path
