@@ -264,6 +264,30 @@ def attach_traffic(roof, name):
     return roof
 
 
+def hbm_kernels():
+    """ncu evidence for the HBM / latency-bound kernels of the path (north_star:
+    HBM GB/s of the panel and permutation kernels), read from the committed
+    summaries; the HBM peak is MEASURED_PEAKS.json's copy bandwidth."""
+    peak = 6454.6
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    out = {"hbm_peak_gbs": peak}
+    for key, name in (("permute_cols_kernel", "ncu_permute_cols_r02.json"),
+                      ("panel_lat_kernel 128x256", "ncu_lat_128x256_r02.json"),
+                      ("panel_qrcp1_kernel (config 2)", "ncu_qrcp1_c2b64_r02.json")):
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", name)))
+            gbs = d.get("dram_gbs")
+            out[key] = {"dram_gbs": gbs, "frac_of_hbm_peak": gbs / peak if gbs else None,
+                        "time_us": (d.get("time_s") or 0) * 1e6, "bound": "hbm" if key.startswith("permute") else
+                        "latency (dependent pivot steps)", "source": "profiles/" + name}
+        except Exception:
+            continue
+    return out
+
+
 def run_device(args):
     import torch
     ws, rank, local = dist_info()
@@ -356,6 +380,7 @@ def run_device(args):
             tms.append(tm)
         roofline = attach_traffic(roofline_from_timing(tms, peak, "config 5 CALU_PRRP"), "ncu_schur_c5_r02.json")
         extra["timed_run_launches_per_step"] = int(sum(tms[-1].launches))
+        extra["hbm_kernels (ncu --set full, profiles/)"] = hbm_kernels()
     del pristine, work
     torch.cuda.empty_cache()
 
