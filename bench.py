@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--cpu-panels", type=int, default=1, help="panels in the bounded CPU sample")
+    ap.add_argument("--cpu-panels", type=int, default=1, help="panels per stratum of the bounded CPU sample")
+    ap.add_argument("--cpu-strata", type=int, default=3, help="depths of the factorization the CPU sample covers")
     return ap.parse_args()
 
 
@@ -105,8 +106,13 @@ def workload(args, ws):
 
 # ------------------------------------------------------------------ reference arm
 def cpu_sample(args, a_cols=None):
-    """The oracle on the first `cpu_panels` panels of config 5 restricted to the
-    columns they touch; returns (seconds, flops, description)."""
+    """The oracle on a bounded, STRATIFIED sample of config 5: one panel (its
+    tournament, L21, block-row finish and the update of the next panel's
+    columns) at three depths of the factorization -- panel 0 on the real
+    first 2b columns, and panels at 1/3 and 2/3 of the way on U(-1,1)
+    stand-ins of the trailing matrix at that depth (same shape and entry
+    family; the cost does not depend on the values).  Returns (seconds,
+    flops, description)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
     from oracle import prrp_oracle as orc
     from paper_1208_2451_b200 import matgen
@@ -114,17 +120,31 @@ def cpu_sample(args, a_cols=None):
     w = (k + 1) * args.b
     if a_cols is None:
         a_cols = matgen.gen_urand_cols(args.n, args.seed, w)
-    t0 = time.perf_counter()
-    orc.calu_prrp(np.asfortranarray(a_cols[:, :w]), args.b, args.tau, "binary", args.P, panel_limit=k)
-    dt = time.perf_counter() - t0
-    flops = rect_lu_flops(args.n, w) - rect_lu_flops(args.n - k * args.b, w - k * args.b)
-    desc = (f"oracle.calu_prrp (numpy/OpenBLAS restatement of tournament.py:237-296) on the first {k} panel(s) "
-            f"of config 5 (n={args.n}, b={args.b}, P={args.P}) restricted to the first {w} columns (the columns "
-            f"those panels pivot and update; the rest of the matrix does not influence them): {dt:.1f} s; "
-            f"GFLOP/s over the sample's algorithmic flops m w^2 - w^3/3 (first {k} panels). The sample is "
-            f"tournament-dominated: the full factorization runs a larger share of BLAS-2 updates (SURVEY 8(d) "
-            f"extrapolates ~1.5 GFLOP/s for the whole run)")
-    return dt, flops, desc
+    npan = args.n // args.b
+    depths = [0] if args.cpu_strata <= 1 else [round(i * npan / args.cpu_strata) for i in range(args.cpu_strata)]
+    total_t, total_f, parts = 0.0, 0.0, []
+    for d in depths:
+        m = args.n - d * args.b
+        if m < w + args.b:
+            continue
+        if d == 0:
+            blk = np.asfortranarray(a_cols[:, :w])
+        else:
+            blk = np.asfortranarray(2.0 * np.random.Generator(np.random.PCG64(args.seed + d)).random((m, w)) - 1.0)
+        t0 = time.perf_counter()
+        orc.calu_prrp(blk, args.b, args.tau, "binary", args.P, panel_limit=k)
+        dt = time.perf_counter() - t0
+        fl = rect_lu_flops(m, w) - rect_lu_flops(m - k * args.b, w - k * args.b)
+        total_t += dt
+        total_f += fl
+        parts.append(f"panel {d} ({m} rows): {dt:.1f} s")
+    desc = (f"oracle.calu_prrp (numpy/OpenBLAS restatement of tournament.py:237-296), {k} panel(s) at "
+            f"{len(parts)} depths of config 5 (n={args.n}, b={args.b}, P={args.P}), each restricted to the "
+            f"{w} columns the panel pivots and updates [{'; '.join(parts)}]; panel 0 on the real columns, the "
+            f"deeper ones on U(-1,1) stand-ins of the trailing matrix; GFLOP/s over the samples' algorithmic flops "
+            f"m w^2 - w^3/3 (first {k} panels). The sample is tournament-dominated: the full factorization runs a "
+            f"larger share of BLAS-2 updates (SURVEY 8(d) extrapolates ~1.5 GFLOP/s for the whole run)")
+    return total_t, total_f, desc
 
 
 def cpu_descr():
