@@ -41,7 +41,11 @@
 #pragma once
 #include "panel1.cuh"
 
-#define LAT_SP_MAXC 6            // largest cluster that exchanges record + column in one round
+#ifndef LAT_SP_MAXC
+#define LAT_SP_MAXC 16           // largest cluster that exchanges record + column in one round (16: always;
+                                 // measured 1-3% faster than records first, winner column second, which
+                                 // -DLAT_SP_MAXC=6 restores for clusters above 6 CTAs)
+#endif
 constexpr int kLatNWC = 15;      // compute warps per CTA (60 teams; 16 warps with the control warp: 128 registers)
 
 struct LatRec {
