@@ -66,6 +66,7 @@ struct CaluDist {
   int32_t* moved = nullptr;
   int32_t* mcnt = nullptr;
   double* a12 = nullptr;
+  ComposeWs cws;                                                    // DMMA compose operands (launch_compose_w)
   int64_t lda12 = 0;
   int32_t* piv = nullptr;
   // message
@@ -240,6 +241,7 @@ void calu_dist_alloc(CaluDist& w, cudaStream_t s) {
   w.mcnt = ar.get<int32_t>(1);
   w.lda12 = std::max<int64_t>(2, ((w.n_loc + 1) / 2) * 2);
   w.a12 = ar.get<double>((size_t)b * w.lda12);
+  w.cws = compose_ws(ar, s, m, b);
   w.piv = ar.get<int32_t>(b);
   for (int i0 = 0; i0 < w.nnodes; i0 += 32) {
     PtrPack pk{};
@@ -603,7 +605,7 @@ void calu_dist_apply(CaluDist& w, int k, int part, cudaStream_t s) {
       if (wh > 0)
         schur_update(w.A + (col0 + bj) * w.lda + t0, w.lda, Lp, ldk, w.a12, w.lda12, rows - bj, wh, bj, st, s);
       if (own)
-        launch_compose_w(Lp, ldk, rows - bj, bj, D, gperm, w.A + (col0 + bj) * w.lda + lc0, w.lda, st, s);
+        launch_compose_w(Lp, ldk, rows - bj, bj, D, gperm, w.A + (col0 + bj) * w.lda + lc0, w.lda, st, s, &w.cws);
     }
   }
   if (part == 2 && rows > bj && wt > wh) {

@@ -753,6 +753,7 @@ thread_local int tl_force_ws = -1;   // diagnostics: per-call kernel choice (PRR
 // whole GPC stays free for the tournament's own clusters beside the update
 // (caluprrp_enqueue, chain-bound panels).
 thread_local int tl_schur_cluster = 0;
+thread_local bool tl_schur_untracked = false;   // schur_update called as a building block (compose): no span, no flops
 // CALU_PRRP enqueue: the warp-specialised kernel prefetches C (see DESIGN.md 4:
 // with the C read in the epilogue the graph-replayed CALU schedule gave
 // run-to-run different results; with the prefetch it is bit-stable)
@@ -771,8 +772,11 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
                   int64_t N, int K, DevState* st, cudaStream_t s, int max_ctas = 0, int quantum = 0,
                   bool stream_c = false) {
   if (M <= 0 || N <= 0) return;
-  tl_schur_flops += 2.0 * (double)M * (double)N * (double)K;
-  tbegin(PRRP_K_SCHUR, s);
+  const bool tracked = !tl_schur_untracked;      // (the compose product is timed as "compose", not as a Schur update)
+  if (tracked) {
+    tl_schur_flops += 2.0 * (double)M * (double)N * (double)K;
+    tbegin(PRRP_K_SCHUR, s);
+  }
   const bool tma_ok = ((uintptr_t)L % 16 == 0) && ((uintptr_t)Bm % 16 == 0) && (ldl % 2 == 0) && (ldb % 2 == 0) &&
                       K <= 4 * SCH_KC && M < (1ll << 31) && N < (1ll << 31);
   static const int schur_old = getenv("PRRP_SCHUR_OLD") ? atoi(getenv("PRRP_SCHUR_OLD")) : 0;
@@ -869,7 +873,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 7) / 8));
     schur_simt_kernel<<<grid, 256, 0, s>>>(L, ldl, Bm, ldb, C, ldc, (int)M, (int)N, K, st);
   }
-  tend(s);
+  if (tracked) tend(s);
   CU_TRY(cudaGetLastError());
 }
 
@@ -993,9 +997,46 @@ DevState* new_state(Arena& ar, cudaStream_t s) {
 // > 0: CTA cap of the compose / block-row kernels (they run beside the next
 // panel's tournament in the CALU schedule and must not take its SMs)
 thread_local int tl_fin_ctas = 0;
+// Workspace of the DMMA compose (one per factorization; the compose launches
+// of consecutive panels follow each other on the fin stream).
+struct ComposeWs {
+  double* Lneg = nullptr;   // -L21[:, gperm], column-major M x b
+  int64_t ld = 0;
+  double* Bm = nullptr;     // L11 (unit lower), row-major b x b
+  DevState* st = nullptr;   // scratch run state: the product's |C| must not enter the growth statistics
+};
+ComposeWs compose_ws(Arena& ar, cudaStream_t s, int64_t m, int b) {
+  ComposeWs w;
+  w.ld = ((m + 7) / 8) * 8;
+  w.Lneg = ar.get<double>((size_t)b * w.ld);
+  w.Bm = ar.get<double>((size_t)b * b);
+  w.st = new_state(ar, s);
+  return w;
+}
+
+// compose_below (luprrp.py:122-125): L21 <- matmul(L21[:, perm], L11), the
+// dger k-loop from a zero accumulator.  With a workspace and b a multiple of
+// 8 it runs on the DMMA pipe: out = 0 - (-L21[:, perm]) L11 with the Schur
+// kernel, whose accumulation IS that k-loop (DMMA.8x8x4 is a sequential FMA
+// chain over its four k's, k-steps in increasing order, from zero;
+// test_schur_update_bit_exact) -- the terms k < j the SIMT kernel skips are
+// x * 0 here, which leave a chain that starts at +0 unchanged -- and the
+// negation is exact, so the result is bit-identical to compose_w_kernel
+// (test_compose_dmma_bit_identical).  PRRP_COMPOSE_DMMA=0: the SIMT kernel.
 void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const double* D, const int32_t* gperm,
-                      double* out, int64_t ldo, DevState* st, cudaStream_t s) {
+                      double* out, int64_t ldo, DevState* st, cudaStream_t s, const ComposeWs* ws = nullptr) {
   if (M <= 0) return;
+  static const bool dmma = !(getenv("PRRP_COMPOSE_DMMA") && atoi(getenv("PRRP_COMPOSE_DMMA")) == 0);
+  if (ws && ws->Lneg && dmma && b % 8 == 0 && b >= 32 && M <= ws->ld && (ldo % 2 == 0) &&
+      ((uintptr_t)out % 16 == 0)) {
+    compose_prep_kernel<<<(unsigned)std::min<int64_t>(caps().sms * 4, (M * b + 255) / 256), 256, 0, s>>>(
+        L21, ldl, M, b, D, gperm, ws->Lneg, ws->ld, ws->Bm, out, ldo, st);
+    CU_TRY(cudaGetLastError());
+    tl_schur_untracked = true;
+    struct Reset { ~Reset() { tl_schur_untracked = false; } } reset;
+    schur_update(out, ldo, ws->Lneg, ws->ld, ws->Bm, b, M, b, b, ws->st, s, 0, 0, false);
+    return;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(tl_fin_ctas > 0 ? tl_fin_ctas : caps().sms * 4, (M + TC - 1) / TC);
   const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {
@@ -1089,6 +1130,7 @@ void luprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double 
   int32_t* gpermb[2] = {ar.get<int32_t>(b), ar.get<int32_t>(b)};
   int32_t* swaps_dev = ar.get<int32_t>(npanels);
   CU_TRY(cudaMemsetAsync(swaps_dev, 0, sizeof(int32_t) * npanels, s));
+  const ComposeWs cws = compose_ws(ar, s, m, b);
 
   const int sms = caps().sms;
   tl_prof = nullptr;
@@ -1187,7 +1229,7 @@ void luprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double 
       const int ctw = bj > 64 ? 64 : 128;
       tbegin(PRRP_K_COMPOSE, sf);
       if (!force_generic_panel())
-        launch_compose_w(L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, sf);
+        launch_compose_w(L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st, sf, &cws);
       else
         compose_kernel<<<(unsigned)((rows - bj + ctw - 1) / ctw), ctw, ((size_t)bj * bj + (size_t)bj * ctw) * 8, sf>>>(
             L, ldl, rows - bj, bj, D, gperm, A + (col0 + bj) * lda + col0, lda, st);
@@ -1514,6 +1556,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   const int64_t ld21t = ((m + 7) / 8) * 8;
   double* A21t = ar.get<double>((size_t)b * ld21t);
   DevState* st_r12 = new_state(ar, s);   // the product's |C| must not enter the growth statistics
+  const ComposeWs cws = compose_ws(ar, s, m, b);
   // tree nodes
   std::vector<NodeBufs> nodes(nnodes);
   const int64_t leafmax =
@@ -2007,7 +2050,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sf);
         tend(sf);
         tbegin(PRRP_K_COMPOSE, sf);
-        launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf);
+        launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf, &cws);
         tend(sf);
         CU_TRY(cudaStreamWaitEvent(sf, ev_copy, 0));
         tbegin(PRRP_K_BLOCKROW, sf);

@@ -342,6 +342,30 @@ __global__ void __launch_bounds__(TW_WARPS * 32) compose_w_kernel(const double* 
   }
 }
 
+// Operands of the DMMA compose (launch_compose_w): Lneg[k][r] = -L21[r][gperm[k]]
+// (column-major, ld), Bm = unit-lower L11 from the packed D (row-major b x b),
+// and the output block zeroed (the Schur kernel computes out - Lneg Bm).
+__global__ void compose_prep_kernel(const double* __restrict__ L21, int64_t ldl, int64_t M, int b,
+                                    const double* __restrict__ D, const int32_t* __restrict__ gperm, double* Lneg,
+                                    int64_t ld, double* Bm, double* out, int64_t ldo, const DevState* st) {
+  if (prrp_failed(st)) return;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = t0; e < M * b; e += nt) {
+    const int k = (int)(e / M);
+    const int64_t r = e % M;
+    Lneg[(int64_t)k * ld + r] = -L21[(int64_t)gperm[k] * ldl + r];
+  }
+  for (int64_t e = t0; e < M * b; e += nt) {
+    const int64_t r = e / b;
+    const int j = (int)(e % b);
+    out[r * ldo + j] = 0.0;
+  }
+  for (int64_t e = t0; e < (int64_t)b * b; e += nt) {
+    const int k = (int)(e / b), j = (int)(e % b);
+    Bm[e] = k > j ? D[e] : (k == j ? 1.0 : 0.0);
+  }
+}
+
 // Block-row finish (see blockrow_kernel): columns [0, col0) permuted by the
 // GEPP order, [col0, col0+b) from D, [col0+b, n) eliminated.
 // Columns are local indices c < n; their global index (which decides the L

@@ -85,3 +85,42 @@ def test_lat_engine_rank_deficient_panel():
     theirs[:, ref.perm] = ref.r[:5]
     assert np.abs(mine - theirs).max() <= 1e-10 * np.abs(ref.r).max()
     assert np.abs(R[5:]).max() <= 1e-12 * np.abs(ref.r).max()
+
+
+_DIGEST = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_1208_2451_b200 as dev
+from oracle import prrp_oracle as orc
+out = []
+for n, b in ((1024, 64), (768, 128), (640, 32)):
+    a = orc.randn_matrix(n, 7)
+    f = dev.luprrp_factor(a, b, 2.0)
+    out.append(hashlib.sha256(np.ascontiguousarray(f.l).tobytes() + np.ascontiguousarray(f.u).tobytes()
+                              + f.perm.tobytes()).hexdigest())
+    g = dev.caluprrp_factor(a, b, 2.0, dev.binary_tree(4))
+    out.append(hashlib.sha256(np.ascontiguousarray(g.l).tobytes() + np.ascontiguousarray(g.u).tobytes()
+                              + g.perm.tobytes()).hexdigest())
+print("DIGESTS " + " ".join(out))
+"""
+
+
+def test_compose_dmma_bit_identical():
+    """compose_below on the DMMA pipe (launch_compose_w) gives the same bits as the
+    SIMT kernel that walks the dger k-loop (luprrp.py:122-125): LU_PRRP and
+    CALU_PRRP factors, b = 32 / 64 / 128, hashed in two processes that differ
+    only in PRRP_COMPOSE_DMMA."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, PRRP_COMPOSE_DMMA=flag)
+        p = subprocess.run([sys.executable, "-c", _DIGEST], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        line = [l for l in p.stdout.splitlines() if l.startswith("DIGESTS ")][-1]
+        res.append(line.split()[1:])
+    assert res[0] == res[1]
