@@ -278,23 +278,25 @@ __global__ void __launch_bounds__(1024) gepp_diag_kernel(const double* src, int6
   gepp_diag(src, ld, rowmap, b, sm, D, piv, gperm, st, panel, red);
 }
 
-// Register GEPP of a b x b block, b <= 64 (gepp.py:39-65, same arithmetic as
-// gepp_diag).  256 threads: thread (i, q) = (t >> 2, t & 3) holds row i,
-// columns 16q .. 16q+15 in registers.  Per step: the owners of column k
+// Register GEPP of a b x b block, b <= B = 64 or 128 (gepp.py:39-65, same
+// arithmetic as gepp_diag).  B * B/16 threads (256 / 1024): thread (i, q) =
+// (t / (B/16), t % (B/16)) holds row i, columns 16q .. 16q+15 in registers.  Per step: the owners of column k
 // publish it, every warp finds the first-max pivot redundantly, the pivot
 // row and row k trade places through shared memory, and each thread updates
 // its 16 entries (product, then subtraction).  Two barriers per step.
 #define GR_T 256
-__global__ void __launch_bounds__(GR_T, 1) gepp_reg_kernel(const double* src, int64_t ld, const int32_t* rowmap, int b,
-                                                          double* D, int32_t* piv, int32_t* gperm, DevState* st,
-                                                          int panel) {
-  __shared__ double colk[2][64];
-  __shared__ __align__(16) double prow[64], krow[64];
-  __shared__ int s_gp[64];
+template <int B>
+__global__ void __launch_bounds__(B * (B / 16), 1) gepp_reg_kernel(const double* src, int64_t ld, const int32_t* rowmap,
+                                                                   int b, double* D, int32_t* piv, int32_t* gperm,
+                                                                   DevState* st, int panel) {
+  constexpr int QN = B / 16;
+  __shared__ double colk[2][B];
+  __shared__ __align__(16) double prow[B], krow[B];
+  __shared__ int s_gp[B];
   __shared__ double red[40];
   if (prrp_failed(st)) return;
   const int t = threadIdx.x, lane = t & 31;
-  const int i = t >> 2, q = t & 3;
+  const int i = t / QN, q = t % QN;
   double a[16];
   double mx = 0.0;
   {
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(GR_T, 1) gepp_reg_kernel(const double* src, in
       mx = fmax(mx, fabs(a[s]));
     }
   }
-  if (t < 64) s_gp[t] = t;
+  if (t < B) s_gp[t] = t;
   __syncthreads();
   for (int k = 0; k < b; ++k) {
     const int ks = k & 15, kq = k >> 4, cb = k & 1;
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(GR_T, 1) gepp_reg_kernel(const double* src, in
     double best = -1.0;
     int bi = INT_MAX;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < B / 32; ++u) {
       const int r = k + lane + 32 * u;
       if (r < b) {
         const double v = fabs(colk[cb][r]);

@@ -130,6 +130,7 @@ DeviceCaps& caps() {
     CU_TRY(cudaFuncSetAttribute(trsm_c2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmC2Smem));
     set_max_dyn((const void*)permute_kernel);
     set_max_dyn((const void*)blockrow_kernel);
+    set_max_dyn((const void*)blockrow_x_kernel);
     set_max_dyn((const void*)compose_kernel);
     set_max_dyn((const void*)gepp_diag_kernel);
     set_max_dyn((const void*)gepp_node_kernel<true>);
@@ -510,7 +511,11 @@ void launch_team(const PanelArgs& a0, cudaStream_t s, int force_nwc = 0, int for
 // GEPP of a b x b block (register kernel for b <= 64, shared-memory kernel above)
 void launch_gepp(const double* src, int64_t ld, const int32_t* rowmap, int b, double* D, int32_t* piv,
                  int32_t* gperm, DevState* st, int panel, cudaStream_t s) {
-  if (b <= 64) gepp_reg_kernel<<<1, GR_T, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
+  // b <= 64: 256 threads.  The same kernel with 1024 threads for b <= 128 (PRRP_GEPP_REG128=1) was
+  // measured SLOWER than the shared-memory kernel (LU_PRRP b = 128: gepp spans 28.2 vs 23.8 ms), so off.
+  static const bool reg128 = getenv("PRRP_GEPP_REG128") && atoi(getenv("PRRP_GEPP_REG128")) != 0;
+  if (b <= 64) gepp_reg_kernel<64><<<1, GR_T, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
+  else if (b <= 128 && reg128) gepp_reg_kernel<128><<<1, 1024, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
   else gepp_diag_kernel<<<1, 128, (size_t)b * (b + 1) * 8, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
 }
 
@@ -1050,6 +1055,15 @@ void launch_compose_w(const double* L21, int64_t ldl, int64_t M, int b, const do
 void launch_blockrow_w(double* A, int64_t lda, int64_t col0, int b, int64_t n, const double* D, const int32_t* gperm,
                        int64_t* perm, DevState* st, cudaStream_t s, int64_t bl = 1, int nr = 1, int rk = 0) {
   if (n <= 0) return;
+  // thread-per-column kernel (b a multiple of 8; bit-identical, ~7x faster at
+  // b = 128); PRRP_BLOCKROW_X=0: the warp-per-column kernel
+  static const bool bx = !(getenv("PRRP_BLOCKROW_X") && atoi(getenv("PRRP_BLOCKROW_X")) == 0);
+  if (bx && b % 8 == 0 && b >= 16 && (b > 64 || n >= 96 * BX_TC)) {   // (b <= 64, few columns: too few CTAs)
+    const unsigned gx = (unsigned)std::min<int64_t>(tl_fin_ctas > 0 ? tl_fin_ctas : caps().sms * 4,
+                                                    (n + BX_TC - 1) / BX_TC);
+    blockrow_x_kernel<<<gx, BX_TC, bx_smem(b), s>>>(A, lda, col0, b, n, D, gperm, perm, st, bl, nr, rk);
+    return;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(tl_fin_ctas > 0 ? tl_fin_ctas : caps().sms * 4, (n + TC - 1) / TC);
   const size_t dyn = ((size_t)b * b + (size_t)b * TCP) * 8;
   switch ((b + 31) / 32) {

@@ -342,6 +342,117 @@ __global__ void __launch_bounds__(TW_WARPS * 32) compose_w_kernel(const double* 
   }
 }
 
+// Block-row finish, thread per column (b a multiple of 8).  The warp-per-
+// column form above keeps half its lanes idle (row i > k) and pays a shuffle
+// per pivot step: 0.59 ms per panel at config 5 on the fin stream, which is
+// close to the critical path there.  Here a thread owns one column of the
+// block row in shared memory (tile[i][c], conflict free) and walks it
+// LEFT-looking in blocks of 8 pivots: the 8 pivot rows of a block are
+// finished in registers, then every row below receives the block's 8
+// updates, four rows at a time (four independent chains per thread).  Per
+// element the operation sequence is unchanged -- x_i -= l_ik x_k for k = 0, 1,
+// ... in increasing order, product rounded, then subtracted (gepp.py:57-59)
+// -- so the result and the running maximum (every intermediate value, the
+// reference's observe_finish) are bit-identical to the warp-per-column
+// kernel.  L11's strictly lower part is staged per pivot block:
+// lt[off(kb) + (i - 8 kb) * 8 + kk] = L11[i][8 kb + kk], read as broadcasts.
+#define BX_TC 128                     // columns (threads) per tile
+__host__ __device__ inline int bx_off(int kb, int b) { return 8 * (kb * b - 4 * kb * (kb - 1)); }
+__host__ __device__ inline size_t bx_smem(int b) {
+  return ((size_t)bx_off(b / 8, b) + (size_t)b * BX_TC) * 8;
+}
+__global__ void __launch_bounds__(BX_TC) blockrow_x_kernel(double* A, int64_t lda, int64_t col0, int b, int64_t n,
+                                                           const double* __restrict__ D, const int32_t* gperm,
+                                                           int64_t* p, DevState* st, int64_t bl, int nr, int rk) {
+  extern __shared__ __align__(16) double sm[];
+  const int nkb = b >> 3;
+  double* lt = sm;                                 // per-block strictly lower L11
+  double* tile = sm + bx_off(nkb, b);              // b x BX_TC
+  __shared__ int s_gp[PRRP_MAXH];
+  __shared__ int64_t s_p[PRRP_MAXH];
+  __shared__ double red[40];
+  if (prrp_failed(st)) return;
+  const int t = threadIdx.x;
+  for (int i = t; i < b; i += blockDim.x) s_gp[i] = gperm[i];
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int rows = b - 8 * kb;
+    double* dst = lt + bx_off(kb, b);
+    for (int e = t; e < rows * 8; e += blockDim.x) {
+      const int i = 8 * kb + e / 8, k = 8 * kb + (e & 7);
+      dst[e] = i > k ? D[i * b + k] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int i = t; i < b; i += blockDim.x) s_p[i] = p[col0 + s_gp[i]];
+    __syncthreads();
+    for (int i = t; i < b; i += blockDim.x) p[col0 + i] = s_p[i];
+  }
+  double mx = 0.0;
+  for (int64_t c0 = (int64_t)blockIdx.x * BX_TC; c0 < n; c0 += (int64_t)gridDim.x * BX_TC) {
+    const int tc = (int)min((int64_t)BX_TC, n - c0);
+    // stage: rows in final GEPP order (L part and trailing part), D for the diagonal block
+    for (int e = t; e < b * BX_TC; e += blockDim.x) {
+      const int i = e / BX_TC, cc = e % BX_TC;
+      if (cc >= tc) continue;
+      const int64_t j = c0 + cc;
+      const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
+      tile[i * BX_TC + cc] = (g >= col0 && g < col0 + b) ? D[i * b + (g - col0)] : A[(col0 + s_gp[i]) * lda + j];
+    }
+    __syncthreads();
+    if (t < tc) {
+      const int64_t j = c0 + t;
+      const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
+      if (g >= col0 + b) {                           // trailing column: eliminate
+        double* col = tile + t;
+        for (int i = 0; i < b; ++i) mx = fmax(mx, fabs(col[i * BX_TC]));
+        for (int kb = 0; kb < nkb; ++kb) {
+          const double* lb = lt + bx_off(kb, b);     // rows 8 kb .. b-1, 8 entries each
+          double x[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) x[kk] = col[(8 * kb + kk) * BX_TC];
+          // the block's own rows
+#pragma unroll
+          for (int kk = 0; kk < 7; ++kk) {
+#pragma unroll
+            for (int ii = kk + 1; ii < 8; ++ii) {
+              x[ii] = sub_rn(x[ii], mul_rn(lb[ii * 8 + kk], x[kk]));
+              mx = fmax(mx, fabs(x[ii]));
+            }
+          }
+#pragma unroll
+          for (int kk = 1; kk < 8; ++kk) col[(8 * kb + kk) * BX_TC] = x[kk];
+          // the rows below, four at a time
+          for (int i0 = 8 * kb + 8; i0 < b; i0 += 4) {
+            const double* l4 = lb + (i0 - 8 * kb) * 8;
+            double v[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) v[r] = col[(i0 + r) * BX_TC];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                v[r] = sub_rn(v[r], mul_rn(l4[r * 8 + kk], x[kk]));
+                mx = fmax(mx, fabs(v[r]));
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) col[(i0 + r) * BX_TC] = v[r];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = t; e < b * BX_TC; e += blockDim.x) {
+      const int i = e / BX_TC, cc = e % BX_TC;
+      if (cc < tc) A[(col0 + i) * lda + c0 + cc] = tile[i * BX_TC + cc];
+    }
+    __syncthreads();
+  }
+  const double m = block_max(mx, red);
+  if (t == 0 && m > 0.0) atomic_max_abs(&st->finish_max, m);
+}
+
 // Operands of the DMMA compose (launch_compose_w): Lneg[k][r] = -L21[r][gperm[k]]
 // (column-major, ld), Bm = unit-lower L11 from the packed D (row-major b x b),
 // and the output block zeroed (the Schur kernel computes out - Lneg Bm).

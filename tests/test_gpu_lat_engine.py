@@ -98,26 +98,29 @@ for n, b in ((1024, 64), (768, 128), (640, 32)):
     a = orc.randn_matrix(n, 7)
     f = dev.luprrp_factor(a, b, 2.0)
     out.append(hashlib.sha256(np.ascontiguousarray(f.l).tobytes() + np.ascontiguousarray(f.u).tobytes()
-                              + f.perm.tobytes()).hexdigest())
+                              + f.perm.tobytes() + repr(f.stats.full_growth_factor).encode()).hexdigest())
     g = dev.caluprrp_factor(a, b, 2.0, dev.binary_tree(4))
     out.append(hashlib.sha256(np.ascontiguousarray(g.l).tobytes() + np.ascontiguousarray(g.u).tobytes()
-                              + g.perm.tobytes()).hexdigest())
+                              + g.perm.tobytes() + repr(g.stats.full_growth_factor).encode()).hexdigest())
 print("DIGESTS " + " ".join(out))
 """
 
 
-def test_compose_dmma_bit_identical():
-    """compose_below on the DMMA pipe (launch_compose_w) gives the same bits as the
-    SIMT kernel that walks the dger k-loop (luprrp.py:122-125): LU_PRRP and
-    CALU_PRRP factors, b = 32 / 64 / 128, hashed in two processes that differ
-    only in PRRP_COMPOSE_DMMA."""
+def test_compose_dmma_and_blockrow_bit_identical():
+    """compose_below on the DMMA pipe (launch_compose_w) and the thread-per-column
+    block-row finish (blockrow_x_kernel) give the same bits -- factors and the
+    finish statistic -- as the kernels that walk the reference's loops literally
+    (luprrp.py:122-125, gepp.py:57-60): LU_PRRP and CALU_PRRP, b = 32 / 64 / 128,
+    hashed in two processes that differ only in PRRP_COMPOSE_DMMA / PRRP_BLOCKROW_X /
+    PRRP_GEPP_REG128 (the 1024-thread register GEPP of the b = 128 diagonal block against
+    the shared-memory kernel)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
     for flag in ("1", "0"):
-        env = dict(os.environ, PRRP_COMPOSE_DMMA=flag)
+        env = dict(os.environ, PRRP_COMPOSE_DMMA=flag, PRRP_BLOCKROW_X=flag, PRRP_GEPP_REG128="0" if flag == "1" else "1")
         p = subprocess.run([sys.executable, "-c", _DIGEST], cwd=root, env=env, capture_output=True, text=True,
                            timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
