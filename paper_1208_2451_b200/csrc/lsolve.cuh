@@ -239,25 +239,35 @@ __device__ void gepp_diag(const double* src, int64_t ld, const int32_t* rowmap, 
       const double yk = __drcp_rn(ckk);
       for (int i = k + 1 + t; i < b; i += T) c[i * bp + k] = div_fast(c[i * bp + k], ckk, yk);
       __syncthreads();
-      for (int j = k + 1 + t; j < b; j += T) {
-        const double ckj = c[k * bp + j];
-        int i = k + 1;
-        for (; i + 8 <= b; i += 8) {       // batch the loads: no smem load->store chains
-          double cv[8], lv[8];
+      // column j = k + 1 + (t % W) and every H-th 8-row chunk below the pivot,
+      // W = min(T, 128) column threads x H = T / W row groups (each element is
+      // updated once per step whatever the split: same bits)
+      const int W = T < 128 ? T : 128, H = T / W;
+      const int tj = t % W, th = t / W;
+      if (th < H) {
+        for (int j = k + 1 + tj; j < b; j += W) {
+          const double ckj = c[k * bp + j];
+          int i = k + 1 + 8 * th;
+          for (; i + 8 <= b; i += 8 * H) {       // batch the loads: no smem load->store chains
+            double cv[8], lv[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) { cv[u] = c[(i + u) * bp + j]; lv[u] = c[(i + u) * bp + k]; }
+            for (int u = 0; u < 8; ++u) { cv[u] = c[(i + u) * bp + j]; lv[u] = c[(i + u) * bp + k]; }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            cv[u] = sub_rn(cv[u], mul_rn(lv[u], ckj));
-            mx = fmax(mx, fabs(cv[u]));
+            for (int u = 0; u < 8; ++u) {
+              cv[u] = sub_rn(cv[u], mul_rn(lv[u], ckj));
+              mx = fmax(mx, fabs(cv[u]));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[(i + u) * bp + j] = cv[u];
           }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) c[(i + u) * bp + j] = cv[u];
-        }
-        for (; i < b; ++i) {
-          const double v = sub_rn(c[i * bp + j], mul_rn(c[i * bp + k], ckj));
-          c[i * bp + j] = v;
-          mx = fmax(mx, fabs(v));
+          // the partial chunk at the bottom belongs to the group whose turn it is
+          if (i < b) {
+            for (; i < b; ++i) {
+              const double v = sub_rn(c[i * bp + j], mul_rn(c[i * bp + k], ckj));
+              c[i * bp + j] = v;
+              mx = fmax(mx, fabs(v));
+            }
+          }
         }
       }
     }

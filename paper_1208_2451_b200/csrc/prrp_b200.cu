@@ -516,7 +516,12 @@ void launch_gepp(const double* src, int64_t ld, const int32_t* rowmap, int b, do
   static const bool reg128 = getenv("PRRP_GEPP_REG128") && atoi(getenv("PRRP_GEPP_REG128")) != 0;
   if (b <= 64) gepp_reg_kernel<64><<<1, GR_T, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
   else if (b <= 128 && reg128) gepp_reg_kernel<128><<<1, 1024, 0, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
-  else gepp_diag_kernel<<<1, 128, (size_t)b * (b + 1) * 8, s>>>(src, ld, rowmap, b, D, piv, gperm, st, panel);
+  else {
+    // 128 column threads x T / 128 row groups (PRRP_GEPP_DIAG_T: 128 = one thread per column as in round 1)
+    static const int gt = getenv("PRRP_GEPP_DIAG_T") ? atoi(getenv("PRRP_GEPP_DIAG_T")) : 512;
+    gepp_diag_kernel<<<1, std::max(128, std::min(1024, gt / 128 * 128)), (size_t)b * (b + 1) * 8, s>>>(
+        src, ld, rowmap, b, D, piv, gperm, st, panel);
+  }
 }
 
 // b in (64, 128]: 8-lane chunked trsm (trsm_c2_kernel); PRRP_TRSM_W=1 selects

@@ -120,7 +120,8 @@ def test_compose_dmma_and_blockrow_bit_identical():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
     for flag in ("1", "0"):
-        env = dict(os.environ, PRRP_COMPOSE_DMMA=flag, PRRP_BLOCKROW_X=flag, PRRP_GEPP_REG128="0" if flag == "1" else "1")
+        env = dict(os.environ, PRRP_COMPOSE_DMMA=flag, PRRP_BLOCKROW_X=flag, PRRP_GEPP_REG128="0" if flag == "1" else "1",
+                   PRRP_GEPP_DIAG_T="512" if flag == "1" else "128")
         p = subprocess.run([sys.executable, "-c", _DIGEST], cwd=root, env=env, capture_output=True, text=True,
                            timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
