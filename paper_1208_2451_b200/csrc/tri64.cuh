@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(TW_WARPS * 32) compose_w_kernel(const double* 
 // block row in shared memory (tile[i][c], conflict free) and walks it
 // LEFT-looking in blocks of 8 pivots: the 8 pivot rows of a block are
 // finished in registers, then every row below receives the block's 8
-// updates, four rows at a time (four independent chains per thread).  Per
+// updates, eight rows at a time (eight independent chains per thread).  Per
 // element the operation sequence is unchanged -- x_i -= l_ik x_k for k = 0, 1,
 // ... in increasing order, product rounded, then subtracted (gepp.py:57-59)
 // -- so the result and the running maximum (every intermediate value, the
@@ -377,9 +377,19 @@ __global__ void __launch_bounds__(BX_TC) blockrow_x_kernel(double* A, int64_t ld
   for (int kb = 0; kb < nkb; ++kb) {
     const int rows = b - 8 * kb;
     double* dst = lt + bx_off(kb, b);
-    for (int e = t; e < rows * 8; e += blockDim.x) {
-      const int i = 8 * kb + e / 8, k = 8 * kb + (e & 7);
-      dst[e] = i > k ? D[i * b + k] : 0.0;
+    for (int e0 = t; e0 < rows * 8; e0 += 8 * blockDim.x) {      // 8 independent loads in flight
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        const int i = 8 * kb + e / 8, k = 8 * kb + (e & 7);
+        v[u] = (e < rows * 8 && i > k) ? D[i * b + k] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < rows * 8) dst[e] = v[u];
+      }
     }
   }
   __syncthreads();
@@ -391,13 +401,20 @@ __global__ void __launch_bounds__(BX_TC) blockrow_x_kernel(double* A, int64_t ld
   double mx = 0.0;
   for (int64_t c0 = (int64_t)blockIdx.x * BX_TC; c0 < n; c0 += (int64_t)gridDim.x * BX_TC) {
     const int tc = (int)min((int64_t)BX_TC, n - c0);
-    // stage: rows in final GEPP order (L part and trailing part), D for the diagonal block
-    for (int e = t; e < b * BX_TC; e += blockDim.x) {
-      const int i = e / BX_TC, cc = e % BX_TC;
-      if (cc >= tc) continue;
-      const int64_t j = c0 + cc;
+    // stage: rows in final GEPP order (L part and trailing part), D for the
+    // diagonal block; thread = column, 8 independent row loads in flight
+    if (t < tc) {
+      const int64_t j = c0 + t;
       const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
-      tile[i * BX_TC + cc] = (g >= col0 && g < col0 + b) ? D[i * b + (g - col0)] : A[(col0 + s_gp[i]) * lda + j];
+      const bool diag = g >= col0 && g < col0 + b;
+      for (int i0 = 0; i0 < b; i0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = diag ? D[(i0 + u) * b + (g - col0)] : A[(col0 + s_gp[i0 + u]) * lda + j];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tile[(i0 + u) * BX_TC + t] = v[u];
+      }
     }
     __syncthreads();
     if (t < tc) {
@@ -405,7 +422,16 @@ __global__ void __launch_bounds__(BX_TC) blockrow_x_kernel(double* A, int64_t ld
       const int64_t g = nr == 1 ? j : ((j / bl) * nr + rk) * bl + j % bl;
       if (g >= col0 + b) {                           // trailing column: eliminate
         double* col = tile + t;
-        for (int i = 0; i < b; ++i) mx = fmax(mx, fabs(col[i * BX_TC]));
+        // eight running maxima (one per row chain: a single one would be a
+        // dependency chain through every update), merged after the column;
+        // a > m ? a : m ignores NaN like fmax (m starts at 0).  (Keeping them
+        // as bit patterns on the integer pipe was measured no faster.)
+        double m8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#define BX_MAX(m, a) { const double a_ = fabs(a); m = a_ > m ? a_ : m; }
+        for (int i = 0; i < b; i += 8) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) BX_MAX(m8[r], col[(i + r) * BX_TC]);
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           const double* lb = lt + bx_off(kb, b);     // rows 8 kb .. b-1, 8 entries each
           double x[8];
@@ -417,35 +443,51 @@ __global__ void __launch_bounds__(BX_TC) blockrow_x_kernel(double* A, int64_t ld
 #pragma unroll
             for (int ii = kk + 1; ii < 8; ++ii) {
               x[ii] = sub_rn(x[ii], mul_rn(lb[ii * 8 + kk], x[kk]));
-              mx = fmax(mx, fabs(x[ii]));
+              BX_MAX(m8[ii], x[ii]);
             }
           }
 #pragma unroll
           for (int kk = 1; kk < 8; ++kk) col[(8 * kb + kk) * BX_TC] = x[kk];
-          // the rows below, four at a time
-          for (int i0 = 8 * kb + 8; i0 < b; i0 += 4) {
-            const double* l4 = lb + (i0 - 8 * kb) * 8;
-            double v[4];
+          // the rows below, eight at a time (eight independent chains)
+          for (int i0 = 8 * kb + 8; i0 < b; i0 += 8) {
+            const double* l8 = lb + (i0 - 8 * kb) * 8;
+            double v[8];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) v[r] = col[(i0 + r) * BX_TC];
+            for (int r = 0; r < 8; ++r) v[r] = col[(i0 + r) * BX_TC];
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
+            for (int kk = 0; kk < 8; kk += 2) {
+              double2 l2[8];
 #pragma unroll
-              for (int r = 0; r < 4; ++r) {
-                v[r] = sub_rn(v[r], mul_rn(l4[r * 8 + kk], x[kk]));
-                mx = fmax(mx, fabs(v[r]));
+              for (int r = 0; r < 8; ++r) l2[r] = *reinterpret_cast<const double2*>(l8 + r * 8 + kk);
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                v[r] = sub_rn(v[r], mul_rn(l2[r].x, x[kk]));
+                BX_MAX(m8[r], v[r]);
+              }
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                v[r] = sub_rn(v[r], mul_rn(l2[r].y, x[kk + 1]));
+                BX_MAX(m8[r], v[r]);
               }
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) col[(i0 + r) * BX_TC] = v[r];
+            for (int r = 0; r < 8; ++r) col[(i0 + r) * BX_TC] = v[r];
           }
         }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) mx = m8[r] > mx ? m8[r] : mx;
+#undef BX_MAX
       }
     }
     __syncthreads();
-    for (int e = t; e < b * BX_TC; e += blockDim.x) {
-      const int i = e / BX_TC, cc = e % BX_TC;
-      if (cc < tc) A[(col0 + i) * lda + c0 + cc] = tile[i * BX_TC + cc];
+    if (t < tc) {
+      for (int i0 = 0; i0 < b; i0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tile[(i0 + u) * BX_TC + t];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) A[(col0 + i0 + u) * lda + c0 + t] = v[u];
+      }
     }
     __syncthreads();
   }
