@@ -329,7 +329,19 @@ __global__ void __launch_bounds__(256) calu_gather_t_kernel(const double* A, int
 // refl[k*(b+1) + b] = beta (0: step skipped).
 __global__ void __launch_bounds__(128) calu_form_negqt_kernel(const double* refl, int b, double* L) {
   extern __shared__ __align__(16) double rf[];   // b x (b + 1)
-  for (int e = threadIdx.x; e < b * (b + 1); e += blockDim.x) rf[e] = refl[e];
+  for (int e0 = threadIdx.x; e0 < b * (b + 1); e0 += 8 * blockDim.x) {   // 8 independent loads in flight
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < b * (b + 1) ? refl[e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < b * (b + 1)) rf[e] = v[u];
+    }
+  }
   __syncthreads();
   const int j = blockIdx.x * 16 + (threadIdx.x >> 3), q = threadIdx.x & 7;
   const bool on = j < b;
