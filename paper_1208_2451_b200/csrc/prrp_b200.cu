@@ -1515,7 +1515,7 @@ int calu_leaf_cmax() {
 }
 bool calu_chain_bound(int64_t m, int64_t n, int b, int pnl, bool flat) {
   // thresholds ~ the chain time of a panel: ~2 ms at b = 128, ~0.8 ms at b = 64
-  static const double cb_ms = getenv("PRRP_CALU_CB_MS") ? atof(getenv("PRRP_CALU_CB_MS")) : 2.0;
+  static const double cb_ms = getenv("PRRP_CALU_CB_MS") ? atof(getenv("PRRP_CALU_CB_MS")) : 1.5;
   static const double cb_ms64 = getenv("PRRP_CALU_CB_MS64") ? atof(getenv("PRRP_CALU_CB_MS64")) : 0.6;
   const double thr = b > 64 ? cb_ms : cb_ms64;
   if (!(thr > 0.0 && (b == 64 || b == 128 || b == 32) && !flat && caps().max_cluster >= 16 &&
@@ -1547,7 +1547,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   static const int calu_narrow_ctas = getenv("PRRP_CALU_NARROW") ? atoi(getenv("PRRP_CALU_NARROW")) : 0;
   static const int calu_wide_q = getenv("PRRP_CALU_WIDE_Q") ? atoi(getenv("PRRP_CALU_WIDE_Q")) : 0;
   static const int calu_wide_ctas = getenv("PRRP_CALU_WIDE_CTAS") ? atoi(getenv("PRRP_CALU_WIDE_CTAS"))
-                                                                  : std::max(1, caps().sms - 8);
+                                                                  : std::max(1, caps().sms - 5);
   DevState* st = new_state(ar, s);
   const int64_t ldl = ((m + 7) / 8) * 8;
   double* Lphys = ar.get<double>((size_t)b * ldl);
