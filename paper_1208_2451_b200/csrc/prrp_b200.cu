@@ -1636,6 +1636,8 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
   std::vector<std::vector<std::pair<int64_t, int>>> node_members(npanels);   // (members, node slot)
 
   static const int early_w2 = getenv("PRRP_CALU_EARLY_W2") ? atoi(getenv("PRRP_CALU_EARLY_W2")) : 0;   // diagnostics
+  // PRRP_CALU_SB_SERIAL bit 2: the previous panel's fin-stream work starts when the leaves' QRCP kernels are done
+  static const bool fin_after_leaf_qrcp = getenv("PRRP_CALU_SB_SERIAL") && (atoi(getenv("PRRP_CALU_SB_SERIAL")) & 4);
   std::vector<cudaEvent_t> leaf_qrcp_ev;
   auto run_level = [&](const std::vector<int64_t>& lo, const std::vector<int64_t>& cnt, bool leaves,
                        int64_t col0, int bj, int panel, int level, int slot0, cudaStream_t qs) {
@@ -1650,7 +1652,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       const int64_t* ridx = leaves ? pos2row + col0 + lo[i] : nodes[i].rowidx;
       if (cnt[i] <= bj) continue;                       // node passes its rows through
       cudaEvent_t qe = nullptr;
-      if (leaves && early_w2) {
+      if (leaves && (early_w2 || fin_after_leaf_qrcp)) {
         CU_TRY(cudaEventCreateWithFlags(&qe, cudaEventDisableTiming));
         leaf_qrcp_ev.push_back(qe);
       }
@@ -1865,6 +1867,11 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
         int slot = 0;
         leaf_qrcp_ev.clear();
         run_level(lo, cnt, true, col0, bj, panel, 0, slot, sm);
+        if (fin_after_leaf_qrcp && pending_fin) {
+          for (cudaEvent_t e : leaf_qrcp_ev) CU_TRY(cudaStreamWaitEvent(sf, e, 0));
+          pending_fin();
+          pending_fin = nullptr;
+        }
         if (early_w2 && pending_side) {
           for (cudaEvent_t e : leaf_qrcp_ev) CU_TRY(cudaStreamWaitEvent(sd, e, 0));
           flush_side(nullptr);
@@ -2060,14 +2067,21 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       fin_ev[panel] = ss.ev(evi++);
       cudaEvent_t fin_done = fin_ev[panel];
       cudaEvent_t ev_copy = ss.ev(evi++);
+      // the L-part row moves and the GEPP of the pivot block need only this
+      // panel's row moves (ev_perm), not its L21: PRRP_CALU_GEPP_EARLY=1 starts
+      // them before the final QR / narrow update (less fin-stream work left
+      // when the next panel's leaf clusters look for SMs).  Measured neutral
+      // (config 5 1150.6 vs 1152.5 ms, config 4 260.5 vs 257.8 ms), so off.
+      static const bool gepp_early = getenv("PRRP_CALU_GEPP_EARLY") && atoi(getenv("PRRP_CALU_GEPP_EARLY")) != 0;
       pending_fin = [=]() {
-        CU_TRY(cudaStreamWaitEvent(sf, ev_narrow, 0));
+        CU_TRY(cudaStreamWaitEvent(sf, gepp_early ? ev_perm : ev_narrow, 0));
         tbegin(PRRP_K_PERMUTE, sf);
         permute_cols(0, col0, col0, mv, mc, perm, panel, sf);
         tend(sf);
         tbegin(PRRP_K_GEPP, sf);
         launch_gepp(blk, lda, nullptr, bj, Dk, pivk, gpk, st, panel, sf);
         tend(sf);
+        if (gepp_early) CU_TRY(cudaStreamWaitEvent(sf, ev_narrow, 0));
         tbegin(PRRP_K_COMPOSE, sf);
         launch_compose_w(Lp, ldl, rows - bj, bj, Dk, gpk, A + (col0 + bj) * lda + col0, lda, st, sf, &cws);
         tend(sf);
@@ -2089,7 +2103,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
                                  (size_t)(n - cw0) * 8, (size_t)bj, cudaMemcpyDeviceToDevice, sd));
       tend(sd);
       CU_TRY(cudaEventRecord(ev_copy, sd));
-      if (!((sb_serial & 2) && calu_defer && b > 64 && !chain_bound(panel + 1))) {
+      if (!((sb_serial & 6) && calu_defer && b > 64 && !chain_bound(panel + 1))) {
         pending_fin();
         pending_fin = nullptr;
       }
