@@ -1509,6 +1509,25 @@ struct CaluOut {
 // tournament chain, not the update, bounds the panel (see caluprrp_enqueue).
 // The single-GPU and the distributed driver use the same rule, so every node
 // runs on the same engine in both (bit-identical results).
+// A warp that sleeps for `us` microseconds: the side and fin streams of the
+// CALU schedule start their work for panel k this long after the narrow
+// update, i.e. after the next panel's leaf clusters have been launched.  A
+// leaf CTA of the thread-per-column engine takes ~60K of an SM's 64K
+// registers, so it cannot share an SM with a row-move / GEPP / compose CTA
+// that got there a few microseconds earlier, and a 16-CTA cluster that does
+// not find 16 free SMs in one GPC waits for the whole level (the straggler
+// leaf of the span traces).  PRRP_CALU_SIDE_DELAY_US (default 0 = off):
+// measured neutral under graph replay (1150 ms at 20 and 50 us, 1154 at 100),
+// so the straggler of the direct-enqueue traces is not a launch-order effect.
+__global__ void spin_delay_kernel(unsigned us) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (t1 - t0 < (unsigned long long)us * 1000ull);
+}
+
 int calu_leaf_cmax() {
   static const int v = getenv("PRRP_CALU_LEAF_CMAX") ? atoi(getenv("PRRP_CALU_LEAF_CMAX")) : 8;
   return v;
@@ -2073,8 +2092,10 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       // when the next panel's leaf clusters look for SMs).  Measured neutral
       // (config 5 1150.6 vs 1152.5 ms, config 4 260.5 vs 257.8 ms), so off.
       static const bool gepp_early = getenv("PRRP_CALU_GEPP_EARLY") && atoi(getenv("PRRP_CALU_GEPP_EARLY")) != 0;
+      static const int side_delay_us = getenv("PRRP_CALU_SIDE_DELAY_US") ? atoi(getenv("PRRP_CALU_SIDE_DELAY_US")) : 0;
       pending_fin = [=]() {
         CU_TRY(cudaStreamWaitEvent(sf, gepp_early ? ev_perm : ev_narrow, 0));
+        if (side_delay_us > 0 && !gepp_early) spin_delay_kernel<<<1, 32, 0, sf>>>((unsigned)side_delay_us);
         tbegin(PRRP_K_PERMUTE, sf);
         permute_cols(0, col0, col0, mv, mc, perm, panel, sf);
         tend(sf);
@@ -2095,6 +2116,7 @@ void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, doubl
       // side: trailing row moves + copy of their pivot-row part, trailing
       // update (next narrow region first)
       CU_TRY(cudaStreamWaitEvent(sd, ev_narrow, 0));
+      if (side_delay_us > 0) spin_delay_kernel<<<1, 32, 0, sd>>>((unsigned)side_delay_us);
       const int64_t cw0 = col0 + bj + wn;
       tbegin(PRRP_K_PERMUTE, sd);
       permute_cols(cw0, n, col0, mv, mc, nullptr, panel, sd);
