@@ -612,9 +612,15 @@ void calu_dist_apply(CaluDist& w, int k, int part, cudaStream_t s) {
     const int64_t wh2 = next_mine ? std::min<int64_t>(wt, b) : 0;
     // the owner of panel k+1 runs its tournament concurrently (dist.py's side
     // stream): leave it a few SMs, as the single-GPU schedule's deferred update does
-    if (wt > wh2)
+    if (wt > wh2) {
+      // chain-bound next panel: GPC-sized clusters, one GPC left to the
+      // tournament's latency-engine clusters (as caluprrp_enqueue does)
+      const bool cb = next_mine && calu_chain_bound(w.m, w.n, w.b, k + 1, w.P == 0);
+      tl_schur_cluster = cb ? 16 : 0;
       schur_update(w.A + (col0 + bj) * w.lda + t0 + wh2, w.lda, Lp, ldk, w.a12 + wh2, w.lda12, rows - bj, wt - wh2,
-                   bj, st, s, dist_tail_ctas());
+                   bj, st, s, cb ? 16 * std::max(1, caps().schur_clusters16 - 1) : dist_tail_ctas());
+      tl_schur_cluster = 0;
+    }
   }
   CU_TRY(cudaGetLastError());
 }
