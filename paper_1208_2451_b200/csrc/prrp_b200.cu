@@ -815,6 +815,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
     static const bool late_c = !getenv("PRRP_SCHUR_LATE_C") || atoi(getenv("PRRP_SCHUR_LATE_C")) != 0;
     static const bool wsc = !getenv("PRRP_SCHUR_WSC") || atoi(getenv("PRRP_SCHUR_WSC")) != 0;
+    static const int ws_exp = getenv("PRRP_WS_EXP") ? (atoi(getenv("PRRP_WS_EXP")) & 16) : 0;   // diagnostics
     if (wsc && vec_ok && static_claims && quantum <= 0) {
       // C staged through shared memory by TMA (read early, registers free)
       const CUtensorMap mapC = make_map(C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, SCH_BM);
@@ -845,7 +846,7 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
       schur_ws_kernel<false><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K,
                                                                            vec_ok, st, ctr,
                                                                            quantum > 0 ? quantum : INT_MAX,
-                                                                           stream_c ? 1 : 0);
+                                                                           (stream_c ? 1 : 0) | ws_exp);
     else
     schur_ws_kernel<true><<<grid, SW_THREADS, sizeof(SchurWSmem), s>>>(mapL, mapB, C, ldc, (int)M, (int)N, K, vec_ok, st,
                                                                  ctr, quantum > 0 ? quantum : INT_MAX,

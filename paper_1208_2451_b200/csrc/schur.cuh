@@ -53,6 +53,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "@!P1 bra WAIT_%=;\n"
       "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// Consumer release of a TMA stage.  The arrive must not be issued while the stage's fragment loads
+// are still in flight: ptxas hoists a plain arrive above the DMMAs that consume the loads, directly
+// behind the last LDS, and on B200 the SYNCS arrive can then overtake those LDS when the LSU is
+// congested (other warps' C traffic) -- the producer's next TMA write lands first and the warp reads
+// the NEXT tile's fragment (measured: 8 x 32 strips wrong in 4-15% of runs of the epilogue-read
+// kernel, tools/schur_determinism.py; DESIGN 4).  `dep` ORs the high words of the stage's last
+// fragment loads (LDS complete in order per warp) and `opaque_zero` is a run-time 0 the compiler
+// cannot fold, so the arrive's address carries a true register dependency on the loaded data.
+__device__ __forceinline__ void mbar_arrive_after(unsigned long long* bar, uint32_t dep, uint32_t opaque_zero) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar) + (dep & opaque_zero)) : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -104,6 +115,7 @@ schur_dmma_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constan
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc % SCH_STAGES;
     mbar_wait(&S.full[s], (kc / SCH_STAGES) & 1);
+    uint32_t dep = 0;
     const double* sa = S.a[s];
     const double* sb = S.b[s];
 #pragma unroll
@@ -113,13 +125,17 @@ schur_dmma_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constan
       for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SCH_KC + k4 + fr) * 8 + fc];
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SCH_KC + k4 + fr) * 8 + fc];
+      if (k4 == SCH_KC - 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dep |= (uint32_t)__double2hiint(af[i]) | (uint32_t)__double2hiint(bf[i]);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (lane == 0) mbar_arrive_after(&S.empty[s], dep, (uint32_t)(ldc >> 40));
     if (t == 0 && kc + SCH_STAGES < nk) {
       mbar_wait(&S.empty[s], (kc / SCH_STAGES) & 1);
       issue(kc + SCH_STAGES);
@@ -394,8 +410,8 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
             const int c0 = n0 + wn + j * 8 + 2 * fr;
             const double* cp = C + (int64_t)r * ldc + c0;
             if (r < M && vec_ok && c0 + 1 < N) {
-              const double2 v = stream_c ? __ldcs(reinterpret_cast<const double2*>(cp))
-                                         : __ldcg(reinterpret_cast<const double2*>(cp));
+              const double2 v = (stream_c & 1) ? __ldcs(reinterpret_cast<const double2*>(cp))
+                                               : __ldcg(reinterpret_cast<const double2*>(cp));
               cv[i][j][0] = v.x;
               cv[i][j][1] = v.y;
             } else {
@@ -417,6 +433,7 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
       for (int kc = 0; kc < nk; ++kc, ++it) {
         const int s = it % SW_ST;
         if (kc > 0) mbar_wait(&S.full[s], (it / SW_ST) & 1);
+        uint32_t dep = 0;
         const double* sa = S.a[s];
         const double* sb = S.b[s];
 #pragma unroll
@@ -426,13 +443,20 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
           for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SW_KC + k4 + fr) * 8 + fc];
 #pragma unroll
           for (int j = 0; j < 4; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
+          if (k4 == SW_KC - 4) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dep |= (uint32_t)__double2hiint(af[i]) | (uint32_t)__double2hiint(bf[i]);
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (lane == 0) {
+          if (stream_c & 16) mbar_arrive(&S.empty[s]);   // diagnostic: the plain (hoistable) arrive
+          else mbar_arrive_after(&S.empty[s], dep, (uint32_t)(ldc >> 40));
+        }
       }
       if (!PC) {
 #ifdef PRRP_SCHUR_RACECHECK
@@ -471,7 +495,7 @@ schur_ws_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant_
           const double v0 = sub_rn(cv[i][j][0], acc[i][j][0]);
           const double v1 = sub_rn(cv[i][j][1], acc[i][j][1]);
           if (vec_ok && c0 + 1 < N) {
-            if (stream_c) __stcs(reinterpret_cast<double2*>(crow + c0), make_double2(v0, v1));
+            if (stream_c & 1) __stcs(reinterpret_cast<double2*>(crow + c0), make_double2(v0, v1));
             else *reinterpret_cast<double2*>(crow + c0) = make_double2(v0, v1);
             mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
           } else {
@@ -591,6 +615,7 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
       for (int kc = 0; kc < nk; ++kc, ++it) {
         const int s = it % SWC_ST;
         if (kc > 0) mbar_wait(&S.full[s], (it / SWC_ST) & 1);
+        uint32_t dep = 0;
         const double* sa = S.a[s];
         const double* sb = S.b[s];
 #pragma unroll
@@ -600,13 +625,19 @@ schur_wsc_kernel(const __grid_constant__ CUtensorMap mapL, const __grid_constant
           for (int i = 0; i < 4; ++i) af[i] = sa[(((wm >> 3) + i) * SW_KC + k4 + fr) * 8 + fc];
 #pragma unroll
           for (int j = 0; j < NJ; ++j) bf[j] = sb[(((wn >> 3) + j) * SW_KC + k4 + fr) * 8 + fc];
+          if (k4 == SW_KC - 4) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dep |= (uint32_t)__double2hiint(af[i]);
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) dep |= (uint32_t)__double2hiint(bf[j]);
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (lane == 0) mbar_arrive_after(&S.empty[s], dep, (uint32_t)(ldc >> 40));
       }
       mbar_wait(&S.cfull, ntile & 1);
 #pragma unroll
