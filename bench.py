@@ -260,7 +260,7 @@ def roofline_from_timing(tms, pk, what):
     flops = tms[0].schur_flops
     achieved = flops / (schur_ms * 1e-3) / 1e12
     breakdown = {k: round(statistics.mean(t.ms[i] for t in tms), 3) for i, k in enumerate(_lib.KCLASSES)}
-    return {"bound": "tensor", "kernel": "schur_wsc_kernel / schur_dmma_kernel (DMMA.8x8x4, TMA-fed)",
+    return {"bound": "tensor", "kernel": "schur_ws_kernel / schur_dmma_kernel (DMMA.8x8x4, TMA-fed)",
             "achieved": achieved, "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk if pk else None,
             "peak_source": "measured live: register-resident mma.sync.m8n8k4.f64 on all SMs, 1.5 s "
                            "(prrp_b200_dmma_peak; MEASURED_PEAKS.json has no FP64 entry)",

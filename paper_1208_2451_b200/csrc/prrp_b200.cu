@@ -814,7 +814,9 @@ void schur_update(double* C, int64_t ldc, const double* L, int64_t ldl, const do
     // keep two k-steps of fragments in flight (83% vs 74% of the DMMA peak at
     // 32640^2 x 128); PRRP_SCHUR_LATE_C=0 prefetches C into registers instead
     static const bool late_c = !getenv("PRRP_SCHUR_LATE_C") || atoi(getenv("PRRP_SCHUR_LATE_C")) != 0;
-    static const bool wsc = !getenv("PRRP_SCHUR_WSC") || atoi(getenv("PRRP_SCHUR_WSC")) != 0;
+    // PRRP_SCHUR_WSC=1: C staged through shared memory by TMA (the default until the ring's
+    // release hazard was fixed, DESIGN 4 "Determinism"; the epilogue read is 1.7% faster on config 5)
+    static const bool wsc = getenv("PRRP_SCHUR_WSC") && atoi(getenv("PRRP_SCHUR_WSC")) != 0;
     static const int ws_exp = getenv("PRRP_WS_EXP") ? (atoi(getenv("PRRP_WS_EXP")) & 16) : 0;   // diagnostics
     if (wsc && vec_ok && static_claims && quantum <= 0) {
       // C staged through shared memory by TMA (read early, registers free)
@@ -1549,7 +1551,7 @@ bool calu_chain_bound(int64_t m, int64_t n, int b, int pnl, bool flat) {
 
 void caluprrp_enqueue(double* A, int64_t lda, int64_t m, int64_t n, int b, double tau, int P, int64_t* perm,
                       cudaStream_t s, Arena& ar, CaluOut& out) {
-  static const bool calu_late_c = getenv("PRRP_CALU_LATE_C") && atoi(getenv("PRRP_CALU_LATE_C")) != 0;
+  static const bool calu_late_c = !getenv("PRRP_CALU_LATE_C") || atoi(getenv("PRRP_CALU_LATE_C")) != 0;
   tl_schur_prefetch_c = !calu_late_c;
   struct ResetPf { ~ResetPf() { tl_schur_prefetch_c = false; } } reset_pf;
   const int npanels = (int)((n + b - 1) / b);
